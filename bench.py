@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- weighted-minhash signatures/sec (row x hash) on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--algo auto]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+    python bench.py --impl reference ...      # the CPU oracle, timed on the host cores
+
+A step is one wmh_hash launch over this rank's resident rows (all of §8(a)'s
+hot-path rows a5-a9; a1-a4 -- column max, the NCCL max exchange, prefix sums,
+IntToComp -- run once before timing, as the paper's "one time pre-processing",
+P:276).  Scaling is weak: every rank hashes its own N-row shard of one
+dataset (rows r*N .. (r+1)*N-1 of the chunk-seeded generator), so the work
+per GPU is fixed as N grows; the only collective is the max exchange in
+prepare.  Timing: CUDA events on the launching stream around each step, an
+L2 flush (256 MiB write) between steps outside the events, barrier +
+synchronize around the K steps, max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "weighted-minhash signatures/sec (row x hash)"
+UNIT = "hashes/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c2", help="c1..c5 (default c2: the metric's workload, configs[1])")
+    p.add_argument("--rows", type=int, default=None, help="rows per GPU (default: the config's N)")
+    p.add_argument("--algo", default="auto", choices=["auto", "simple", "tiled"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------- workload
+def workload(cfg_name: str, rank: int, n_rows: int | None):
+    import datagen
+    cfg = datagen.CONFIGS[cfg_name]
+    n = cfg.n_rows if n_rows is None else n_rows
+    lo, hi = rank * n, (rank + 1) * n
+    if cfg_name == "c2":
+        data = datagen.Dense(datagen.gen_c2_rows(cfg.data_seed, lo, hi, cfg.dim))
+    elif cfg_name == "c1":
+        data = datagen.Dense(datagen.gen_counter_c1_rows(cfg.data_seed, np.arange(lo, hi), cfg.dim))
+    elif cfg_name == "c5":
+        data = datagen.Dense(datagen.gen_counter_c5_rows(cfg.data_seed, np.arange(lo, hi), cfg.dim))
+    else:
+        _, full = datagen.make(cfg_name, n_rows=hi)
+        data = full.take(np.arange(lo, hi))
+    return cfg, n, data
+
+
+def desc(cfg, n):
+    return (f"{cfg.name}: N={n} rows/GPU, D={cfg.dim}, {cfg.kind} uint8, k={cfg.k}, cap={cfg.cap}, "
+            f"uint{8 * cfg.sig_bytes} signatures, seed={cfg.seed}")
+
+
+def expected_draws(x_sum: np.ndarray, M: int, k: int, cap: int) -> float:
+    """sum_n k * E_n with E_n = (1 - (1 - s_n)^cap) / s_n (Theorem 2 capped, reading R9)."""
+    s = x_sum.astype(np.float64) / M
+    e = np.where(s > 0, -np.expm1(cap * np.log1p(-np.minimum(s, 1 - 1e-300))) / np.maximum(s, 1e-300), cap)
+    e = np.where(s >= 1, 1.0, e)
+    return float(k * e.sum())
+
+
+def row_sums(data):
+    import datagen
+    if isinstance(data, datagen.Dense):
+        return data.x.sum(axis=1, dtype=np.int64)
+    return np.add.reduceat(data.val.astype(np.int64), data.row_ptr[:-1]) * (np.diff(data.row_ptr) > 0) \
+        if len(data.val) else np.zeros(data.n_rows, np.int64)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML clock / throttle-reason sampling in a thread (every ~5 ms)."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int):
+        self.samples = []
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:                      # noqa: BLE001
+            self.err = repr(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, rs))
+            except Exception:                       # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "note": getattr(self, "err", "no samples")}
+        mhz = [m for m, _ in self.samples]
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        reasons = [n for b, n in self.REASONS.items() if bits & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(mhz), "sm_mhz_min": min(mhz)}
+
+
+# ------------------------------------------------------------- CPU oracle leg
+def oracle_rate(cfg, data, M_bounds, seconds: float):
+    """Time the oracle (as it stands) on a bounded row sample of the same
+    workload, on all host cores; returns (hashes/s, cores, sample description)."""
+    import datagen
+    import oracle
+    L = oracle.Layout(M_bounds)
+    cores = os.cpu_count() or 1
+    n = data.n_rows
+
+    def run(rows):
+        if isinstance(data, datagen.Dense):
+            x = np.ascontiguousarray(data.x[rows])
+            t0 = time.perf_counter()
+            L.hash_dense(x, cfg.seed, cfg.k, cfg.cap, threads=cores)
+        else:
+            sub = data.take(rows)
+            t0 = time.perf_counter()
+            L.hash_csr(sub.row_ptr, sub.col, sub.val, cfg.seed, cfg.k, cfg.cap, threads=cores)
+        return time.perf_counter() - t0
+
+    rng = np.random.default_rng(2024)
+    probe = np.sort(rng.choice(n, size=min(n, max(cores, 16)), replace=False))
+    dt = run(probe)
+    per_row = dt / len(probe) * cores / max(1, min(cores, len(probe)))
+    want = int(min(n, max(len(probe), seconds / max(per_row, 1e-9))))
+    rows = np.sort(rng.choice(n, size=want, replace=False))
+    dt = run(rows)
+    rate = len(rows) * cfg.k / dt
+    return rate, cores, f"{len(rows)} of {n} rows (seeded uniform sample), all k={cfg.k} hashes, {dt:.1f} s"
+
+
+def layout_bounds(cfg, data):
+    import datagen
+    if cfg.fixed_bound is not None:
+        return np.full(data.dim, cfg.fixed_bound, np.uint32)
+    if isinstance(data, datagen.Dense):
+        return data.x.max(axis=0).astype(np.uint32)
+    m = np.zeros(data.dim, np.uint32)
+    np.maximum.at(m, data.col, data.val.astype(np.uint32))
+    return m
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, n, data = workload(args.config, 0, args.rows)
+    bounds = layout_bounds(cfg, data)
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r, cores, sample = oracle_rate(cfg, data, bounds, per_step)
+        if i >= args.warmup:
+            rates.append(r)
+    value = statistics.mean(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": desc(cfg, n), "parallelism": "host threads (rank 0 only)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    from paper_1602_08393_b200 import build
+    build.build()
+    import paper_1602_08393_b200 as wmh
+
+    cfg, n, data = workload(args.config, rank, args.rows)
+    # inputs resident in HBM before the timed region
+    import datagen
+    if isinstance(data, datagen.Dense):
+        rows = wmh.Rows.from_dense(torch.from_numpy(data.x).to(dev))
+        in_bytes = data.x.nbytes
+    else:
+        rows = wmh.Rows.from_csr(torch.from_numpy(data.row_ptr).to(dev), torch.from_numpy(data.col).to(dev),
+                                 torch.from_numpy(data.val).to(dev), data.dim)
+        in_bytes = data.row_ptr.nbytes + data.col.nbytes + data.val.nbytes
+    if cfg.fixed_bound is not None:
+        layout = wmh.prepare(rows, bounds=torch.full((data.dim,), cfg.fixed_bound, dtype=torch.uint32, device=dev))
+    else:
+        layout = wmh.prepare(rows)          # colmax + NCCL all-reduce(MAX) when world > 1
+    M = layout.M
+    sig = torch.empty((n, cfg.k), dtype=torch.uint8 if cfg.sig_bytes == 1 else torch.uint16, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig)
+
+    clocks = ClockSampler(dev.index if world == 1 else local)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in evs:
+        flush.zero_()                        # L2 flush outside the timed events
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max_ms = float(t.item())
+    hashes_per_step_total = n * cfg.k * world
+    value = hashes_per_step_total * args.steps / (t_max_ms / 1e3)
+    ms_per_step = t_max_ms / args.steps
+
+    # ---- roofline of the dominant (only) kernel of the step
+    x_sum = row_sums(data)
+    draws = expected_draws(x_sum, M, cfg.k, cfg.cap)      # this rank's algorithmic draw-tests per launch
+    kern_s = (t_ms / args.steps) / 1e3
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:                                      # noqa: BLE001
+        pass
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    roof = roofline(args.algo, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
+
+    # ---- e2e: the public host-buffer API, H2D rows + hash + D2H signatures every step
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r, cores, sample = oracle_rate(cfg, data, layout_bounds(cfg, data), args.cpu_seconds)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": desc(cfg, n), "global_rows": n * world, "k": cfg.k, "M": M,
+                       "algo": args.algo, "parallelism": f"rows sharded x{world}, no collective in the step",
+                       "l2": "flushed between steps (256 MiB write outside the timed events); "
+                             f"inputs {in_bytes / 2**20:.0f} MiB + signatures "
+                             f"{sig.numel() * sig.element_size() / 2**20:.0f} MiB per step",
+                       "expected_draws_per_step": draws * world},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": args.steps * 1,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# Lane-instructions per draw-test of the dominant kernel's minimal sequence,
+# counted from SASS.  SIMPLE: RNG + range reduction + packed
+# lookup + row lookup + compare + loop, per (row, draw).
+I_DRAW = {"simple": 30.0}
+
+
+def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
+    issue = n_sm * 4 * 32 * sm_mhz * 1e6            # lane-instructions / s at the max SM clock
+    i_draw = I_DRAW.get(algo, I_DRAW["simple"])
+    peak = issue / i_draw / 1e9                     # Gdraw-tests / s
+    achieved = draws / kern_s / 1e9
+    hbm = peaks.get("hbm_gbs", 6545.6)
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gdraws/s", "frac": achieved / peak,
+            "traffic": None, "peak_source": f"{n_sm} SMs x 128 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) "
+                                            f"/ {i_draw:.0f} lane-instr per draw",
+            "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3, "t_kernel_ms": kern_s * 1e3}
+
+
+def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist):
+    import datagen
+    import torch
+    if isinstance(data, datagen.Dense):
+        hx = torch.from_numpy(data.x).pin_memory()
+        hrows = wmh.Rows.from_dense(hx)
+        h2d = hx.numel()
+    else:
+        rp = torch.from_numpy(data.row_ptr).pin_memory()
+        col = torch.from_numpy(data.col).pin_memory()
+        val = torch.from_numpy(data.val).pin_memory()
+        hrows = wmh.Rows.from_csr(rp, col, val, data.dim)
+        h2d = rp.numel() * 8 + col.numel() * 4 + val.numel()
+    out = torch.empty((n, cfg.k), dtype=torch.uint8 if cfg.sig_bytes == 1 else torch.uint16).pin_memory()
+    for _ in range(2):
+        wmh.hash_host(layout, hrows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, out=out)
+    steps = max(1, min(args.steps, 5))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        wmh.hash_host(layout, hrows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, out=out)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    return {"value": n * cfg.k * world * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(out.numel() * out.element_size()), "steps": steps,
+            "api": "wmh_hash_host (pinned host rows -> H2D -> hash -> D2H signatures, synchronised)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,178 @@
+/*
+ * wmh.h -- C ABI of libwmh.so: B200 (sm_100a) rejection-sampling weighted
+ * minwise hashing (Shrivastava, "Exact Weighted Minwise Hashing in Constant
+ * Time", ICML 2016, arXiv 1602.08393).
+ *
+ * Citations are PAPER.md line numbers "P:n" with the section / equation /
+ * algorithm they fall in; readings R1..R16 are listed in DESIGN.md §2.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Plain C types only.  Every array argument is a DEVICE pointer owned by
+ *    the caller (typically a torch tensor) unless the name says _host.  The
+ *    library never frees caller memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls are asynchronous and stream-ordered; the only
+ *    host<->device synchronisations are the ones a function documents.
+ *  - Every call returns a wmh_status.  On failure a human-readable message is
+ *    available from wmh_last_error() (thread-local, valid until the next
+ *    call on the same thread).  Arguments are validated before any launch;
+ *    an invalid call launches nothing and leaves outputs untouched.
+ *  - Weights are integers x in {0..255} (uint8).  The paper quantises to
+ *    integer bounds m_i = ceil(max) (Sec. 3.1); real-valued inputs
+ *    must be scaled and quantised by the caller (Sec. 4).
+ *  - There is no CPU fallback: without a CUDA device every compute call
+ *    fails with WMH_ECUDA.
+ */
+#ifndef WMH_H
+#define WMH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    WMH_OK = 0,
+    WMH_EINVAL = 1,    /* an argument is out of its documented domain            */
+    WMH_EBOUND = 2,    /* a weight exceeds its bound m_c (row, col in last_error) */
+    WMH_EEMPTY = 3,    /* M = sum m_c = 0: no cell exists to draw from            */
+    WMH_EOVERFLOW = 4, /* M >= 2^32: cells are indexed by uint32                  */
+    WMH_ECUDA = 5,     /* CUDA runtime / launch failure (or no device)            */
+    WMH_ENOMEM = 6     /* device allocation failed                                */
+} wmh_status;
+
+typedef enum { WMH_DENSE = 0, WMH_CSR = 1 } wmh_kind;
+
+/* A batch of non-negative integer vectors x (Sec. 2: "x_i >= 0").
+ *  kind = WMH_DENSE: `dense` is n_rows x dim uint8, row-major, row n at
+ *                    dense + n*dim.  row_ptr/col/val are ignored.
+ *  kind = WMH_CSR:   row_ptr (int64, n_rows+1, row_ptr[0] = 0,
+ *                    non-decreasing), col (int32, nnz, strictly ascending
+ *                    within a row, 0 <= col < dim), val (uint8, nnz, > 0);
+ *                    nnz must equal row_ptr[n_rows] (host copy of it, so the
+ *                    library need not read it back).  Explicit zeros are
+ *                    allowed but wasteful.
+ * n_rows may be 0 (every call is then a no-op returning WMH_OK). */
+typedef struct {
+    int32_t kind;
+    int64_t n_rows;
+    int64_t dim;
+    const uint8_t *dense;
+    const int64_t *row_ptr;
+    const int32_t *col;
+    const uint8_t *val;
+    int64_t nnz;
+} wmh_rows;
+
+/* Opaque, immutable red-green layout (Eq. 4; Alg. 4).
+ * Owned by the library; share it read-only across streams and threads;
+ * free it with wmh_layout_free after all work using it has completed. */
+typedef struct wmh_layout wmh_layout;
+
+/* ---- a1: column maxima --------------------------------------------------
+ * colmax[c] = max_n x[n][c] over the given rows (the per-coordinate bound m_i
+ * "computed (estimated) while reading the data").
+ * colmax: device uint32[dim], fully overwritten.  Multi-GPU callers reduce
+ * the per-rank results with an all-reduce(MAX) / all-gather + max before
+ * wmh_prepare so that M, and hence every draw, is identical on every rank
+ * (the random sequence must be consistent across vectors).
+ * Errors: EINVAL (null pointers, dim < 1, n_rows < 0, bad kind), ECUDA. */
+wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *stream);
+
+/* ---- a3 + a4: prefix sums and Alg. 4 ComputeHashMaps --------------------
+ * Builds CompToM[c] = sum_{i<c} m_i (Eq. 3; exclusive prefix, interval
+ * c = [CompToM[c], CompToM[c+1]), reading R3) and IntToComp[t] = c for every
+ * integer cell t of interval c (Alg. 4; M cells, reading R4).
+ * Components with m_c = 0 get no cells (reading R11).
+ *   bounds: device uint32[dim], every m_c <= 255 (weights are uint8);
+ *           copied, so the caller may free it after the call returns.
+ *   rows:   optional (may be NULL).  When given, every weight is checked
+ *           against its bound (and CSR structure is validated); the first
+ *           offender is reported as WMH_EBOUND / WMH_EINVAL.
+ * Synchronises `stream` once to read back M (8 bytes) and the checks.
+ * Errors: EINVAL (null, dim < 1, a bound > 255, malformed CSR), EBOUND,
+ *         EEMPTY (M = 0), EOVERFLOW (M >= 2^32), ENOMEM, ECUDA. */
+wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh_rows *rows, wmh_layout **out,
+                       void *stream);
+
+/* Layout facts (host values): dim, M, flags (bit 0: every m_c equal, so
+ * IntToComp is the division r / m), the uniform bound (0 if not uniform). */
+wmh_status wmh_layout_info(const wmh_layout *layout, int64_t *dim, uint64_t *M, uint32_t *flags,
+                           uint32_t *uniform_bound);
+
+/* Read-only DEVICE views of the layout's tables, for tests: comp_to_m
+ * (uint32[dim+1]), int_to_comp (uint32[M]), bounds (uint32[dim]). */
+wmh_status wmh_layout_tables(const wmh_layout *layout, const uint32_t **comp_to_m,
+                             const uint32_t **int_to_comp, const uint32_t **bounds);
+
+void wmh_layout_free(wmh_layout *layout);
+
+/* ---- a5..a9: the hash ------------------------------------------------------
+ * sig[n][j] = h_j(x_n), j = 0..k-1, row-major n_rows x k, for every row:
+ *   S   = splitmix64(seed)                                   (reading R7)
+ *   r_t = floor(splitmix64(S ^ (j << 32) ^ t) * M / 2^64)     (R6, R8)
+ *   c   = IntToComp[r_t];  green iff r_t - CompToM[c] < x_c  (Alg. 5, P:297-316;
+ *                                                             R1, R2)
+ *   h   = t + 1 for the first green t < cap, else cap         (Alg. 3, P:158-180;
+ *                                                             Def.; R9)
+ * Draws depend only on (seed, j, t, M) -- never on x (the consistency of
+ * P:190-191) -- so rows may be sharded across GPUs freely.  An all-zero row
+ * yields cap for every j (reading R12).
+ *   rows must satisfy x <= bounds of `layout` (checked by wmh_prepare when
+ *        given rows; NOT re-checked here) and rows->dim == layout dim.
+ *   k >= 1; 1 <= cap <= 2^(8*sig_bytes) - 1; sig_bytes in {1, 2}.
+ *   sig_out: device, n_rows*k*sig_bytes bytes (uint8 or uint16 values).
+ *   n_saturated: optional device uint64, INCREMENTED (not overwritten) by
+ *        the number of (row, j) that reached the cap without a green draw.
+ * Output is bit-identical to the CPU oracle for the same inputs.
+ * Errors: EINVAL, ENOMEM (scratch), ECUDA. */
+wmh_status wmh_hash(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
+                    int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, void *stream);
+
+/* Kernel selection for tests and benchmarks (all variants are bit-identical). */
+typedef enum {
+    WMH_ALGO_AUTO = 0,   /* pick per input (the default used by wmh_hash)         */
+    WMH_ALGO_SIMPLE = 1, /* one thread per (row, j), global-table lookups         */
+    WMH_ALGO_TILED = 2   /* rows staged in shared memory, draws shared by a tile  */
+} wmh_algo;
+
+typedef struct {
+    int32_t algo;        /* wmh_algo */
+    int32_t reserved[7]; /* must be zero */
+} wmh_hash_opts;
+
+wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k,
+                       uint32_t cap, int32_t sig_bytes, void *sig_out, uint64_t *n_saturated,
+                       const wmh_hash_opts *opts, void *stream);
+
+/* End-to-end convenience (the e2e path): rows and signatures in HOST memory
+ * (pinned or pageable).  Copies the rows host->device into library scratch
+ * (kept across calls and grown on demand, one per thread), runs wmh_hash on
+ * `stream`, copies the signatures device->host and synchronises `stream`.
+ * rows_host uses the wmh_rows layout with HOST pointers.  Errors: as wmh_hash. */
+wmh_status wmh_hash_host(const wmh_layout *layout, const wmh_rows *rows_host, uint64_t seed, uint32_t k,
+                         uint32_t cap, int32_t sig_bytes, void *sig_out_host, void *stream);
+
+/* ---- a10: signature agreement (Eq. 14-15) -----------------------
+ * matches[p] = #{ j : sig[a_p][j] == sig[b_p][j] } for pairs[p] = (a_p, b_p)
+ * (device int64[n_pairs][2]); optional jhat[p] = matches[p] / k as an IEEE
+ * round-to-nearest float (J-hat of Eq. 14).  sig is n_rows x k of sig_bytes.
+ * Pair indices must lie in [0, n_rows): out-of-range pairs get matches = 0
+ * and jhat = NaN, and the call returns WMH_EINVAL after synchronising
+ * `stream` once to count them (only when check_pairs != 0).
+ * Errors: EINVAL, ECUDA. */
+wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k, int64_t n_rows, const int64_t *pairs,
+                       int64_t n_pairs, uint32_t *matches, float *jhat, int32_t check_pairs, void *stream);
+
+/* Thread-local description of the last failure ("" if none). */
+const char *wmh_last_error(void);
+
+/* Library version string, e.g. "wmh 0.1 sm_100a". */
+const char *wmh_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WMH_H */

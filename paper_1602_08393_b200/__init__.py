@@ -1,0 +1,222 @@
+"""B200-native rejection-sampling weighted minwise hashing (arXiv 1602.08393).
+
+Thin Python binding over the C ABI of ``libwmh.so`` (``include/wmh.h``):
+argument marshalling only -- every step of the hot path runs in the sm_100a
+kernels.  PyTorch is used for device memory, streams and ``torch.distributed``
+(the cross-GPU maxima exchange in :func:`prepare`).  There is no CPU fallback:
+every compute call raises if the extension or a CUDA device is missing.
+
+    rows   = Rows.from_dense(x_uint8_cuda)          # or Rows.from_csr(row_ptr, col, val, dim)
+    layout = prepare(rows)                          # a1-a4 (+ NCCL max over `group`)
+    sig    = hash(layout, rows, seed=1, k=500, cap=65535)      # a5-a9
+    m, j   = collide(sig, pairs)                    # a10 (Eq. 14)
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import WmhError  # noqa: F401
+
+__all__ = ["Rows", "Layout", "colmax", "prepare", "hash", "hash_host", "collide", "WmhError", "version"]
+
+
+def _stream(stream=None) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _need_cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+@dataclass
+class Rows:
+    """A batch of vectors x >= 0 with uint8 weights, dense or CSR."""
+    kind: int
+    n_rows: int
+    dim: int
+    dense: torch.Tensor | None = None
+    row_ptr: torch.Tensor | None = None
+    col: torch.Tensor | None = None
+    val: torch.Tensor | None = None
+    nnz: int = 0
+
+    @staticmethod
+    def from_dense(x: torch.Tensor) -> "Rows":
+        if x.dtype != torch.uint8 or x.dim() != 2:
+            raise ValueError("dense rows must be a 2-D uint8 tensor")
+        return Rows(_lib.WMH_DENSE, x.shape[0], x.shape[1], dense=x)
+
+    @staticmethod
+    def from_csr(row_ptr: torch.Tensor, col: torch.Tensor, val: torch.Tensor, dim: int) -> "Rows":
+        if row_ptr.dtype != torch.int64 or col.dtype != torch.int32 or val.dtype != torch.uint8:
+            raise ValueError("CSR rows need row_ptr int64, col int32, val uint8")
+        return Rows(_lib.WMH_CSR, row_ptr.numel() - 1, int(dim), row_ptr=row_ptr, col=col, val=val,
+                    nnz=col.numel())
+
+    def _c(self, device: bool = True) -> _lib.WmhRows:
+        for name in ("dense", "row_ptr", "col", "val"):
+            t = getattr(self, name)
+            if t is not None and device:
+                _need_cuda(t, name)
+        return _lib.WmhRows(self.kind, self.n_rows, self.dim,
+                            None if self.dense is None else self.dense.data_ptr(),
+                            None if self.row_ptr is None else self.row_ptr.data_ptr(),
+                            None if self.col is None else self.col.data_ptr(),
+                            None if self.val is None else self.val.data_ptr(), self.nnz)
+
+    def slice(self, begin: int, end: int) -> "Rows":
+        """Rows [begin, end) as a view (dense) or a re-based copy of row_ptr (CSR)."""
+        if self.kind == _lib.WMH_DENSE:
+            return Rows.from_dense(self.dense[begin:end])
+        rp = self.row_ptr[begin:end + 1]
+        a = int(rp[0].item())
+        b = int(rp[-1].item())
+        return Rows.from_csr((rp - a).contiguous(), self.col[a:b], self.val[a:b], self.dim)
+
+
+
+class _CudaArray:
+    """Zero-copy view of a library-owned device array (read-only)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, True), "version": 3}
+
+
+class Layout:
+    """The red-green layout: bounds m_c, CompToM (Eq. 3) and IntToComp (Alg. 4)."""
+
+    def __init__(self, handle: int, keepalive=None):
+        self._h = ctypes.c_void_p(handle)
+        dim, M, flags, ub = ctypes.c_int64(), ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
+        _lib.check(_lib.load().wmh_layout_info(self._h, ctypes.byref(dim), ctypes.byref(M), ctypes.byref(flags),
+                                               ctypes.byref(ub)))
+        self.dim, self.M, self.flags, self.uniform_bound = dim.value, M.value, flags.value, ub.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def tables(self):
+        """(comp_to_m[D+1], int_to_comp[M], bounds[D]) as read-only uint32 CUDA tensors (views)."""
+        c2m, i2c, b = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(_lib.load().wmh_layout_tables(self._h, ctypes.byref(c2m), ctypes.byref(i2c), ctypes.byref(b)))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        mk = lambda p, n: torch.as_tensor(_CudaArray(p.value, n, "<u4"), device=dev)  # noqa: E731
+        return mk(c2m, self.dim + 1), mk(i2c, self.M), mk(b, self.dim)
+
+    def close(self):
+        if self._h:
+            torch.cuda.synchronize()
+            _lib.load().wmh_layout_free(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            if self._h and self._h.value:
+                _lib.load().wmh_layout_free(self._h)
+        except Exception:
+            pass
+
+
+def colmax(rows: Rows, stream=None) -> torch.Tensor:
+    """a1: per-column maxima of `rows` (uint32 [D] on the rows' device)."""
+    dev = (rows.dense if rows.dense is not None else rows.col).device
+    out = torch.empty(rows.dim, dtype=torch.uint32, device=dev)
+    _lib.check(_lib.load().wmh_colmax(ctypes.byref(rows._c()), _ptr(out), _stream(stream)))
+    return out
+
+
+def prepare(rows: Rows | None = None, bounds: torch.Tensor | None = None, group=None, validate: bool = True,
+            stream=None) -> Layout:
+    """a1-a4.  Without `bounds`, m_c is the column max of `rows`, reduced with an
+    all-reduce(MAX) over the torch.distributed `group` (None = the default group
+    when a multi-rank job is initialised; False = no reduction).  That is the
+    only collective of the path: it makes M -- hence every draw -- identical on
+    every rank."""
+    if bounds is None:
+        if rows is None:
+            raise ValueError("prepare needs rows or bounds")
+        bounds = colmax(rows, stream)
+        dist = torch.distributed
+        world = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        if group is not False and (group is not None or world):
+            b32 = bounds.view(torch.int32)            # values <= 255: same bits; NCCL-friendly dtype
+            dist.all_reduce(b32, op=dist.ReduceOp.MAX, group=group)
+    else:
+        _need_cuda(bounds, "bounds")
+        if bounds.dtype not in (torch.uint32, torch.int32):
+            raise ValueError("bounds must be uint32/int32")
+    h = ctypes.c_void_p()
+    crows = ctypes.byref(rows._c()) if (rows is not None and validate) else None
+    _lib.check(_lib.load().wmh_prepare(_ptr(bounds), bounds.numel(), crows, ctypes.byref(h), _stream(stream)))
+    return Layout(h.value)
+
+
+def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
+         algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
+         stream=None) -> torch.Tensor:
+    """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16)."""
+    if sig_bytes is None:
+        sig_bytes = 1 if cap <= 255 else 2
+    dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
+    dev = (rows.dense if rows.dense is not None else rows.row_ptr).device
+    if out is None:
+        out = torch.empty((rows.n_rows, k), dtype=dtype, device=dev)
+    elif out.dtype != dtype or out.numel() != rows.n_rows * k:
+        raise ValueError("out has the wrong dtype or size")
+    if n_saturated is not None and (n_saturated.dtype not in (torch.int64, torch.uint64) or not n_saturated.is_cuda):
+        raise ValueError("n_saturated must be a CUDA int64 tensor")
+    opts = _lib.WmhHashOpts(_lib.ALGOS[algo])
+    _lib.check(_lib.load().wmh_hash_ex(layout.handle, ctypes.byref(rows._c()), seed & (2**64 - 1), k, cap, sig_bytes,
+                                       _ptr(out), _ptr(n_saturated), ctypes.byref(opts), _stream(stream)))
+    return out
+
+
+def hash_host(layout: Layout, rows_host, seed: int, k: int, cap: int, sig_bytes: int | None = None,
+              out: np.ndarray | torch.Tensor | None = None, stream=None):
+    """End-to-end through the C ABI with HOST buffers (wmh_hash_host): H2D of the
+    rows, the hash, D2H of the signatures, synchronised.  `rows_host` is a Rows
+    of CPU tensors (pinned for full PCIe speed)."""
+    if sig_bytes is None:
+        sig_bytes = 1 if cap <= 255 else 2
+    dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
+    if out is None:
+        out = torch.empty((rows_host.n_rows, k), dtype=dtype)
+    c = rows_host._c(device=False)
+    _lib.check(_lib.load().wmh_hash_host(layout.handle, ctypes.byref(c), seed & (2**64 - 1), k, cap, sig_bytes,
+                                         ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+    return out
+
+
+def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, stream=None):
+    """a10: (matches uint32 [P], jhat float32 [P]) with jhat = matches / k (Eq. 14)."""
+    _need_cuda(sig, "sig")
+    _need_cuda(pairs, "pairs")
+    if pairs.dtype != torch.int64:
+        raise ValueError("pairs must be int64 [P, 2]")
+    sb = sig.element_size()
+    n_rows, k = sig.shape
+    P = pairs.numel() // 2
+    matches = torch.empty(P, dtype=torch.uint32, device=sig.device)
+    jhat = torch.empty(P, dtype=torch.float32, device=sig.device)
+    _lib.check(_lib.load().wmh_collide(_ptr(sig), sb, k, n_rows, _ptr(pairs), P, _ptr(matches), _ptr(jhat),
+                                       1 if check_pairs else 0, _stream(stream)))
+    return matches, jhat
+
+
+def version() -> str:
+    return _lib.load().wmh_version().decode()

@@ -1,0 +1,83 @@
+// common.cuh -- internal declarations shared by the libwmh.so translation units.
+// Product code (CUDA path).  Shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "wmh.h"
+
+struct wmh_layout {
+    int64_t dim = 0;
+    uint64_t M = 0;
+    uint32_t flags = 0;          // bit 0: uniform bounds
+    uint32_t uniform_m = 0;      // the common bound when uniform, else 0
+    uint32_t *bounds = nullptr;       // [dim]
+    uint32_t *comp_to_m = nullptr;    // [dim + 1]   CompToM, exclusive prefix (Eq. 3)
+    uint32_t *int_to_comp = nullptr;  // [M]         IntToComp (Alg. 4)
+    uint32_t *cell_pack = nullptr;    // [M]         (c << 8) | (t - CompToM[c]): Alg. 5 in one load
+    int device = 0;
+};
+
+#define WMH_LAYOUT_UNIFORM 1u
+
+namespace wmh {
+
+// ----------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+wmh_status cuda_fail(cudaError_t e, const char *what);
+#define WMH_CUDA_TRY(expr, what)                                  \
+    do {                                                          \
+        cudaError_t _e = (expr);                                  \
+        if (_e != cudaSuccess) return ::wmh::cuda_fail(_e, what); \
+    } while (0)
+#define WMH_LAUNCH_CHECK(what) WMH_CUDA_TRY(cudaGetLastError(), what)
+
+wmh_status check_rows(const wmh_rows *rows, bool need_data);
+int num_sms();
+
+// ---------------------------------------------------------------- the RNG
+// Reading R6-R8: a counter-based stream.  The paper's
+// "r = M x Uniform(0,1)" (Alg. 3) with a consistent seed
+// becomes r_t = floor(splitmix64(S ^ (j<<32) ^ t) * M / 2^64), S =
+// splitmix64(seed).  SplitMix64 is the output function of Steele, Lea &
+// Flood (2014).
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t v) {
+    uint64_t z = v + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// floor(z * M / 2^64) for M < 2^32 as two 32x32->64 multiplies:
+// z*M = zh*M*2^32 + zl*M, so the top word is (zh*M + (zl*M >> 32)) >> 32.
+__device__ __forceinline__ uint32_t mulhi_range(uint64_t z, uint32_t M) {
+    uint32_t zl = (uint32_t)z, zh = (uint32_t)(z >> 32);
+    uint64_t lo = (uint64_t)zl * M;
+    uint64_t hi = (uint64_t)zh * M + (lo >> 32);
+    return (uint32_t)(hi >> 32);
+}
+
+// key_hi = hi32(S) ^ j is fixed per hash; only the low word varies with t.
+__device__ __forceinline__ uint32_t draw_r(uint64_t S, uint32_t j, uint32_t t, uint32_t M) {
+    uint64_t key = S ^ ((uint64_t)j << 32) ^ (uint64_t)t;
+    return mulhi_range(splitmix64(key), M);
+}
+
+// ------------------------------------------------------------ launchers
+struct HashArgs {
+    const wmh_layout *L;
+    wmh_rows rows;
+    uint64_t S;          // splitmix64(seed)
+    uint32_t k, cap;
+    int sig_bytes;
+    void *sig;
+    unsigned long long *n_sat;   // may be null
+    cudaStream_t stream;
+};
+
+wmh_status launch_hash_simple(const HashArgs &a);
+wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
+
+}  // namespace wmh

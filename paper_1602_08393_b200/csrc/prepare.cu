@@ -1,0 +1,366 @@
+// prepare.cu -- a1 (column maxima), bound/structure validation, a3 (prefix sums,
+// Eq. 3) and a4 (IntToComp, Alg. 4) on the device.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace wmh {
+
+// ------------------------------------------------------------ a1: colmax
+// Dense: each thread owns 16 consecutive columns (one uint4 per row) and a
+// slice of rows; per-byte max with __vmaxu4, then one atomicMax per column.
+// Reads N*D bytes once (HBM-bound).
+__global__ void colmax_dense_vec16(const uint8_t *__restrict__ x, int64_t n_rows, int64_t dim,
+                                   int64_t rows_per_slice, uint32_t *__restrict__ colmax) {
+    const int64_t nvec = dim / 16;
+    const int64_t cv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cv >= nvec) return;
+    const int64_t r0 = (int64_t)blockIdx.y * rows_per_slice;
+    const int64_t r1 = min(n_rows, r0 + rows_per_slice);
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (int64_t n = r0; n < r1; n++) {
+        uint4 v = __ldg(reinterpret_cast<const uint4 *>(x + n * dim) + cv);
+        acc.x = __vmaxu4(acc.x, v.x);
+        acc.y = __vmaxu4(acc.y, v.y);
+        acc.z = __vmaxu4(acc.z, v.z);
+        acc.w = __vmaxu4(acc.w, v.w);
+    }
+    uint32_t w[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            uint32_t v = (w[q] >> (8 * b)) & 0xFFu;
+            if (v) atomicMax(&colmax[cv * 16 + q * 4 + b], v);
+        }
+}
+
+// Generic byte path (any dim / alignment).
+__global__ void colmax_dense_bytes(const uint8_t *__restrict__ x, int64_t n_rows, int64_t dim,
+                                   int64_t rows_per_slice, uint32_t *__restrict__ colmax) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= dim) return;
+    const int64_t r0 = (int64_t)blockIdx.y * rows_per_slice;
+    const int64_t r1 = min(n_rows, r0 + rows_per_slice);
+    uint32_t m = 0;
+    for (int64_t n = r0; n < r1; n++) m = max(m, (uint32_t)x[n * dim + c]);
+    if (m) atomicMax(&colmax[c], m);
+}
+
+// CSR: one thread per nonzero; read first, atomic only when it would raise the
+// max (hot Zipf columns otherwise serialise on one address).
+__global__ void colmax_csr(const int32_t *__restrict__ col, const uint8_t *__restrict__ val, int64_t nnz,
+                           uint32_t *__restrict__ colmax) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = val[e];
+        int32_t c = col[e];
+        if (v > *((volatile uint32_t *)&colmax[c])) atomicMax(&colmax[c], v);
+    }
+}
+
+// ---------------------------------------------------------- validation
+// First offending position, as a min-reduced 64-bit key.
+__global__ void check_dense_bounds(const uint8_t *__restrict__ x, int64_t n_rows, int64_t dim,
+                                   const uint32_t *__restrict__ bounds, unsigned long long *first_bad) {
+    for (int64_t n = blockIdx.x; n < n_rows; n += gridDim.x)
+        for (int64_t c = threadIdx.x; c < dim; c += blockDim.x)
+            if (x[n * dim + c] > bounds[c]) atomicMin(first_bad, (unsigned long long)(n * dim + c));
+}
+
+// One warp per row: row_ptr monotone, columns in range and strictly
+// ascending, values within bounds.  key = (nnz index << 3) | code.
+__global__ void check_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                          const uint8_t *__restrict__ val, int64_t n_rows, int64_t dim, int64_t nnz,
+                          const uint32_t *__restrict__ bounds, unsigned long long *first_bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t n = warp; n < n_rows; n += nwarps) {
+        int64_t a = row_ptr[n], b = row_ptr[n + 1];
+        if (a > b || a < 0 || b > nnz || (n == 0 && a != 0) || (n == n_rows - 1 && b != nnz)) {
+            if (lane == 0) atomicMin(first_bad, ((unsigned long long)(a < 0 ? 0 : a) << 3) | 4ull);
+            continue;
+        }
+        for (int64_t e = a + lane; e < b; e += 32) {
+            int32_t c = col[e];
+            unsigned code = 0;
+            if (c < 0 || c >= dim) code = 1;
+            else if (e > a && col[e - 1] >= c) code = 2;
+            else if (val[e] > bounds[c]) code = 3;
+            if (code) atomicMin(first_bad, ((unsigned long long)e << 3) | code);
+        }
+    }
+}
+
+// ------------------------------------------------------- a3: prefix sums
+constexpr int SCAN_B = 1024;
+
+// Per-block sum, min and max of the bounds (u64 sums: overflow is detected, not wrapped).
+__global__ void scan_block_sums(const uint32_t *__restrict__ m, int64_t dim, unsigned long long *__restrict__ sums,
+                                unsigned int *__restrict__ mn, unsigned int *__restrict__ mx) {
+    __shared__ unsigned long long ws[SCAN_B / 32];
+    __shared__ unsigned int wmn[SCAN_B / 32], wmx[SCAN_B / 32];
+    int64_t i = (int64_t)blockIdx.x * SCAN_B + threadIdx.x;
+    uint32_t v = i < dim ? m[i] : 0u;
+    unsigned long long s = v;
+    unsigned int lo = i < dim ? v : 0xFFFFFFFFu, hi = v;
+    for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) { ws[threadIdx.x >> 5] = s; wmn[threadIdx.x >> 5] = lo; wmx[threadIdx.x >> 5] = hi; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = ws[threadIdx.x];
+        lo = wmn[threadIdx.x];
+        hi = wmx[threadIdx.x];
+        for (int o = 16; o; o >>= 1) {
+            s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+            lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+        }
+        if (threadIdx.x == 0) { sums[blockIdx.x] = s; atomicMin(mn, lo); atomicMax(mx, hi); }
+    }
+}
+
+// Exclusive scan of the block sums in one block (looping over 1024-wide
+// segments); writes total M to *M_out.
+__global__ void scan_sums_single(unsigned long long *__restrict__ sums, int64_t nblocks,
+                                 unsigned long long *__restrict__ M_out) {
+    __shared__ unsigned long long wtot[SCAN_B / 32];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nblocks; base += SCAN_B) {
+        int64_t i = base + threadIdx.x;
+        unsigned long long v = i < nblocks ? sums[i] : 0ull;
+        unsigned long long inc = v;                       // warp inclusive scan
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if ((threadIdx.x & 31) >= o) inc += t;
+        }
+        if ((threadIdx.x & 31) == 31) wtot[threadIdx.x >> 5] = inc;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            unsigned long long w = wtot[threadIdx.x], wi = w;
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+                if (threadIdx.x >= o) wi += t;
+            }
+            wtot[threadIdx.x] = wi - w;                   // exclusive warp offsets
+        }
+        __syncthreads();
+        unsigned long long excl = carry + wtot[threadIdx.x >> 5] + inc - v;
+        if (i < nblocks) sums[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == SCAN_B - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *M_out = carry;
+}
+
+// comp_to_m[c] = sums[block] + exclusive in-block prefix (as u32; the host
+// rejects M >= 2^32 before any table is used).  comp_to_m[dim] = M.
+__global__ void scan_apply(const uint32_t *__restrict__ m, int64_t dim, const unsigned long long *__restrict__ sums,
+                          const unsigned long long *__restrict__ M_total, uint32_t *__restrict__ comp_to_m) {
+    __shared__ unsigned long long wtot[SCAN_B / 32];
+    int64_t i = (int64_t)blockIdx.x * SCAN_B + threadIdx.x;
+    unsigned long long v = i < dim ? m[i] : 0u;
+    unsigned long long inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if ((threadIdx.x & 31) >= o) inc += t;
+    }
+    if ((threadIdx.x & 31) == 31) wtot[threadIdx.x >> 5] = inc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long w = wtot[threadIdx.x], wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (threadIdx.x >= o) wi += t;
+        }
+        wtot[threadIdx.x] = wi - w;
+    }
+    __syncthreads();
+    if (i < dim) comp_to_m[i] = (uint32_t)(sums[blockIdx.x] + wtot[threadIdx.x >> 5] + inc - v);
+    if (i == 0) comp_to_m[dim] = (uint32_t)(*M_total);
+}
+
+// ----------------------------------------------------------- a4: IntToComp
+// One warp per component c: lanes write IntToComp[t] = c and the packed
+// form (c << 8) | (t - CompToM[c]) for t in [CompToM[c], CompToM[c+1]).
+// Zero-width components write nothing (reading R11).
+__global__ void fill_int_to_comp(const uint32_t *__restrict__ comp_to_m, int64_t dim, uint32_t *__restrict__ i2c,
+                                 uint32_t *__restrict__ pack) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < dim; c += nwarps) {
+        uint32_t a = comp_to_m[c], b = comp_to_m[c + 1];
+        for (uint32_t t = a + lane; t < b; t += 32) {
+            i2c[t] = (uint32_t)c;
+            pack[t] = ((uint32_t)c << 8) | (t - a);
+        }
+    }
+}
+
+}  // namespace wmh
+
+using namespace wmh;
+
+// ===================================================================== C ABI
+extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *stream) {
+    wmh_status st = check_rows(rows, true);
+    if (st != WMH_OK) return st;
+    if (!colmax) { set_error("wmh_colmax: colmax is NULL"); return WMH_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    WMH_CUDA_TRY(cudaMemsetAsync(colmax, 0, sizeof(uint32_t) * rows->dim, s), "memset colmax");
+    if (rows->n_rows == 0) return WMH_OK;
+    if (rows->kind == WMH_DENSE) {
+        const int sms = num_sms();
+        bool vec = (rows->dim % 16 == 0) && ((uintptr_t)rows->dense % 16 == 0);
+        int64_t cols_units = vec ? rows->dim / 16 : rows->dim;
+        int threads = 128;
+        int64_t gx = (cols_units + threads - 1) / threads;
+        int64_t want_blocks = (int64_t)sms * 8;
+        int64_t gy = max((int64_t)1, min(rows->n_rows, want_blocks / max((int64_t)1, gx)));
+        gy = min(gy, (int64_t)65535);
+        int64_t per = (rows->n_rows + gy - 1) / gy;
+        gy = (rows->n_rows + per - 1) / per;
+        dim3 grid((unsigned)gx, (unsigned)gy);
+        if (vec)
+            colmax_dense_vec16<<<grid, threads, 0, s>>>(rows->dense, rows->n_rows, rows->dim, per, colmax);
+        else
+            colmax_dense_bytes<<<grid, threads, 0, s>>>(rows->dense, rows->n_rows, rows->dim, per, colmax);
+    } else {
+        if (rows->nnz > 0) {
+            int64_t blocks = min((int64_t)num_sms() * 16, (rows->nnz + 255) / 256);
+            colmax_csr<<<(unsigned)blocks, 256, 0, s>>>(rows->col, rows->val, rows->nnz, colmax);
+        }
+    }
+    WMH_LAUNCH_CHECK("colmax launch");
+    return WMH_OK;
+}
+
+extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh_rows *rows, wmh_layout **out,
+                                  void *stream) {
+    if (!out) { set_error("wmh_prepare: out is NULL"); return WMH_EINVAL; }
+    *out = nullptr;
+    if (!bounds) { set_error("wmh_prepare: bounds is NULL"); return WMH_EINVAL; }
+    if (dim < 1 || dim > (1ll << 24)) { set_error("wmh_prepare: dim=%lld outside [1, 2^24]", (long long)dim); return WMH_EINVAL; }
+    if (rows) {
+        wmh_status st = check_rows(rows, true);
+        if (st != WMH_OK) return st;
+        if (rows->dim != dim) { set_error("wmh_prepare: rows->dim=%lld != dim=%lld", (long long)rows->dim, (long long)dim); return WMH_EINVAL; }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    WMH_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+
+    wmh_layout *L = new wmh_layout();
+    L->dim = dim;
+    L->device = dev;
+    auto fail = [&](wmh_status st) { wmh_layout_free(L); return st; };
+
+    if (cudaMalloc(&L->bounds, sizeof(uint32_t) * dim) != cudaSuccess ||
+        cudaMalloc(&L->comp_to_m, sizeof(uint32_t) * (dim + 1)) != cudaSuccess) {
+        set_error("wmh_prepare: cudaMalloc of %lld-entry tables failed", (long long)dim);
+        return fail(WMH_ENOMEM);
+    }
+    if (cudaMemcpyAsync(L->bounds, bounds, sizeof(uint32_t) * dim, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return fail(cuda_fail(cudaGetLastError(), "copy bounds"));
+
+    const int64_t nb = (dim + SCAN_B - 1) / SCAN_B;
+    // scratch: sums[nb], M, first_bad, mn, mx
+    unsigned long long *scr = nullptr;
+    size_t scr_bytes = sizeof(unsigned long long) * (nb + 4);
+    if (cudaMallocAsync((void **)&scr, scr_bytes, s) != cudaSuccess) {
+        set_error("wmh_prepare: scratch alloc failed");
+        return fail(WMH_ENOMEM);
+    }
+    unsigned long long *sums = scr, *Mdev = scr + nb, *bad = scr + nb + 1;
+    unsigned int *mnmx = reinterpret_cast<unsigned int *>(scr + nb + 2);
+    unsigned long long init[4] = {0ull, ~0ull, 0x00000000FFFFFFFFull, 0ull};  // M, bad, {mn=~0,mx=0}, pad
+    cudaMemcpyAsync(Mdev, init, sizeof(init), cudaMemcpyHostToDevice, s);
+
+    const int sms = num_sms();
+    if (rows && rows->n_rows > 0) {
+        if (rows->kind == WMH_DENSE)
+            check_dense_bounds<<<sms * 8, 256, 0, s>>>(rows->dense, rows->n_rows, dim, L->bounds, bad);
+        else
+            check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, rows->val, rows->n_rows, dim, rows->nnz,
+                                              L->bounds, bad);
+    }
+    scan_block_sums<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, mnmx, mnmx + 1);
+    scan_sums_single<<<1, SCAN_B, 0, s>>>(sums, nb, Mdev);
+    scan_apply<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, Mdev, L->comp_to_m);
+    if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(scr, s); return fail(cuda_fail(cudaGetLastError(), "prepare scan launch")); }
+
+    unsigned long long host[4];
+    cudaError_t e1 = cudaMemcpyAsync(host, Mdev, sizeof(host), cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaFreeAsync(scr, s);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(cuda_fail(e1 != cudaSuccess ? e1 : e2, "prepare readback"));
+    const unsigned long long M = host[0], first_bad = host[1];
+    const unsigned int mn = (unsigned int)(host[2] & 0xFFFFFFFFu), mx = (unsigned int)(host[2] >> 32);
+
+    if (mx > 255) { set_error("wmh_prepare: a bound is %u > 255 (weights are uint8)", mx); return fail(WMH_EINVAL); }
+    if (first_bad != ~0ull) {
+        if (rows->kind == WMH_DENSE) {
+            long long r = (long long)(first_bad / (unsigned long long)dim), c = (long long)(first_bad % (unsigned long long)dim);
+            set_error("wmh_prepare: weight x[%lld][%lld] exceeds its bound", r, c);
+            return fail(WMH_EBOUND);
+        }
+        unsigned code = (unsigned)(first_bad & 7ull);
+        long long e = (long long)(first_bad >> 3);
+        static const char *what[] = {"", "column index out of range", "columns not strictly ascending",
+                                     "value exceeds its bound", "row_ptr malformed"};
+        set_error("wmh_prepare: CSR nonzero %lld: %s", e, what[code <= 4 ? code : 0]);
+        return fail(code == 3 ? WMH_EBOUND : WMH_EINVAL);
+    }
+    if (M == 0) { set_error("wmh_prepare: M = sum of bounds is 0"); return fail(WMH_EEMPTY); }
+    if (M >= (1ull << 32)) { set_error("wmh_prepare: M = %llu >= 2^32", M); return fail(WMH_EOVERFLOW); }
+    L->M = M;
+    if (mn == mx) { L->flags |= WMH_LAYOUT_UNIFORM; L->uniform_m = mx; }
+
+    if (cudaMalloc(&L->int_to_comp, sizeof(uint32_t) * M) != cudaSuccess ||
+        cudaMalloc(&L->cell_pack, sizeof(uint32_t) * M) != cudaSuccess) {
+        set_error("wmh_prepare: cudaMalloc of IntToComp (%llu cells) failed", M);
+        return fail(WMH_ENOMEM);
+    }
+    int64_t blocks = min((int64_t)sms * 16, (dim * 32 + 255) / 256);
+    fill_int_to_comp<<<(unsigned)blocks, 256, 0, s>>>(L->comp_to_m, dim, L->int_to_comp, L->cell_pack);
+    if (cudaGetLastError() != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "fill IntToComp launch"));
+    *out = L;
+    return WMH_OK;
+}
+
+extern "C" wmh_status wmh_layout_info(const wmh_layout *L, int64_t *dim, uint64_t *M, uint32_t *flags,
+                                      uint32_t *uniform_bound) {
+    if (!L) { set_error("wmh_layout_info: layout is NULL"); return WMH_EINVAL; }
+    if (dim) *dim = L->dim;
+    if (M) *M = L->M;
+    if (flags) *flags = L->flags;
+    if (uniform_bound) *uniform_bound = L->uniform_m;
+    return WMH_OK;
+}
+
+extern "C" wmh_status wmh_layout_tables(const wmh_layout *L, const uint32_t **c2m, const uint32_t **i2c,
+                                        const uint32_t **bounds) {
+    if (!L) { set_error("wmh_layout_tables: layout is NULL"); return WMH_EINVAL; }
+    if (c2m) *c2m = L->comp_to_m;
+    if (i2c) *i2c = L->int_to_comp;
+    if (bounds) *bounds = L->bounds;
+    return WMH_OK;
+}
+
+extern "C" void wmh_layout_free(wmh_layout *L) {
+    if (!L) return;
+    cudaFree(L->bounds);
+    cudaFree(L->comp_to_m);
+    cudaFree(L->int_to_comp);
+    cudaFree(L->cell_pack);
+    delete L;
+}
