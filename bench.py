@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--config", default="c2", help="c1..c5 (default c2: the metric's workload, configs[1])")
     p.add_argument("--rows", type=int, default=None, help="rows per GPU (default: the config's N)")
     p.add_argument("--algo", default="auto", choices=["auto", "simple", "tiled"])
+    p.add_argument("--chunk", type=int, default=0, help="tiled: draws per re-queue (0 = auto)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -253,7 +254,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig)
+        wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig, chunk=args.chunk)
 
     clocks = ClockSampler(dev.index if world == 1 else local)
     clocks.start()

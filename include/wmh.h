@@ -140,7 +140,10 @@ typedef enum {
 
 typedef struct {
     int32_t algo;        /* wmh_algo */
-    int32_t reserved[7]; /* must be zero */
+    int32_t chunk;       /* TILED: draws tested per row before re-queueing it, one of
+                            0 (auto: picked per tile from its effective sparsity
+                            s = |x|_1 / M, Eq. 17), 4, 8, 16, 32 */
+    int32_t reserved[6]; /* must be zero */
 } wmh_hash_opts;
 
 wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k,

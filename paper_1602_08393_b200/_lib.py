@@ -26,7 +26,7 @@ class WmhRows(ctypes.Structure):
 
 
 class WmhHashOpts(ctypes.Structure):
-    _fields_ = [("algo", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+    _fields_ = [("algo", ctypes.c_int32), ("chunk", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
 class WmhError(RuntimeError):

@@ -75,6 +75,7 @@ struct HashArgs {
     void *sig;
     unsigned long long *n_sat;   // may be null
     cudaStream_t stream;
+    int chunk;           // TILED: 0 = auto, else 4/8/16/32
 };
 
 wmh_status launch_hash_simple(const HashArgs &a);

@@ -1,12 +1,378 @@
-// hash_tiled.cu -- WMH_ALGO_TILED (placeholder until the tiled kernel lands).
+// hash_tiled.cu -- WMH_ALGO_TILED for dense rows: the B200 form of Alg. 3.
+//
+// The paper's draw stream is independent of x ("consistency", P:190-191:
+// every vector sees the same r_1, r_2, ... for a given hash), so one draw
+// r_t of hash j can be tested against MANY rows.  A CTA stages a tile of R
+// rows in shared memory; a warp takes one hash j at a time and walks the
+// stream 32 draws per round: each lane produces one draw (c_t, off_t) --
+// from a per-launch table of the first T0 draws of every hash, else
+// computed on the fly (a6) -- the 32 draws are broadcast into every lane's
+// registers, and each lane tests them against the rows it owns (lane = row):
+// green iff x[row][c_t] > off_t (Alg. 5).  A row is tested
+// against C draws (C = 4..32, picked per tile from its effective sparsity
+// s = |x|_1 / M, Eq. 17) before it is re-queued: the first green t
+// gives h = t + 1 (Alg. 3 / Def.), rows without one stay on the
+// warp's pending list.  When few rows remain pending the warp switches to
+// draw-parallel mode (lane = draw, loop over the pending rows, ballot + ffs
+// finds the first green).  Rows still pending at the cap get h = cap (R9).
+//
+// Shared-memory rows use an odd word stride, so the 32 lanes of a
+// row-parallel test (same c_t, 32 different rows) hit 32 different banks.
 #include "common.cuh"
 
 namespace wmh {
 
-wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
-    (void)a;
-    *handled = false;
+constexpr int T0 = 256;                 // draws per hash kept in the per-launch table
+constexpr int STRAGGLERS = 6;           // pending rows at or below which a warp goes draw-parallel
+
+// Packed cell of draw r: (c << 8) | (r - CompToM[c])  (Alg. 5 in one value).
+__device__ __forceinline__ uint32_t cell_of(uint32_t r, const uint32_t *__restrict__ pack, uint32_t uni_m) {
+    if (uni_m) {                        // uniform bounds: IntToComp[r] = r / m
+        uint32_t c = r / uni_m;
+        return (c << 8) | (r - c * uni_m);
+    }
+    return __ldg(pack + r);
+}
+
+// table[j * T0 + t] = packed cell of r_t of hash j, t < T0.
+__global__ void draw_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
+                                  const uint32_t *__restrict__ pack, uint32_t uni_m) {
+    const int64_t total = (int64_t)k * T0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
+        table[i] = cell_of(draw_r(S, j, t, M), pack, uni_m);
+    }
+}
+
+struct TiledParams {
+    const uint8_t *x;
+    int64_t n_rows;
+    int D, SW, R;               // dim, smem row stride (words, odd), rows per tile
+    int n_hchunks, hchunk;      // hash chunks per tile item
+    int64_t n_items;
+    uint32_t k, cap, M, uni_m;
+    uint64_t S;
+    int chunk;                  // 0 = auto
+    const uint32_t *table;      // [k][T0]
+    const uint32_t *pack;
+    void *sig;
+    unsigned long long *n_sat;
+    unsigned long long *item_ctr;
+};
+
+template <int SIGB>
+__device__ __forceinline__ void store_sig(void *sig, int64_t idx, uint32_t h) {
+    if (SIGB == 1) reinterpret_cast<uint8_t *>(sig)[idx] = (uint8_t)h;
+    else reinterpret_cast<uint16_t *>(sig)[idx] = (uint16_t)h;
+}
+
+// The packed cell of draw t of hash j.
+__device__ __forceinline__ uint32_t draw_cell(const TiledParams &p, const uint32_t *tab, uint64_t keyj, uint32_t t) {
+    if (t < (uint32_t)T0) return __ldg(tab + t);
+    return cell_of(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m);
+}
+
+// Row-parallel rounds of one hash over the warp's pending list, C draws per
+// re-queue.  Returns the number of rows still pending (in *cur) and the next
+// round index in *q; stops early when <= STRAGGLERS rows remain.
+template <int SIGB, int C>
+__device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const uint8_t *srow_bytes, int SW4,
+                                                   uint2 *sdraw, uint16_t *&cur, uint16_t *&nxt, int npend,
+                                                   uint32_t j, const uint32_t *tab, uint64_t keyj, int64_t row0,
+                                                   uint32_t *q_io) {
+    const int lane = threadIdx.x & 31;
+    uint32_t q = *q_io;
+    while (npend > STRAGGLERS && q * 32 < p.cap) {
+        const uint32_t t = q * 32 + lane;
+        const uint32_t cell = draw_cell(p, tab, keyj, t);
+        uint2 d = make_uint2(cell >> 8, cell & 0xFFu);
+        if (t >= p.cap) d = make_uint2(0u, 0xFFFFFFFFu);          // past the cap: never green
+        __syncwarp();
+        sdraw[lane] = d;
+        __syncwarp();
+        uint32_t dc[32], doff[32];
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            uint4 v = reinterpret_cast<const uint4 *>(sdraw)[i];
+            dc[2 * i] = v.x; doff[2 * i] = v.y; dc[2 * i + 1] = v.z; doff[2 * i + 1] = v.w;
+        }
+#pragma unroll
+        for (int sub = 0; sub < 32 / C; sub++) {
+            if (npend == 0) break;
+            int nn = 0;
+            for (int base = 0; base < npend; base += 32) {
+                const int i = base + lane;
+                const bool active = i < npend;
+                const int r = active ? cur[i] : 0;
+                uint32_t h = C;
+                if (active) {
+                    const uint8_t *row = srow_bytes + r * SW4;
+#pragma unroll
+                    for (int tt = C - 1; tt >= 0; tt--) {
+                        uint32_t v = row[dc[sub * C + tt]];
+                        h = (v > doff[sub * C + tt]) ? (uint32_t)tt : h;
+                    }
+                }
+                const bool still = active && h == C;
+                if (active && !still)
+                    store_sig<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + j, q * 32 + sub * C + h + 1);
+                unsigned m = __ballot_sync(0xFFFFFFFFu, still);
+                if (still) nxt[nn + __popc(m & ((1u << lane) - 1))] = (uint16_t)r;
+                nn += __popc(m);
+            }
+            __syncwarp();
+            uint16_t *tmp = cur; cur = nxt; nxt = tmp;
+            npend = nn;
+        }
+        q++;
+    }
+    *q_io = q;
+    return npend;
+}
+
+template <int SIGB, int NT>
+__global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kernel(const TiledParams p) {
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int R = p.R, SW = p.SW, SW4 = p.SW * 4;
+    uint32_t *srows = smem;                                            // R * SW words
+    uint2 *sdraw_all = reinterpret_cast<uint2 *>(smem + R * SW);       // [warps][32]
+    uint16_t *spend_all = reinterpret_cast<uint16_t *>(sdraw_all + NW * 32);   // [warps][2][R]
+    uint8_t *salive = reinterpret_cast<uint8_t *>(spend_all + NW * 2 * R);    // [R]
+    __shared__ long long s_item;
+    __shared__ int s_hash;
+    __shared__ unsigned long long s_xsum;
+    __shared__ int s_nalive;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint2 *sdraw = sdraw_all + warp * 32;
+    uint16_t *pendA = spend_all + warp * 2 * R, *pendB = pendA + R;
+    const uint8_t *srow_bytes = reinterpret_cast<const uint8_t *>(srows);
+    unsigned long long sat = 0;
+    const int words = (p.D + 3) >> 2;
+
+    for (;;) {
+        __syncthreads();                                    // previous item fully done with smem
+        if (threadIdx.x == 0) {
+            s_item = (long long)atomicAdd(p.item_ctr, 1ull);
+            s_hash = 0;
+            s_xsum = 0;
+            s_nalive = 0;
+        }
+        __syncthreads();
+        const long long item = s_item;
+        if (item >= p.n_items) break;
+        const int64_t tile = item / p.n_hchunks;
+        const int hc = (int)(item % p.n_hchunks);
+        const int64_t row0 = tile * R;
+        const int nr = (int)min((int64_t)R, p.n_rows - row0);
+        const uint32_t j0 = (uint32_t)hc * p.hchunk;
+        const uint32_t j1 = min(p.k, j0 + (uint32_t)p.hchunk);
+
+        // ---- a5: stage the tile's rows (coalesced 4-byte words) ----------
+        const uint8_t *gx = p.x + row0 * (int64_t)p.D;
+        if ((p.D & 3) == 0) {
+            const uint32_t *g32 = reinterpret_cast<const uint32_t *>(gx);
+            for (int i = threadIdx.x; i < nr * words; i += NT) {
+                int r = i / words, w = i - r * words;
+                srows[r * SW + w] = __ldg(g32 + (int64_t)r * words + w);
+            }
+        } else {
+            uint8_t *sb = reinterpret_cast<uint8_t *>(srows);
+            for (int i = threadIdx.x; i < nr * p.D; i += NT) {
+                int r = i / p.D, c = i - r * p.D;
+                sb[r * SW4 + c] = __ldg(gx + (int64_t)r * p.D + c);
+            }
+        }
+        __syncthreads();
+        // per-row |x|_1 (an all-zero row never turns green: h = cap), tile s
+        for (int r = warp; r < nr; r += NW) {
+            uint32_t acc = 0;
+            if ((p.D & 3) == 0) {
+                for (int w = lane; w < words; w += 32) acc = __dp4a(srows[r * SW + w], 0x01010101u, acc);
+            } else {
+                for (int c = lane; c < p.D; c += 32) acc += srow_bytes[r * SW4 + c];
+            }
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+            if (lane == 0) {
+                salive[r] = acc != 0;
+                if (acc) { atomicAdd(&s_xsum, (unsigned long long)acc); atomicAdd(&s_nalive, 1); }
+            }
+        }
+        __syncthreads();
+        int C = p.chunk;
+        if (C == 0) {                   // C ~ 0.5 / s (cost model in DESIGN.md §5)
+            const double s = s_nalive ? (double)s_xsum / ((double)s_nalive * (double)p.M) : 1.0;
+            C = s > 0.1 ? 4 : s > 0.04 ? 8 : s > 0.015 ? 16 : 32;
+        }
+
+        // ---- hashes of this item, one warp per hash, dynamically assigned ----
+        for (;;) {
+            int jj = 0;
+            if (lane == 0) jj = atomicAdd(&s_hash, 1);
+            jj = __shfl_sync(0xFFFFFFFFu, jj, 0);
+            const uint32_t j = j0 + (uint32_t)jj;
+            if (j >= j1) break;
+
+            // initial pending list: the alive rows; dead rows saturate now
+            int npend = 0;
+            for (int base = 0; base < nr; base += 32) {
+                int r = base + lane;
+                bool alive = r < nr && salive[r];
+                unsigned m = __ballot_sync(0xFFFFFFFFu, alive);
+                if (alive) pendA[npend + __popc(m & ((1u << lane) - 1))] = (uint16_t)r;
+                if (r < nr && !alive) { store_sig<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + j, p.cap); sat++; }
+                npend += __popc(m);
+            }
+            __syncwarp();
+            uint16_t *cur = pendA, *nxt = pendB;
+            const uint32_t *tab = p.table + (int64_t)j * T0;
+            const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
+            uint32_t q = 0;
+            switch (C) {
+                case 4: npend = rounds_row_parallel<SIGB, 4>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
+                case 8: npend = rounds_row_parallel<SIGB, 8>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
+                case 16: npend = rounds_row_parallel<SIGB, 16>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
+                default: npend = rounds_row_parallel<SIGB, 32>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
+            }
+            // ---- a9: rows with no green draw before the cap saturate ----------
+            if (npend > 0 && q * 32 >= p.cap) {
+                for (int i = lane; i < npend; i += 32) {
+                    store_sig<SIGB>(p.sig, (row0 + cur[i]) * (int64_t)p.k + j, p.cap);
+                    sat++;
+                }
+                npend = 0;
+            }
+            // ---- draw-parallel mode for the last <= STRAGGLERS rows ---------------
+            if (npend > 0) {
+                int rr[STRAGGLERS];
+                unsigned live = 0;
+#pragma unroll
+                for (int i = 0; i < STRAGGLERS; i++) {
+                    rr[i] = i < npend ? (int)cur[i] : 0;
+                    if (i < npend) live |= 1u << i;
+                }
+                for (; live && q * 32 < p.cap; q++) {
+                    const uint32_t t = q * 32 + lane;
+                    const uint32_t cell = draw_cell(p, tab, keyj, t);
+                    const uint32_t c = cell >> 8, off = t < p.cap ? (cell & 0xFFu) : 0xFFFFFFFFu;
+#pragma unroll
+                    for (int i = 0; i < STRAGGLERS; i++) {
+                        if (live & (1u << i)) {
+                            const uint32_t v = srow_bytes[rr[i] * SW4 + c];
+                            const unsigned g = __ballot_sync(0xFFFFFFFFu, v > off);
+                            if (g) {
+                                if (lane == 0)
+                                    store_sig<SIGB>(p.sig, (row0 + rr[i]) * (int64_t)p.k + j, q * 32 + __ffs(g));
+                                live &= ~(1u << i);
+                            }
+                        }
+                    }
+                }
+                // ---- a9: rows with no green draw before the cap saturate -------
+#pragma unroll
+                for (int i = 0; i < STRAGGLERS; i++)
+                    if ((live & (1u << i)) && lane == 0) {
+                        store_sig<SIGB>(p.sig, (row0 + rr[i]) * (int64_t)p.k + j, p.cap);
+                        sat++;
+                    }
+            }
+            __syncwarp();
+        }
+    }
+    if (p.n_sat) {
+        for (int o = 16; o; o >>= 1) sat += __shfl_xor_sync(0xFFFFFFFFu, sat, o);
+        if (lane == 0 && sat) atomicAdd(p.n_sat, sat);
+    }
+}
+
+static size_t tiled_smem(int R, int SW, int NW) {
+    return (size_t)R * SW * 4 + (size_t)NW * 32 * sizeof(uint2) + (size_t)NW * 2 * R * 2 + R + 16;
+}
+
+template <int SIGB, int NT>
+static wmh_status launch_tiled(const TiledParams &p, size_t smem, int grid, cudaStream_t s) {
+    auto *fn = hash_tiled_dense_kernel<SIGB, NT>;
+    WMH_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "tiled smem attr");
+    fn<<<grid, NT, smem, s>>>(p);
+    WMH_LAUNCH_CHECK("hash_tiled_dense launch");
     return WMH_OK;
+}
+
+wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
+    *handled = false;
+    if (a.rows.kind != WMH_DENSE) return WMH_OK;          // CSR: simple kernel (tiled CSR is next)
+    const int D = (int)a.rows.dim;
+    const int SW = (((D + 3) >> 2) | 1);                  // odd word stride: conflict-free lane=row tests
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int smem_optin = 0, smem_sm = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    // Two 256-thread CTAs per SM when a >= 32-row tile fits twice, else one
+    // 512-thread CTA with the largest tile that fits.
+    int ctas = 2, NT = 256, R = 0;
+    for (; ctas >= 1; ctas--) {
+        NT = ctas == 2 ? 256 : 512;
+        size_t budget = min((size_t)smem_optin, (size_t)smem_sm / ctas - 1024);
+        R = 256;
+        while (R >= 32 && tiled_smem(R, SW, NT / 32) > budget) R -= 16;
+        if (R >= 32) break;
+    }
+    if (R < 32) return WMH_OK;                            // rows too long for a 32-row tile
+    const size_t smem = tiled_smem(R, SW, NT / 32);
+    *handled = true;
+
+    const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
+    const int sms = num_sms();
+    // split the k hashes into chunks so there are >= ~16 items per resident CTA
+    int64_t slots = (int64_t)sms * ctas;
+    int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 8, (slots * 16 + n_tiles - 1) / n_tiles));
+    n_hchunks = max(1, min(n_hchunks, (int)a.k));
+    int hchunk = (int)((a.k + n_hchunks - 1) / n_hchunks);
+    n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
+
+    uint8_t *scratch = nullptr;
+    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint32_t);
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "tiled scratch alloc");
+    uint32_t *table = reinterpret_cast<uint32_t *>(scratch);
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
+    WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "tiled counter memset");
+
+    const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
+    const uint32_t M = (uint32_t)a.L->M;
+    {
+        int64_t total = (int64_t)a.k * T0;
+        int blocks = (int)min((int64_t)sms * 8, (total + 255) / 256);
+        draw_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, M, a.L->cell_pack, uni_m);
+        WMH_LAUNCH_CHECK("draw table launch");
+    }
+    TiledParams p;
+    p.x = a.rows.dense;
+    p.n_rows = a.rows.n_rows;
+    p.D = D;
+    p.SW = SW;
+    p.R = R;
+    p.n_hchunks = n_hchunks;
+    p.hchunk = hchunk;
+    p.n_items = n_tiles * n_hchunks;
+    p.k = a.k;
+    p.cap = a.cap;
+    p.M = M;
+    p.uni_m = uni_m;
+    p.S = a.S;
+    p.chunk = a.chunk;
+    p.table = table;
+    p.pack = a.L->cell_pack;
+    p.sig = a.sig;
+    p.n_sat = a.n_sat;
+    p.item_ctr = ctr;
+    const int grid = (int)min((int64_t)sms * ctas, p.n_items);
+    wmh_status st;
+    if (a.sig_bytes == 1) st = NT == 256 ? launch_tiled<1, 256>(p, smem, grid, a.stream) : launch_tiled<1, 512>(p, smem, grid, a.stream);
+    else st = NT == 256 ? launch_tiled<2, 256>(p, smem, grid, a.stream) : launch_tiled<2, 512>(p, smem, grid, a.stream);
+    cudaFreeAsync(scratch, a.stream);
+    return st;
 }
 
 }  // namespace wmh
