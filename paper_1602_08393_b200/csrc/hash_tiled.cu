@@ -18,6 +18,9 @@
 //
 // Shared-memory rows use an odd word stride, so the 32 lanes of a
 // row-parallel test (same c_t, 32 different rows) hit 32 different banks.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace wmh {
@@ -58,6 +61,7 @@ struct TiledParams {
     void *sig;
     unsigned long long *n_sat;
     unsigned long long *item_ctr;
+    unsigned long long *stats;  // debug (WMH_TILED_STATS=1): tiles per C, sum of tile s * 1e9
 };
 
 template <int SIGB>
@@ -204,7 +208,9 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
         if (C == 0) {                   // C ~ 0.5 / s (cost model in DESIGN.md §5)
             const double s = s_nalive ? (double)s_xsum / ((double)s_nalive * (double)p.M) : 1.0;
             C = s > 0.1 ? 4 : s > 0.04 ? 8 : s > 0.015 ? 16 : 32;
+            if (p.stats && threadIdx.x == 0) atomicAdd(p.stats + 5, (unsigned long long)(s * 1e9));
         }
+        if (p.stats && threadIdx.x == 0) atomicAdd(p.stats + (31 - __clz(C)) - 2, 1ull);
 
         // ---- hashes of this item, one warp per hash, dynamically assigned ----
         for (;;) {
@@ -337,7 +343,8 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "tiled scratch alloc");
     uint32_t *table = reinterpret_cast<uint32_t *>(scratch);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
-    WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "tiled counter memset");
+    WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), a.stream), "tiled counter memset");
+    static const bool want_stats = getenv("WMH_TILED_STATS") != nullptr;
 
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
     const uint32_t M = (uint32_t)a.L->M;
@@ -367,10 +374,20 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     p.sig = a.sig;
     p.n_sat = a.n_sat;
     p.item_ctr = ctr;
+    p.stats = want_stats ? ctr + 1 : nullptr;
     const int grid = (int)min((int64_t)sms * ctas, p.n_items);
     wmh_status st;
     if (a.sig_bytes == 1) st = NT == 256 ? launch_tiled<1, 256>(p, smem, grid, a.stream) : launch_tiled<1, 512>(p, smem, grid, a.stream);
     else st = NT == 256 ? launch_tiled<2, 256>(p, smem, grid, a.stream) : launch_tiled<2, 512>(p, smem, grid, a.stream);
+    if (want_stats && st == WMH_OK) {
+        unsigned long long h[7] = {0};
+        cudaMemcpyAsync(h, ctr, sizeof h, cudaMemcpyDeviceToHost, a.stream);
+        cudaStreamSynchronize(a.stream);
+        unsigned long long tiles = h[1] + h[2] + h[3] + h[4];
+        fprintf(stderr, "[wmh tiled] R=%d SW=%d NT=%d grid=%d items=%lld hchunk=%d tiles C4=%llu C8=%llu C16=%llu C32=%llu mean_s=%.5f\n",
+                R, SW, NT, grid, (long long)p.n_items, hchunk, h[1], h[2], h[3], h[4],
+                tiles ? (double)h[6] / 1e9 / (double)tiles : 0.0);
+    }
     cudaFreeAsync(scratch, a.stream);
     return st;
 }
