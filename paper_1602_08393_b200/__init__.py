@@ -22,7 +22,8 @@ import torch
 from . import _lib
 from ._lib import WmhError  # noqa: F401
 
-__all__ = ["Rows", "Layout", "colmax", "prepare", "hash", "hash_host", "collide", "WmhError", "version"]
+__all__ = ["Rows", "Layout", "colmax", "reduce_bounds", "shard", "prepare", "hash", "hash_host", "collide", "WmhError",
+           "version"]
 
 
 def _stream(stream=None) -> int:
@@ -140,6 +141,30 @@ def colmax(rows: Rows, stream=None) -> torch.Tensor:
     return out
 
 
+def reduce_bounds(bounds: torch.Tensor, group=None) -> torch.Tensor:
+    """a2: m <- elementwise max over the ranks of `group` (in place; returns it).
+
+    `group`: None = the default group when a multi-rank job is initialised,
+    False = no reduction, else a ProcessGroup.  The uint32 bounds travel as an
+    int32 view (values <= 255, same bits) so NCCL and gloo both take them."""
+    dist = torch.distributed
+    if group is False:
+        return bounds
+    world = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    if world:
+        dist.all_reduce(bounds.view(torch.int32), op=dist.ReduceOp.MAX, group=group)
+    return bounds
+
+
+def shard(n_rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous row block [lo, hi) of rank `rank` out of `world` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, rem = divmod(n_rows, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
 def prepare(rows: Rows | None = None, bounds: torch.Tensor | None = None, group=None, validate: bool = True,
             stream=None) -> Layout:
     """a1-a4.  Without `bounds`, m_c is the column max of `rows`, reduced with an
@@ -150,12 +175,7 @@ def prepare(rows: Rows | None = None, bounds: torch.Tensor | None = None, group=
     if bounds is None:
         if rows is None:
             raise ValueError("prepare needs rows or bounds")
-        bounds = colmax(rows, stream)
-        dist = torch.distributed
-        world = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
-        if group is not False and (group is not None or world):
-            b32 = bounds.view(torch.int32)            # values <= 255: same bits; NCCL-friendly dtype
-            dist.all_reduce(b32, op=dist.ReduceOp.MAX, group=group)
+        bounds = reduce_bounds(colmax(rows, stream), group)
     else:
         _need_cuda(bounds, "bounds")
         if bounds.dtype not in (torch.uint32, torch.int32):

@@ -4,17 +4,17 @@
 // every vector sees the same r_1, r_2, ... for a given hash), so one draw
 // r_t of hash j can be tested against MANY rows.  A CTA stages a tile of R
 // rows in shared memory; a warp takes one hash j at a time and walks the
-// stream 32 draws per round: each lane produces one draw (c_t, off_t) --
-// from a per-launch table of the first T0 draws of every hash, else
-// computed on the fly (a6) -- the 32 draws are broadcast into every lane's
-// registers, and each lane tests them against the rows it owns (lane = row):
-// green iff x[row][c_t] > off_t (Alg. 5).  A row is tested
-// against C draws (C = 4..32, picked per tile from its effective sparsity
-// s = |x|_1 / M, Eq. 17) before it is re-queued: the first green t
-// gives h = t + 1 (Alg. 3 / Def.), rows without one stay on the
-// warp's pending list.  When few rows remain pending the warp switches to
-// draw-parallel mode (lane = draw, loop over the pending rows, ballot + ffs
-// finds the first green).  Rows still pending at the cap get h = cap (R9).
+// stream: the first T0 = 256 draws of every hash come from a per-launch table
+// (prefetched one hash ahead into a per-warp shared buffer), later ones are
+// computed on the fly (a6).  Draws are broadcast into every lane's registers
+// and each lane tests them against the rows it owns (lane = row): green iff
+// x[row][c_t] > off_t (Alg. 5).  A row is tested against C draws
+// (C = 4..32, picked per tile from its effective sparsity s = |x|_1 / M,
+// Eq. 17) before it is re-queued: the first green t gives h = t + 1
+// (Alg. 3 / Def.), rows without one stay on the warp's pending
+// list.  When few rows remain pending the warp switches to draw-parallel
+// mode (lane = draw, loop over the pending rows, ballot + ffs finds the first
+// green).  Rows still pending at the cap get h = cap (reading R9).
 //
 // Shared-memory rows use an odd word stride, so the 32 lanes of a
 // row-parallel test (same c_t, 32 different rows) hit 32 different banks.
@@ -70,39 +70,61 @@ __device__ __forceinline__ void store_sig(void *sig, int64_t idx, uint32_t h) {
     else reinterpret_cast<uint16_t *>(sig)[idx] = (uint16_t)h;
 }
 
-// The packed cell of draw t of hash j.
-__device__ __forceinline__ uint32_t draw_cell(const TiledParams &p, const uint32_t *tab, uint64_t keyj, uint32_t t) {
-    if (t < (uint32_t)T0) return __ldg(tab + t);
+// The packed cell of draw t >= T0 of hash j (computed: a6 + Alg. 5 lookup).
+__device__ __forceinline__ uint32_t late_cell(const TiledParams &p, uint64_t keyj, uint32_t t) {
     return cell_of(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m);
 }
 
-// Row-parallel rounds of one hash over the warp's pending list, C draws per
-// re-queue.  Returns the number of rows still pending (in *cur) and the next
-// round index in *q; stops early when <= STRAGGLERS rows remain.
+// Per-warp state of the hash being processed.
+struct HashCtx {
+    const uint32_t *buf;        // shared: packed cells of draws 0..T0-1 of hash j
+    uint32_t *win;              // shared: 32-draw window for draws >= T0
+    uint32_t j;
+    uint64_t keyj;
+    int64_t row0;
+};
+
+// Row-parallel rounds over the warp's pending list (cur), C draws per
+// re-queue.  Returns the number of rows still pending (left in cur) and the
+// next round in *q; stops when <= STRAGGLERS rows remain or at the cap.
 template <int SIGB, int C>
-__device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const uint8_t *srow_bytes, int SW4,
-                                                   uint2 *sdraw, uint16_t *&cur, uint16_t *&nxt, int npend,
-                                                   uint32_t j, const uint32_t *tab, uint64_t keyj, int64_t row0,
-                                                   uint32_t *q_io) {
+__device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const HashCtx &hx, const uint8_t *srow_bytes,
+                                                   int SW4, const uint16_t *&cur, uint16_t *own0, uint16_t *own1,
+                                                   int npend, uint32_t *q_io) {
     const int lane = threadIdx.x & 31;
     uint32_t q = *q_io;
+    int flip = 0;
     while (npend > STRAGGLERS && q * 32 < p.cap) {
-        const uint32_t t = q * 32 + lane;
-        const uint32_t cell = draw_cell(p, tab, keyj, t);
-        uint2 d = make_uint2(cell >> 8, cell & 0xFFu);
-        if (t >= p.cap) d = make_uint2(0u, 0xFFFFFFFFu);          // past the cap: never green
-        __syncwarp();
-        sdraw[lane] = d;
-        __syncwarp();
-        uint32_t dc[32], doff[32];
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-            uint4 v = reinterpret_cast<const uint4 *>(sdraw)[i];
-            dc[2 * i] = v.x; doff[2 * i] = v.y; dc[2 * i + 1] = v.z; doff[2 * i + 1] = v.w;
+        const uint32_t *src;
+        if (q * 32 < (uint32_t)T0) {
+            src = hx.buf + q * 32;
+        } else {                                             // beyond the table: compute this round
+            const uint32_t c = late_cell(p, hx.keyj, q * 32 + lane);
+            __syncwarp();
+            hx.win[lane] = c;
+            __syncwarp();
+            src = hx.win;
         }
+        const bool cap_round = q * 32 + 32 > p.cap;
 #pragma unroll
         for (int sub = 0; sub < 32 / C; sub++) {
             if (npend == 0) break;
+            uint32_t dc[C], doff[C];
+#pragma unroll
+            for (int i = 0; i < C / 4; i++) {
+                const uint4 v = reinterpret_cast<const uint4 *>(src + sub * C)[i];
+                dc[4 * i + 0] = v.x >> 8; doff[4 * i + 0] = v.x & 0xFFu;
+                dc[4 * i + 1] = v.y >> 8; doff[4 * i + 1] = v.y & 0xFFu;
+                dc[4 * i + 2] = v.z >> 8; doff[4 * i + 2] = v.z & 0xFFu;
+                dc[4 * i + 3] = v.w >> 8; doff[4 * i + 3] = v.w & 0xFFu;
+            }
+            if (cap_round) {                                 // draws at or past the cap never turn green
+#pragma unroll
+                for (int tt = 0; tt < C; tt++)
+                    if (q * 32 + sub * C + tt >= p.cap) doff[tt] = 0xFFFFFFFFu;
+            }
+            uint16_t *nxt = flip ? own1 : own0;
+            flip ^= 1;
             int nn = 0;
             for (int base = 0; base < npend; base += 32) {
                 const int i = base + lane;
@@ -113,19 +135,19 @@ __device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const u
                     const uint8_t *row = srow_bytes + r * SW4;
 #pragma unroll
                     for (int tt = C - 1; tt >= 0; tt--) {
-                        uint32_t v = row[dc[sub * C + tt]];
-                        h = (v > doff[sub * C + tt]) ? (uint32_t)tt : h;
+                        const uint32_t v = row[dc[tt]];
+                        h = (v > doff[tt]) ? (uint32_t)tt : h;
                     }
                 }
                 const bool still = active && h == C;
                 if (active && !still)
-                    store_sig<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + j, q * 32 + sub * C + h + 1);
-                unsigned m = __ballot_sync(0xFFFFFFFFu, still);
+                    store_sig<SIGB>(p.sig, (hx.row0 + r) * (int64_t)p.k + hx.j, q * 32 + sub * C + h + 1);
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, still);
                 if (still) nxt[nn + __popc(m & ((1u << lane) - 1))] = (uint16_t)r;
                 nn += __popc(m);
             }
             __syncwarp();
-            uint16_t *tmp = cur; cur = nxt; nxt = tmp;
+            cur = nxt;
             npend = nn;
         }
         q++;
@@ -139,21 +161,23 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) uint32_t smem[];
     const int R = p.R, SW = p.SW, SW4 = p.SW * 4;
-    uint32_t *srows = smem;                                            // R * SW words
-    uint2 *sdraw_all = reinterpret_cast<uint2 *>(smem + R * SW);       // [warps][32]
-    uint16_t *spend_all = reinterpret_cast<uint16_t *>(sdraw_all + NW * 32);   // [warps][2][R]
-    uint8_t *salive = reinterpret_cast<uint8_t *>(spend_all + NW * 2 * R);    // [R]
+    uint32_t *srows = smem;                                             // [R][SW] words
+    uint32_t *sbuf_all = smem + R * SW;                                 // [NW][T0] packed draws
+    uint32_t *swin_all = sbuf_all + NW * T0;                            // [NW][32] late draws
+    uint16_t *spend_all = reinterpret_cast<uint16_t *>(swin_all + NW * 32);   // [NW][2][R]
+    uint16_t *salive = spend_all + NW * 2 * R;                          // [R] alive row list
+    uint8_t *sflag = reinterpret_cast<uint8_t *>(salive + R);           // [R] row has |x|_1 > 0
     __shared__ long long s_item;
-    __shared__ int s_hash;
+    __shared__ int s_hash, s_nalive;
     __shared__ unsigned long long s_xsum;
-    __shared__ int s_nalive;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint2 *sdraw = sdraw_all + warp * 32;
-    uint16_t *pendA = spend_all + warp * 2 * R, *pendB = pendA + R;
+    uint32_t *sbuf = sbuf_all + warp * T0;
+    uint32_t *swin = swin_all + warp * 32;
+    uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
     const uint8_t *srow_bytes = reinterpret_cast<const uint8_t *>(srows);
     unsigned long long sat = 0;
-    const int words = (p.D + 3) >> 2;
+    const bool vec16 = (p.D % 16 == 0) && ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
 
     for (;;) {
         __syncthreads();                                    // previous item fully done with smem
@@ -173,73 +197,95 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
         const uint32_t j0 = (uint32_t)hc * p.hchunk;
         const uint32_t j1 = min(p.k, j0 + (uint32_t)p.hchunk);
 
-        // ---- a5: stage the tile's rows (coalesced 4-byte words) ----------
-        const uint8_t *gx = p.x + row0 * (int64_t)p.D;
-        if ((p.D & 3) == 0) {
-            const uint32_t *g32 = reinterpret_cast<const uint32_t *>(gx);
-            for (int i = threadIdx.x; i < nr * words; i += NT) {
-                int r = i / words, w = i - r * words;
-                srows[r * SW + w] = __ldg(g32 + (int64_t)r * words + w);
-            }
-        } else {
-            uint8_t *sb = reinterpret_cast<uint8_t *>(srows);
-            for (int i = threadIdx.x; i < nr * p.D; i += NT) {
-                int r = i / p.D, c = i - r * p.D;
-                sb[r * SW4 + c] = __ldg(gx + (int64_t)r * p.D + c);
-            }
-        }
-        __syncthreads();
-        // per-row |x|_1 (an all-zero row never turns green: h = cap), tile s
+        // ---- a5: stage the tile (one warp per row, 16-byte loads), |x|_1 per row ----
         for (int r = warp; r < nr; r += NW) {
+            const uint8_t *g = p.x + (row0 + r) * (int64_t)p.D;
+            uint32_t *srow = srows + r * SW;
             uint32_t acc = 0;
-            if ((p.D & 3) == 0) {
-                for (int w = lane; w < words; w += 32) acc = __dp4a(srows[r * SW + w], 0x01010101u, acc);
+            if (vec16) {
+                for (int c = lane; c < p.D / 16; c += 32) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(g) + c);
+                    srow[4 * c + 0] = v.x; srow[4 * c + 1] = v.y; srow[4 * c + 2] = v.z; srow[4 * c + 3] = v.w;
+                    acc = __dp4a(v.x, 0x01010101u, acc);
+                    acc = __dp4a(v.y, 0x01010101u, acc);
+                    acc = __dp4a(v.z, 0x01010101u, acc);
+                    acc = __dp4a(v.w, 0x01010101u, acc);
+                }
             } else {
-                for (int c = lane; c < p.D; c += 32) acc += srow_bytes[r * SW4 + c];
+                uint8_t *sb = reinterpret_cast<uint8_t *>(srow);
+                for (int c = lane; c < p.D; c += 32) {
+                    const uint8_t v = __ldg(g + c);
+                    sb[c] = v;
+                    acc += v;
+                }
             }
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-            if (lane == 0) {
-                salive[r] = acc != 0;
-                if (acc) { atomicAdd(&s_xsum, (unsigned long long)acc); atomicAdd(&s_nalive, 1); }
-            }
+            if (lane == 0 && acc) atomicAdd(&s_xsum, (unsigned long long)acc);
+            // alive flag, compacted below; an all-zero row never turns green (h = cap)
+            if (lane == 0) sflag[r] = acc != 0;
         }
         __syncthreads();
+        // compact the alive rows into salive (warp 0); dead rows are rare
+        if (warp == 0) {
+            int n = 0;
+            for (int base = 0; base < nr; base += 32) {
+                const int r = base + lane;
+                const bool alive = r < nr && sflag[r];
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, alive);
+                if (alive) salive[n + __popc(m & ((1u << lane) - 1))] = (uint16_t)r;
+                n += __popc(m);
+            }
+            if (lane == 0) s_nalive = n;
+        }
+        __syncthreads();
+        const int nalive = s_nalive;
         int C = p.chunk;
-        if (C == 0) {                   // C ~ 0.5 / s (cost model in DESIGN.md §5)
-            const double s = s_nalive ? (double)s_xsum / ((double)s_nalive * (double)p.M) : 1.0;
-            C = s > 0.1 ? 4 : s > 0.04 ? 8 : s > 0.015 ? 16 : 32;
+        if (C == 0) {                   // C from the tile's effective sparsity
+            const double s = nalive ? (double)s_xsum / ((double)nalive * (double)p.M) : 1.0;
+            C = s > 0.15 ? 4 : s > 0.08 ? 8 : s > 0.02 ? 16 : 32;
             if (p.stats && threadIdx.x == 0) atomicAdd(p.stats + 5, (unsigned long long)(s * 1e9));
         }
         if (p.stats && threadIdx.x == 0) atomicAdd(p.stats + (31 - __clz(C)) - 2, 1ull);
 
-        // ---- hashes of this item, one warp per hash, dynamically assigned ----
-        for (;;) {
+        // ---- hashes of this item: one warp per hash, dynamically assigned, the
+        //      next hash's table prefetched while the current one runs ------------
+        auto grab = [&]() {
             int jj = 0;
             if (lane == 0) jj = atomicAdd(&s_hash, 1);
-            jj = __shfl_sync(0xFFFFFFFFu, jj, 0);
-            const uint32_t j = j0 + (uint32_t)jj;
-            if (j >= j1) break;
-
-            // initial pending list: the alive rows; dead rows saturate now
-            int npend = 0;
-            for (int base = 0; base < nr; base += 32) {
-                int r = base + lane;
-                bool alive = r < nr && salive[r];
-                unsigned m = __ballot_sync(0xFFFFFFFFu, alive);
-                if (alive) pendA[npend + __popc(m & ((1u << lane) - 1))] = (uint16_t)r;
-                if (r < nr && !alive) { store_sig<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + j, p.cap); sat++; }
-                npend += __popc(m);
-            }
+            return j0 + (uint32_t)__shfl_sync(0xFFFFFFFFu, jj, 0);
+        };
+        uint32_t j = grab();
+        uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;
+        if (j < j1) {
+            const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0) + 2 * lane;
+            pa = __ldg(t4);
+            pb = __ldg(t4 + 1);
+        }
+        while (j < j1) {
             __syncwarp();
-            uint16_t *cur = pendA, *nxt = pendB;
-            const uint32_t *tab = p.table + (int64_t)j * T0;
-            const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
+            reinterpret_cast<uint4 *>(sbuf)[2 * lane] = pa;
+            reinterpret_cast<uint4 *>(sbuf)[2 * lane + 1] = pb;
+            __syncwarp();
+            const uint32_t jn = grab();
+            if (jn < j1) {
+                const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0) + 2 * lane;
+                pa = __ldg(t4);
+                pb = __ldg(t4 + 1);
+            }
+            HashCtx hx;
+            hx.buf = sbuf;
+            hx.win = swin;
+            hx.j = j;
+            hx.keyj = p.S ^ ((uint64_t)j << 32);
+            hx.row0 = row0;
+            const uint16_t *cur = salive;
+            int npend = nalive;
             uint32_t q = 0;
             switch (C) {
-                case 4: npend = rounds_row_parallel<SIGB, 4>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
-                case 8: npend = rounds_row_parallel<SIGB, 8>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
-                case 16: npend = rounds_row_parallel<SIGB, 16>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
-                default: npend = rounds_row_parallel<SIGB, 32>(p, srow_bytes, SW4, sdraw, cur, nxt, npend, j, tab, keyj, row0, &q); break;
+                case 4: npend = rounds_row_parallel<SIGB, 4>(p, hx, srow_bytes, SW4, cur, own0, own1, npend, &q); break;
+                case 8: npend = rounds_row_parallel<SIGB, 8>(p, hx, srow_bytes, SW4, cur, own0, own1, npend, &q); break;
+                case 16: npend = rounds_row_parallel<SIGB, 16>(p, hx, srow_bytes, SW4, cur, own0, own1, npend, &q); break;
+                default: npend = rounds_row_parallel<SIGB, 32>(p, hx, srow_bytes, SW4, cur, own0, own1, npend, &q); break;
             }
             // ---- a9: rows with no green draw before the cap saturate ----------
             if (npend > 0 && q * 32 >= p.cap) {
@@ -260,7 +306,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
                 }
                 for (; live && q * 32 < p.cap; q++) {
                     const uint32_t t = q * 32 + lane;
-                    const uint32_t cell = draw_cell(p, tab, keyj, t);
+                    const uint32_t cell = t < (uint32_t)T0 ? sbuf[t] : late_cell(p, hx.keyj, t);
                     const uint32_t c = cell >> 8, off = t < p.cap ? (cell & 0xFFu) : 0xFFFFFFFFu;
 #pragma unroll
                     for (int i = 0; i < STRAGGLERS; i++) {
@@ -275,7 +321,6 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
                         }
                     }
                 }
-                // ---- a9: rows with no green draw before the cap saturate -------
 #pragma unroll
                 for (int i = 0; i < STRAGGLERS; i++)
                     if ((live & (1u << i)) && lane == 0) {
@@ -283,7 +328,18 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
                         sat++;
                     }
             }
-            __syncwarp();
+            j = jn;
+        }
+        // all-zero rows of the tile: h = cap for every hash of the item (reading R12)
+        if (nalive < nr) {
+            __syncthreads();
+            for (int r = warp; r < nr; r += NW) {
+                if (sflag[r]) continue;
+                for (uint32_t jj = j0 + lane; jj < j1; jj += 32) {
+                    store_sig<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + jj, p.cap);
+                    sat++;
+                }
+            }
         }
     }
     if (p.n_sat) {
@@ -293,7 +349,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
 }
 
 static size_t tiled_smem(int R, int SW, int NW) {
-    return (size_t)R * SW * 4 + (size_t)NW * 32 * sizeof(uint2) + (size_t)NW * 2 * R * 2 + R + 16;
+    return (size_t)R * SW * 4 + (size_t)NW * (T0 + 32) * 4 + (size_t)NW * 2 * R * 2 + (size_t)R * 3 + 16;
 }
 
 template <int SIGB, int NT>
@@ -331,11 +387,11 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
 
     const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
     const int sms = num_sms();
-    // split the k hashes into chunks so there are >= ~16 items per resident CTA
-    int64_t slots = (int64_t)sms * ctas;
-    int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 8, (slots * 16 + n_tiles - 1) / n_tiles));
+    // split the k hashes into chunks so there are >= ~8 items per resident CTA
+    const int64_t slots = (int64_t)sms * ctas;
+    int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 8, (slots * 8 + n_tiles - 1) / n_tiles));
     n_hchunks = max(1, min(n_hchunks, (int)a.k));
-    int hchunk = (int)((a.k + n_hchunks - 1) / n_hchunks);
+    const int hchunk = (int)((a.k + n_hchunks - 1) / n_hchunks);
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
 
     uint8_t *scratch = nullptr;
@@ -349,8 +405,8 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
     const uint32_t M = (uint32_t)a.L->M;
     {
-        int64_t total = (int64_t)a.k * T0;
-        int blocks = (int)min((int64_t)sms * 8, (total + 255) / 256);
+        const int64_t total = (int64_t)a.k * T0;
+        const int blocks = (int)min((int64_t)sms * 8, (total + 255) / 256);
         draw_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, M, a.L->cell_pack, uni_m);
         WMH_LAUNCH_CHECK("draw table launch");
     }
@@ -375,7 +431,7 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     p.n_sat = a.n_sat;
     p.item_ctr = ctr;
     p.stats = want_stats ? ctr + 1 : nullptr;
-    const int grid = (int)min((int64_t)sms * ctas, p.n_items);
+    const int grid = (int)min(slots, p.n_items);
     wmh_status st;
     if (a.sig_bytes == 1) st = NT == 256 ? launch_tiled<1, 256>(p, smem, grid, a.stream) : launch_tiled<1, 512>(p, smem, grid, a.stream);
     else st = NT == 256 ? launch_tiled<2, 256>(p, smem, grid, a.stream) : launch_tiled<2, 512>(p, smem, grid, a.stream);
@@ -383,7 +439,7 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
         unsigned long long h[7] = {0};
         cudaMemcpyAsync(h, ctr, sizeof h, cudaMemcpyDeviceToHost, a.stream);
         cudaStreamSynchronize(a.stream);
-        unsigned long long tiles = h[1] + h[2] + h[3] + h[4];
+        const unsigned long long tiles = h[1] + h[2] + h[3] + h[4];
         fprintf(stderr, "[wmh tiled] R=%d SW=%d NT=%d grid=%d items=%lld hchunk=%d tiles C4=%llu C8=%llu C16=%llu C32=%llu mean_s=%.5f\n",
                 R, SW, NT, grid, (long long)p.n_items, hchunk, h[1], h[2], h[3], h[4],
                 tiles ? (double)h[6] / 1e9 / (double)tiles : 0.0);
