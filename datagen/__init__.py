@@ -106,6 +106,50 @@ def gen_counter_c5_rows_slow(data_seed: int, rows, dim: int) -> np.ndarray:
     return out
 
 
+# ------------------------------------------------- device twin (gen_kernels.cu)
+_GEN_SO = None
+
+
+def build_gen(force: bool = False) -> str:
+    """Compile gen_kernels.cu (sm_100a) into datagen/libwmhgen.so."""
+    import os
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    src, so = os.path.join(here, "gen_kernels.cu"), os.path.join(here, "libwmhgen.so")
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        tmp = so + f".tmp{os.getpid()}"
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared",
+                               "-Xcompiler", "-fPIC", "-o", tmp, src])
+        os.replace(tmp, so)
+    return so
+
+
+def gpu_counter_rows(name: str, data_seed: int, row0: int, n_rows: int, dim: int, device="cuda"):
+    """Rows row0 .. row0+n_rows-1 of the c1 / c5 recipe generated on the GPU
+    (bit-identical to gen_counter_c1_rows / gen_counter_c5_rows)."""
+    import ctypes
+    import torch
+    global _GEN_SO
+    if _GEN_SO is None:
+        L = ctypes.CDLL(build_gen())
+        L.wmhgen_counter_rows.restype = ctypes.c_int
+        L.wmhgen_counter_rows.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p]
+        _GEN_SO = L
+    kind = {"c1": 1, "c5": 5}[name]
+    out = torch.empty((n_rows, dim), dtype=torch.uint8, device=device)
+    th = torch.from_numpy(C5_THRESH[:255].view(np.int64).copy()).to(device)
+    rc = _GEN_SO.wmhgen_counter_rows(kind, fmix64_int(data_seed), row0, n_rows, dim, C1_ZERO_THRESH,
+                                     ctypes.c_void_p(th.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                     ctypes.c_void_p(torch.cuda.current_stream(out.device).cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"wmhgen_counter_rows failed ({rc})")
+    torch.cuda.current_stream(out.device).synchronize()
+    del th
+    return out
+
+
 # ----------------------------------------------------------------- data classes
 @dataclass
 class Dense:

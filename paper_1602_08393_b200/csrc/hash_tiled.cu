@@ -37,13 +37,15 @@ __device__ __forceinline__ uint32_t cell_of(uint32_t r, const uint32_t *__restri
     return __ldg(pack + r);
 }
 
-// table[j * T0 + t] = packed cell of r_t of hash j, t < T0.
-__global__ void draw_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
+__device__ __forceinline__ uint2 unpack_cell(uint32_t cell) { return make_uint2(cell >> 8, cell & 0xFFu); }
+
+// table[j * T0 + t] = (c, r_t - CompToM[c]) of draw r_t of hash j, t < T0.
+__global__ void draw_table_kernel(uint2 *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
                                   const uint32_t *__restrict__ pack, uint32_t uni_m) {
     const int64_t total = (int64_t)k * T0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
-        table[i] = cell_of(draw_r(S, j, t, M), pack, uni_m);
+        table[i] = unpack_cell(cell_of(draw_r(S, j, t, M), pack, uni_m));
     }
 }
 
@@ -56,7 +58,7 @@ struct TiledParams {
     uint32_t k, cap, M, uni_m;
     uint64_t S;
     int chunk;                  // 0 = auto
-    const uint32_t *table;      // [k][T0]
+    const uint2 *table;         // [k][T0] (c, off)
     const uint32_t *pack;
     void *sig;
     unsigned long long *n_sat;
@@ -70,15 +72,15 @@ __device__ __forceinline__ void store_sig(void *sig, int64_t idx, uint32_t h) {
     else reinterpret_cast<uint16_t *>(sig)[idx] = (uint16_t)h;
 }
 
-// The packed cell of draw t >= T0 of hash j (computed: a6 + Alg. 5 lookup).
-__device__ __forceinline__ uint32_t late_cell(const TiledParams &p, uint64_t keyj, uint32_t t) {
-    return cell_of(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m);
+// (c, off) of draw t >= T0 of hash j (computed: a6 + Alg. 5 lookup).
+__device__ __forceinline__ uint2 late_cell(const TiledParams &p, uint64_t keyj, uint32_t t) {
+    return unpack_cell(cell_of(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m));
 }
 
 // Per-warp state of the hash being processed.
 struct HashCtx {
-    const uint32_t *buf;        // shared: packed cells of draws 0..T0-1 of hash j
-    uint32_t *win;              // shared: 32-draw window for draws >= T0
+    const uint2 *buf;           // shared: (c, off) of draws 0..T0-1 of hash j
+    uint2 *win;                 // shared: 32-draw window for draws >= T0
     uint32_t j;
     uint64_t keyj;
     int64_t row0;
@@ -95,11 +97,11 @@ __device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const H
     uint32_t q = *q_io;
     int flip = 0;
     while (npend > STRAGGLERS && q * 32 < p.cap) {
-        const uint32_t *src;
+        const uint2 *src;
         if (q * 32 < (uint32_t)T0) {
             src = hx.buf + q * 32;
         } else {                                             // beyond the table: compute this round
-            const uint32_t c = late_cell(p, hx.keyj, q * 32 + lane);
+            const uint2 c = late_cell(p, hx.keyj, q * 32 + lane);
             __syncwarp();
             hx.win[lane] = c;
             __syncwarp();
@@ -111,12 +113,9 @@ __device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const H
             if (npend == 0) break;
             uint32_t dc[C], doff[C];
 #pragma unroll
-            for (int i = 0; i < C / 4; i++) {
+            for (int i = 0; i < C / 2; i++) {
                 const uint4 v = reinterpret_cast<const uint4 *>(src + sub * C)[i];
-                dc[4 * i + 0] = v.x >> 8; doff[4 * i + 0] = v.x & 0xFFu;
-                dc[4 * i + 1] = v.y >> 8; doff[4 * i + 1] = v.y & 0xFFu;
-                dc[4 * i + 2] = v.z >> 8; doff[4 * i + 2] = v.z & 0xFFu;
-                dc[4 * i + 3] = v.w >> 8; doff[4 * i + 3] = v.w & 0xFFu;
+                dc[2 * i] = v.x; doff[2 * i] = v.y; dc[2 * i + 1] = v.z; doff[2 * i + 1] = v.w;
             }
             if (cap_round) {                                 // draws at or past the cap never turn green
 #pragma unroll
@@ -162,8 +161,8 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
     extern __shared__ __align__(16) uint32_t smem[];
     const int R = p.R, SW = p.SW, SW4 = p.SW * 4;
     uint32_t *srows = smem;                                             // [R][SW] words
-    uint32_t *sbuf_all = smem + R * SW;                                 // [NW][T0] packed draws
-    uint32_t *swin_all = sbuf_all + NW * T0;                            // [NW][32] late draws
+    uint2 *sbuf_all = reinterpret_cast<uint2 *>(smem + R * SW);         // [NW][T0] draws (c, off)
+    uint2 *swin_all = sbuf_all + NW * T0;                               // [NW][32] late draws
     uint16_t *spend_all = reinterpret_cast<uint16_t *>(swin_all + NW * 32);   // [NW][2][R]
     uint16_t *salive = spend_all + NW * 2 * R;                          // [R] alive row list
     uint8_t *sflag = reinterpret_cast<uint8_t *>(salive + R);           // [R] row has |x|_1 > 0
@@ -172,8 +171,8 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
     __shared__ unsigned long long s_xsum;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t *sbuf = sbuf_all + warp * T0;
-    uint32_t *swin = swin_all + warp * 32;
+    uint2 *sbuf = sbuf_all + warp * T0;
+    uint2 *swin = swin_all + warp * 32;
     uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
     const uint8_t *srow_bytes = reinterpret_cast<const uint8_t *>(srows);
     unsigned long long sat = 0;
@@ -255,22 +254,22 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
             return j0 + (uint32_t)__shfl_sync(0xFFFFFFFFu, jj, 0);
         };
         uint32_t j = grab();
-        uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;
+        uint4 pre[4];                                      // this lane's 8 draws of the next hash
         if (j < j1) {
-            const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0) + 2 * lane;
-            pa = __ldg(t4);
-            pb = __ldg(t4 + 1);
+            const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0);
+#pragma unroll
+            for (int i = 0; i < 4; i++) pre[i] = __ldg(t4 + 32 * i + lane);
         }
         while (j < j1) {
             __syncwarp();
-            reinterpret_cast<uint4 *>(sbuf)[2 * lane] = pa;
-            reinterpret_cast<uint4 *>(sbuf)[2 * lane + 1] = pb;
+#pragma unroll
+            for (int i = 0; i < 4; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
             __syncwarp();
             const uint32_t jn = grab();
             if (jn < j1) {
-                const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0) + 2 * lane;
-                pa = __ldg(t4);
-                pb = __ldg(t4 + 1);
+                const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0);
+#pragma unroll
+                for (int i = 0; i < 4; i++) pre[i] = __ldg(t4 + 32 * i + lane);
             }
             HashCtx hx;
             hx.buf = sbuf;
@@ -306,8 +305,8 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
                 }
                 for (; live && q * 32 < p.cap; q++) {
                     const uint32_t t = q * 32 + lane;
-                    const uint32_t cell = t < (uint32_t)T0 ? sbuf[t] : late_cell(p, hx.keyj, t);
-                    const uint32_t c = cell >> 8, off = t < p.cap ? (cell & 0xFFu) : 0xFFFFFFFFu;
+                    const uint2 cell = t < (uint32_t)T0 ? sbuf[t] : late_cell(p, hx.keyj, t);
+                    const uint32_t c = cell.x, off = t < p.cap ? cell.y : 0xFFFFFFFFu;
 #pragma unroll
                     for (int i = 0; i < STRAGGLERS; i++) {
                         if (live & (1u << i)) {
@@ -349,7 +348,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
 }
 
 static size_t tiled_smem(int R, int SW, int NW) {
-    return (size_t)R * SW * 4 + (size_t)NW * (T0 + 32) * 4 + (size_t)NW * 2 * R * 2 + (size_t)R * 3 + 16;
+    return (size_t)R * SW * 4 + (size_t)NW * (T0 + 32) * 8 + (size_t)NW * 2 * R * 2 + (size_t)R * 3 + 16;
 }
 
 template <int SIGB, int NT>
@@ -395,9 +394,9 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
 
     uint8_t *scratch = nullptr;
-    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint32_t);
+    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint2);
     WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "tiled scratch alloc");
-    uint32_t *table = reinterpret_cast<uint32_t *>(scratch);
+    uint2 *table = reinterpret_cast<uint2 *>(scratch);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), a.stream), "tiled counter memset");
     static const bool want_stats = getenv("WMH_TILED_STATS") != nullptr;
