@@ -296,7 +296,8 @@ def main():
         pass
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    roof = roofline(args.algo, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
+    algo_used = wmh.last_algo or args.algo
+    roof = roofline(algo_used, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
 
     # ---- e2e: the public host-buffer API, H2D rows + hash + D2H signatures every step
     e2e = None
@@ -332,9 +333,11 @@ def main():
 
 
 # Lane-instructions per draw-test of the dominant kernel's minimal sequence,
-# counted from SASS.  SIMPLE: RNG + range reduction + packed
-# lookup + row lookup + compare + loop, per (row, draw).
-I_DRAW = {"simple": 30.0}
+# counted from SASS.  SIMPLE: the paper's per-(row, draw) loop:
+# SplitMix64 + 64x32 multiply-high + packed lookup + row lookup + compare +
+# loop.  TILED: the draw is shared by the tile, so a draw-test of one row is
+# IMAD (address) + LDS.U8 + ISETP + SEL.
+I_DRAW = {"simple": 30.0, "tiled": 4.0}
 
 
 def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
@@ -344,8 +347,10 @@ def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
     achieved = draws / kern_s / 1e9
     hbm = peaks.get("hbm_gbs", 6545.6)
     return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gdraws/s", "frac": achieved / peak,
-            "traffic": None, "peak_source": f"{n_sm} SMs x 128 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) "
-                                            f"/ {i_draw:.0f} lane-instr per draw",
+            "traffic": None, "kernel": algo,
+            "peak_source": f"{n_sm} SMs x 128 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) "
+                           f"/ {i_draw:.0f} lane-instr per draw-test ({algo})",
+            "frac_vs_paper_loop": achieved / (issue / I_DRAW["simple"] / 1e9),
             "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3, "t_kernel_ms": kern_s * 1e3}
 
 

@@ -143,12 +143,13 @@ typedef struct {
     int32_t chunk;       /* TILED: draws tested per row before re-queueing it, one of
                             0 (auto: picked per tile from its effective sparsity
                             s = |x|_1 / M, Eq. 17), 4, 8, 16, 32 */
-    int32_t reserved[6]; /* must be zero */
+    int32_t algo_used;   /* OUTPUT: written by wmh_hash_ex with the kernel that ran (wmh_algo) */
+    int32_t reserved[5]; /* must be zero */
 } wmh_hash_opts;
 
 wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k,
                        uint32_t cap, int32_t sig_bytes, void *sig_out, uint64_t *n_saturated,
-                       const wmh_hash_opts *opts, void *stream);
+                       wmh_hash_opts *opts, void *stream);
 
 /* End-to-end convenience (the e2e path): rows and signatures in HOST memory
  * (pinned or pageable).  Copies the rows host->device into library scratch

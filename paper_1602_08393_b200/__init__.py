@@ -186,6 +186,9 @@ def prepare(rows: Rows | None = None, bounds: torch.Tensor | None = None, group=
     return Layout(h.value)
 
 
+last_algo = None     # name of the kernel the last hash() call ran ('simple' / 'tiled')
+
+
 def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
          algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
          chunk: int = 0, stream=None) -> torch.Tensor:
@@ -203,6 +206,8 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
     opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk)
     _lib.check(_lib.load().wmh_hash_ex(layout.handle, ctypes.byref(rows._c()), seed & (2**64 - 1), k, cap, sig_bytes,
                                        _ptr(out), _ptr(n_saturated), ctypes.byref(opts), _stream(stream)))
+    global last_algo
+    last_algo = {v: n for n, v in _lib.ALGOS.items()}.get(opts.algo_used, "?")
     return out
 
 

@@ -26,7 +26,8 @@ class WmhRows(ctypes.Structure):
 
 
 class WmhHashOpts(ctypes.Structure):
-    _fields_ = [("algo", ctypes.c_int32), ("chunk", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+    _fields_ = [("algo", ctypes.c_int32), ("chunk", ctypes.c_int32), ("algo_used", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
 class WmhError(RuntimeError):

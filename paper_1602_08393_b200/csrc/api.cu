@@ -128,7 +128,9 @@ static wmh_status validate_hash(const wmh_layout *L, const wmh_rows *rows, uint3
 }
 
 static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
-                                int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, int algo, int chunk, cudaStream_t s) {
+                                int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, int algo, int chunk, cudaStream_t s,
+                                int *algo_used) {
+    *algo_used = algo == WMH_ALGO_AUTO ? WMH_ALGO_SIMPLE : algo;
     if (rows->n_rows == 0) return WMH_OK;
     HashArgs a;
     a.L = L;
@@ -144,27 +146,32 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     if (algo == WMH_ALGO_AUTO || algo == WMH_ALGO_TILED) {
         bool handled = false;
         wmh_status st = launch_hash_tiled(a, &handled);
+        if (handled) *algo_used = WMH_ALGO_TILED;
         if (st != WMH_OK || handled) return st;
         if (algo == WMH_ALGO_TILED) { set_error("wmh_hash: the tiled kernel does not take this input shape"); return WMH_EINVAL; }
     }
+    *algo_used = WMH_ALGO_SIMPLE;
     return launch_hash_simple(a);
 }
 
 extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
-                                  int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, const wmh_hash_opts *opts,
+                                  int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, wmh_hash_opts *opts,
                                   void *stream) {
     wmh_status st = validate_hash(L, rows, k, cap, sig_bytes, sig_out, false);
     if (st != WMH_OK) return st;
     int algo = WMH_ALGO_AUTO, chunk = 0;
     if (opts) {
         algo = opts->algo;
-        for (int i = 0; i < 6; i++)
+        for (int i = 0; i < 5; i++)
             if (opts->reserved[i]) { set_error("wmh_hash_ex: reserved option fields must be zero"); return WMH_EINVAL; }
         chunk = opts->chunk;
         if (chunk != 0 && chunk != 4 && chunk != 8 && chunk != 16 && chunk != 32) { set_error("wmh_hash_ex: chunk=%d not in {0,4,8,16,32}", chunk); return WMH_EINVAL; }
         if (algo < WMH_ALGO_AUTO || algo > WMH_ALGO_TILED) { set_error("wmh_hash_ex: unknown algo %d", algo); return WMH_EINVAL; }
     }
-    return hash_dispatch(L, rows, seed, k, cap, sig_bytes, sig_out, n_saturated, algo, chunk, (cudaStream_t)stream);
+    int used = 0;
+    st = hash_dispatch(L, rows, seed, k, cap, sig_bytes, sig_out, n_saturated, algo, chunk, (cudaStream_t)stream, &used);
+    if (opts) opts->algo_used = used;
+    return st;
 }
 
 extern "C" wmh_status wmh_hash(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
@@ -231,7 +238,8 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
         d.val = base + off_val;
     }
     void *dsig = base + in_bytes;
-    st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, s);
+    int used = 0;
+    st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, s, &used);
     if (st != WMH_OK) return st;
     WMH_CUDA_TRY(cudaMemcpyAsync(sig_out_host, dsig, sig_bytes_total, cudaMemcpyDeviceToHost, s), "e2e D2H signatures");
     WMH_CUDA_TRY(cudaStreamSynchronize(s), "e2e synchronize");

@@ -80,5 +80,6 @@ struct HashArgs {
 
 wmh_status launch_hash_simple(const HashArgs &a);
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
+wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled);
 
 }  // namespace wmh

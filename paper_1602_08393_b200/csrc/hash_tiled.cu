@@ -362,7 +362,7 @@ static wmh_status launch_tiled(const TiledParams &p, size_t smem, int grid, cuda
 
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     *handled = false;
-    if (a.rows.kind != WMH_DENSE) return WMH_OK;          // CSR: simple kernel (tiled CSR is next)
+    if (a.rows.kind != WMH_DENSE) return launch_hash_tiled_csr(a, handled);
     const int D = (int)a.rows.dim;
     const int SW = (((D + 3) >> 2) | 1);                  // odd word stride: conflict-free lane=row tests
     int dev = 0;
