@@ -57,6 +57,20 @@ def workload(cfg_name: str, rank: int, n_rows: int | None):
     cfg = datagen.CONFIGS[cfg_name]
     n = cfg.n_rows if n_rows is None else n_rows
     lo, hi = rank * n, (rank + 1) * n
+    cache = os.environ.get("BENCH_CACHE_DIR")      # optional: reuse generated rows within one session
+    if cache and cfg.kind == "dense":
+        path = os.path.join(cache, f"{cfg_name}_{lo}_{hi}.npy")
+        if os.path.exists(path):
+            return cfg, n, datagen.Dense(np.load(path))
+    data = _generate(cfg_name, cfg, lo, hi)
+    if cache and cfg.kind == "dense":
+        os.makedirs(cache, exist_ok=True)
+        np.save(path, data.x)
+    return cfg, n, data
+
+
+def _generate(cfg_name, cfg, lo, hi):
+    import datagen
     if cfg_name == "c2":
         data = datagen.Dense(datagen.gen_c2_rows(cfg.data_seed, lo, hi, cfg.dim))
     elif cfg_name == "c1":
@@ -66,7 +80,7 @@ def workload(cfg_name: str, rank: int, n_rows: int | None):
     else:
         _, full = datagen.make(cfg_name, n_rows=hi)
         data = full.take(np.arange(lo, hi))
-    return cfg, n, data
+    return data
 
 
 def desc(cfg, n):

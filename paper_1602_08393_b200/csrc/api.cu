@@ -4,6 +4,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -180,69 +181,132 @@ extern "C" wmh_status wmh_hash(const wmh_layout *L, const wmh_rows *rows, uint64
 }
 
 // ------------------------------------------------------------- e2e entry
+// Host rows in, host signatures out.  The rows are cut into chunks that flow
+// through three internal streams -- H2D copy, hash, D2H copy -- so the PCIe
+// transfers of neighbouring chunks overlap each other and the kernels.
 namespace {
-struct HostScratch {
-    void *buf = nullptr;
-    size_t bytes = 0;
+constexpr int E2E_SLOTS = 3;
+
+struct E2EState {
     int device = -1;
-    ~HostScratch() { if (buf) cudaFree(buf); }
-    void *get(size_t need, wmh_status *st) {
+    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_in[E2E_SLOTS] = {}, ev_comp[E2E_SLOTS] = {}, ev_out[E2E_SLOTS] = {};
+    void *buf[E2E_SLOTS] = {};
+    size_t bytes[E2E_SLOTS] = {};
+
+    wmh_status init() {
         int dev = 0;
         cudaGetDevice(&dev);
-        if (buf && (bytes < need || dev != device)) { cudaFree(buf); buf = nullptr; bytes = 0; }
-        if (!buf) {
-            size_t want = need + need / 8 + 256;
-            if (cudaMalloc(&buf, want) != cudaSuccess) { *st = cuda_fail(cudaGetLastError(), "e2e scratch alloc"); return nullptr; }
-            bytes = want;
-            device = dev;
+        if (device == dev) return WMH_OK;
+        release();
+        WMH_CUDA_TRY(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "e2e stream");
+        WMH_CUDA_TRY(cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking), "e2e stream");
+        WMH_CUDA_TRY(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "e2e stream");
+        WMH_CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming), "e2e event");
+        for (int i = 0; i < E2E_SLOTS; i++) {
+            WMH_CUDA_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming), "e2e event");
+            WMH_CUDA_TRY(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming), "e2e event");
+            WMH_CUDA_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming), "e2e event");
         }
-        *st = WMH_OK;
-        return buf;
+        device = dev;
+        return WMH_OK;
     }
+    wmh_status reserve(int slot, size_t need) {
+        if (bytes[slot] >= need) return WMH_OK;
+        if (buf[slot]) { cudaStreamSynchronize(s_out); cudaFree(buf[slot]); buf[slot] = nullptr; bytes[slot] = 0; }
+        WMH_CUDA_TRY(cudaMalloc(&buf[slot], need), "e2e scratch alloc");
+        bytes[slot] = need;
+        return WMH_OK;
+    }
+    void release() {
+        if (device < 0) return;
+        for (int i = 0; i < E2E_SLOTS; i++) {
+            if (buf[i]) cudaFree(buf[i]);
+            buf[i] = nullptr;
+            bytes[i] = 0;
+            if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+            if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
+            if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+        }
+        if (ev_start) cudaEventDestroy(ev_start);
+        if (s_in) cudaStreamDestroy(s_in);
+        if (s_comp) cudaStreamDestroy(s_comp);
+        if (s_out) cudaStreamDestroy(s_out);
+        device = -1;
+    }
+    ~E2EState() { release(); }
 };
-thread_local HostScratch g_scratch;
+thread_local E2EState g_e2e;
 inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+__global__ void rebase_row_ptr(int64_t *rp, int64_t n, int64_t base) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        rp[i] -= base;
+}
 }  // namespace
 
 extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_host, uint64_t seed, uint32_t k,
                                     uint32_t cap, int32_t sig_bytes, void *sig_out_host, void *stream) {
     wmh_status st = validate_hash(L, rows_host, k, cap, sig_bytes, sig_out_host, true);
     if (st != WMH_OK) return st;
-    cudaStream_t s = (cudaStream_t)stream;
     const wmh_rows &h = *rows_host;
     if (h.n_rows == 0) return WMH_OK;
-    size_t sig_bytes_total = (size_t)h.n_rows * k * sig_bytes;
-    size_t in_bytes = 0, off_rp = 0, off_col = 0, off_val = 0;
-    if (h.kind == WMH_DENSE) {
-        in_bytes = align256((size_t)h.n_rows * h.dim);
-    } else {
-        off_rp = 0;
-        off_col = align256(sizeof(int64_t) * (h.n_rows + 1));
-        off_val = off_col + align256(sizeof(int32_t) * h.nnz);
-        in_bytes = off_val + align256(h.nnz);
-    }
-    uint8_t *base = (uint8_t *)g_scratch.get(in_bytes + sig_bytes_total, &st);
-    if (!base) return st;
-    wmh_rows d = h;
-    if (h.kind == WMH_DENSE) {
-        WMH_CUDA_TRY(cudaMemcpyAsync(base, h.dense, (size_t)h.n_rows * h.dim, cudaMemcpyHostToDevice, s), "e2e H2D rows");
-        d.dense = base;
-    } else {
-        WMH_CUDA_TRY(cudaMemcpyAsync(base + off_rp, h.row_ptr, sizeof(int64_t) * (h.n_rows + 1), cudaMemcpyHostToDevice, s), "e2e H2D row_ptr");
-        if (h.nnz) {
-            WMH_CUDA_TRY(cudaMemcpyAsync(base + off_col, h.col, sizeof(int32_t) * h.nnz, cudaMemcpyHostToDevice, s), "e2e H2D col");
-            WMH_CUDA_TRY(cudaMemcpyAsync(base + off_val, h.val, h.nnz, cudaMemcpyHostToDevice, s), "e2e H2D val");
+    E2EState &E = g_e2e;
+    if ((st = E.init()) != WMH_OK) return st;
+    // chunks of >= 2048 rows, <= 8 of them
+    const int64_t cr = std::max<int64_t>(2048, (h.n_rows + 7) / 8);
+    const int64_t n_chunks = (h.n_rows + cr - 1) / cr;
+    const size_t row_sig = (size_t)k * sig_bytes;
+    WMH_CUDA_TRY(cudaEventRecord(E.ev_start, (cudaStream_t)stream), "e2e start event");
+    WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_in, E.ev_start, 0), "e2e wait");
+    for (int64_t ci = 0; ci < n_chunks; ci++) {
+        const int slot = (int)(ci % E2E_SLOTS);
+        const int64_t a = ci * cr, b = std::min<int64_t>(h.n_rows, a + cr), nr = b - a;
+        size_t in_bytes, off_col = 0, off_val = 0;
+        int64_t e0 = 0, e1 = 0;
+        if (h.kind == WMH_DENSE) {
+            in_bytes = align256((size_t)nr * h.dim);
+        } else {
+            e0 = h.row_ptr[a];
+            e1 = h.row_ptr[b];
+            off_col = align256(sizeof(int64_t) * (nr + 1));
+            off_val = off_col + align256(sizeof(int32_t) * (e1 - e0));
+            in_bytes = off_val + align256((size_t)(e1 - e0));
         }
-        d.row_ptr = (const int64_t *)(base + off_rp);
-        d.col = (const int32_t *)(base + off_col);
-        d.val = base + off_val;
+        // the slot's previous chunk must have finished its D2H before reuse
+        WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_in, E.ev_out[slot], 0), "e2e wait");
+        if ((st = E.reserve(slot, in_bytes + nr * row_sig)) != WMH_OK) return st;
+        uint8_t *base = (uint8_t *)E.buf[slot];
+        wmh_rows d = h;
+        d.n_rows = nr;
+        if (h.kind == WMH_DENSE) {
+            WMH_CUDA_TRY(cudaMemcpyAsync(base, h.dense + a * h.dim, (size_t)nr * h.dim, cudaMemcpyHostToDevice, E.s_in), "e2e H2D rows");
+            d.dense = base;
+        } else {
+            WMH_CUDA_TRY(cudaMemcpyAsync(base, h.row_ptr + a, sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, E.s_in), "e2e H2D row_ptr");
+            if (e1 > e0) {
+                WMH_CUDA_TRY(cudaMemcpyAsync(base + off_col, h.col + e0, sizeof(int32_t) * (e1 - e0), cudaMemcpyHostToDevice, E.s_in), "e2e H2D col");
+                WMH_CUDA_TRY(cudaMemcpyAsync(base + off_val, h.val + e0, (size_t)(e1 - e0), cudaMemcpyHostToDevice, E.s_in), "e2e H2D val");
+            }
+            rebase_row_ptr<<<std::max<int64_t>(1, std::min<int64_t>(64, (nr + 256) / 256)), 256, 0, E.s_in>>>((int64_t *)base, nr + 1, e0);
+            WMH_LAUNCH_CHECK("e2e rebase");
+            d.row_ptr = (const int64_t *)base;
+            d.col = (const int32_t *)(base + off_col);
+            d.val = base + off_val;
+            d.nnz = e1 - e0;
+        }
+        WMH_CUDA_TRY(cudaEventRecord(E.ev_in[slot], E.s_in), "e2e event");
+        WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_comp, E.ev_in[slot], 0), "e2e wait");
+        void *dsig = base + in_bytes;
+        int used = 0;
+        st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, E.s_comp, &used);
+        if (st != WMH_OK) return st;
+        WMH_CUDA_TRY(cudaEventRecord(E.ev_comp[slot], E.s_comp), "e2e event");
+        WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_out, E.ev_comp[slot], 0), "e2e wait");
+        WMH_CUDA_TRY(cudaMemcpyAsync((uint8_t *)sig_out_host + a * row_sig, dsig, nr * row_sig, cudaMemcpyDeviceToHost, E.s_out), "e2e D2H signatures");
+        WMH_CUDA_TRY(cudaEventRecord(E.ev_out[slot], E.s_out), "e2e event");
     }
-    void *dsig = base + in_bytes;
-    int used = 0;
-    st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, s, &used);
-    if (st != WMH_OK) return st;
-    WMH_CUDA_TRY(cudaMemcpyAsync(sig_out_host, dsig, sig_bytes_total, cudaMemcpyDeviceToHost, s), "e2e D2H signatures");
-    WMH_CUDA_TRY(cudaStreamSynchronize(s), "e2e synchronize");
+    WMH_CUDA_TRY(cudaStreamSynchronize(E.s_out), "e2e synchronize");
     return WMH_OK;
 }
 

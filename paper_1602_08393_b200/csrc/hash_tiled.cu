@@ -26,7 +26,7 @@
 namespace wmh {
 
 constexpr int T0 = 256;                 // draws per hash kept in the per-launch table
-constexpr int STRAGGLERS = 6;           // pending rows at or below which a warp goes draw-parallel
+constexpr int STRAG_MAX = 16;           // max pending rows handled draw-parallel (threshold: p.strag)
 
 // Packed cell of draw r: (c << 8) | (r - CompToM[c])  (Alg. 5 in one value).
 __device__ __forceinline__ uint32_t cell_of(uint32_t r, const uint32_t *__restrict__ pack, uint32_t uni_m) {
@@ -58,6 +58,7 @@ struct TiledParams {
     uint32_t k, cap, M, uni_m;
     uint64_t S;
     int chunk;                  // 0 = auto
+    int strag;                  // pending rows at or below which a warp goes draw-parallel
     const uint2 *table;         // [k][T0] (c, off)
     const uint32_t *pack;
     void *sig;
@@ -88,7 +89,7 @@ struct HashCtx {
 
 // Row-parallel rounds over the warp's pending list (cur), C draws per
 // re-queue.  Returns the number of rows still pending (left in cur) and the
-// next round in *q; stops when <= STRAGGLERS rows remain or at the cap.
+// next round in *q; stops when <= p.strag rows remain or at the cap.
 template <int SIGB, int C>
 __device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const HashCtx &hx, const uint8_t *srow_bytes,
                                                    int SW4, const uint16_t *&cur, uint16_t *own0, uint16_t *own1,
@@ -96,7 +97,7 @@ __device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const H
     const int lane = threadIdx.x & 31;
     uint32_t q = *q_io;
     int flip = 0;
-    while (npend > STRAGGLERS && q * 32 < p.cap) {
+    while (npend > p.strag && q * 32 < p.cap) {
         const uint2 *src;
         if (q * 32 < (uint32_t)T0) {
             src = hx.buf + q * 32;
@@ -294,12 +295,12 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
                 }
                 npend = 0;
             }
-            // ---- draw-parallel mode for the last <= STRAGGLERS rows ---------------
+            // ---- draw-parallel mode for the last <= p.strag rows ------------------
             if (npend > 0) {
-                int rr[STRAGGLERS];
+                int rr[STRAG_MAX];
                 unsigned live = 0;
 #pragma unroll
-                for (int i = 0; i < STRAGGLERS; i++) {
+                for (int i = 0; i < STRAG_MAX; i++) {
                     rr[i] = i < npend ? (int)cur[i] : 0;
                     if (i < npend) live |= 1u << i;
                 }
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
                     const uint2 cell = t < (uint32_t)T0 ? sbuf[t] : late_cell(p, hx.keyj, t);
                     const uint32_t c = cell.x, off = t < p.cap ? cell.y : 0xFFFFFFFFu;
 #pragma unroll
-                    for (int i = 0; i < STRAGGLERS; i++) {
+                    for (int i = 0; i < STRAG_MAX; i++) {
                         if (live & (1u << i)) {
                             const uint32_t v = srow_bytes[rr[i] * SW4 + c];
                             const unsigned g = __ballot_sync(0xFFFFFFFFu, v > off);
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < STRAGGLERS; i++)
+                for (int i = 0; i < STRAG_MAX; i++)
                     if ((live & (1u << i)) && lane == 0) {
                         store_sig<SIGB>(p.sig, (row0 + rr[i]) * (int64_t)p.k + j, p.cap);
                         sat++;
@@ -372,7 +373,8 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     // Two 256-thread CTAs per SM when a >= 32-row tile fits twice, else one
     // 512-thread CTA with the largest tile that fits.
-    int ctas = 2, NT = 256, R = 0;
+    static const int force_ctas = getenv("WMH_TILED_CTAS") ? atoi(getenv("WMH_TILED_CTAS")) : 0;
+    int ctas = force_ctas == 1 ? 1 : 2, NT = 256, R = 0;
     for (; ctas >= 1; ctas--) {
         NT = ctas == 2 ? 256 : 512;
         size_t budget = min((size_t)smem_optin, (size_t)smem_sm / ctas - 1024);
@@ -424,6 +426,8 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     p.uni_m = uni_m;
     p.S = a.S;
     p.chunk = a.chunk;
+    static const int strag_env = getenv("WMH_TILED_STRAG") ? atoi(getenv("WMH_TILED_STRAG")) : -1;
+    p.strag = strag_env >= 0 ? min(strag_env, STRAG_MAX) : 6;
     p.table = table;
     p.pack = a.L->cell_pack;
     p.sig = a.sig;
