@@ -176,6 +176,10 @@ const char *wmh_last_error(void);
 /* Library version string, e.g. "wmh 0.1 sm_100a". */
 const char *wmh_version(void);
 
+/* Number of CUDA kernels this library has launched in the process so far
+ * (all entry points; a monotone counter for launch accounting in benchmarks). */
+uint64_t wmh_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

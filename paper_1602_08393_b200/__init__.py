@@ -245,3 +245,8 @@ def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, st
 
 def version() -> str:
     return _lib.load().wmh_version().decode()
+
+
+def kernel_launches() -> int:
+    """How many CUDA kernels libwmh.so has launched in this process."""
+    return int(_lib.load().wmh_kernel_launches())

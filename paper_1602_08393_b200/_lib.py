@@ -16,7 +16,8 @@ STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 
 
 # Every symbol include/wmh.h declares (tests check the .so exports all of them).
 EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_tables", "wmh_layout_free",
-           "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version"]
+           "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version",
+           "wmh_kernel_launches"]
 
 
 class WmhRows(ctypes.Structure):
@@ -66,6 +67,7 @@ def load() -> ctypes.CDLL:
             "wmh_collide": (st, [vp, i32, u32, i64, vp, i64, vp, vp, i32, vp]),
             "wmh_last_error": (ctypes.c_char_p, []),
             "wmh_version": (ctypes.c_char_p, []),
+            "wmh_kernel_launches": (ctypes.c_uint64, []),
         }
         for name, (res, args) in proto.items():
             f = getattr(L, name)

@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -25,6 +26,9 @@ wmh_status cuda_fail(cudaError_t e, const char *what) {
     set_error("%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? WMH_ENOMEM : WMH_ECUDA;
 }
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int num_sms() {
     static int cached[64] = {0};
@@ -346,3 +350,5 @@ extern "C" wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k
 extern "C" const char *wmh_last_error(void) { return g_err; }
 
 extern "C" const char *wmh_version(void) { return "wmh 0.1 sm_100a"; }
+
+extern "C" uint64_t wmh_kernel_launches(void) { return wmh::g_launches.load(std::memory_order_relaxed); }

@@ -32,7 +32,14 @@ wmh_status cuda_fail(cudaError_t e, const char *what);
         cudaError_t _e = (expr);                                  \
         if (_e != cudaSuccess) return ::wmh::cuda_fail(_e, what); \
     } while (0)
-#define WMH_LAUNCH_CHECK(what) WMH_CUDA_TRY(cudaGetLastError(), what)
+// Every kernel launch site is followed by WMH_LAUNCH_CHECK, which also counts
+// the launch (wmh_kernel_launches()).
+void count_launch(unsigned n = 1);
+#define WMH_LAUNCH_CHECK(what)                   \
+    do {                                         \
+        ::wmh::count_launch();                   \
+        WMH_CUDA_TRY(cudaGetLastError(), what);  \
+    } while (0)
 
 wmh_status check_rows(const wmh_rows *rows, bool need_data);
 int num_sms();

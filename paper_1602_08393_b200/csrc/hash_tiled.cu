@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
         int C = p.chunk;
         if (C == 0) {                   // C from the tile's effective sparsity
             const double s = nalive ? (double)s_xsum / ((double)nalive * (double)p.M) : 1.0;
-            C = s > 0.15 ? 4 : s > 0.08 ? 8 : s > 0.02 ? 16 : 32;
+            C = s > 0.2 ? 8 : s > 0.1 ? 16 : 32;
             if (p.stats && threadIdx.x == 0) atomicAdd(p.stats + 5, (unsigned long long)(s * 1e9));
         }
         if (p.stats && threadIdx.x == 0) atomicAdd(p.stats + (31 - __clz(C)) - 2, 1ull);
@@ -371,10 +371,11 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     int smem_optin = 0, smem_sm = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    // Two 256-thread CTAs per SM when a >= 32-row tile fits twice, else one
-    // 512-thread CTA with the largest tile that fits.
     static const int force_ctas = getenv("WMH_TILED_CTAS") ? atoi(getenv("WMH_TILED_CTAS")) : 0;
-    int ctas = force_ctas == 1 ? 1 : 2, NT = 256, R = 0;
+    // One 512-thread CTA per SM with the largest tile that fits (measured
+    // faster than two 256-thread CTAs with half-size tiles); WMH_TILED_CTAS=2
+    // selects the latter.
+    int ctas = force_ctas == 2 ? 2 : 1, NT = 256, R = 0;
     for (; ctas >= 1; ctas--) {
         NT = ctas == 2 ? 256 : 512;
         size_t budget = min((size_t)smem_optin, (size_t)smem_sm / ctas - 1024);
@@ -427,7 +428,7 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     p.S = a.S;
     p.chunk = a.chunk;
     static const int strag_env = getenv("WMH_TILED_STRAG") ? atoi(getenv("WMH_TILED_STRAG")) : -1;
-    p.strag = strag_env >= 0 ? min(strag_env, STRAG_MAX) : 6;
+    p.strag = strag_env >= 0 ? min(strag_env, STRAG_MAX) : 4;
     p.table = table;
     p.pack = a.L->cell_pack;
     p.sig = a.sig;

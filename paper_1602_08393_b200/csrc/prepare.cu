@@ -296,6 +296,7 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     scan_block_sums<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, mnmx, mnmx + 1);
     scan_sums_single<<<1, SCAN_B, 0, s>>>(sums, nb, Mdev);
     scan_apply<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, Mdev, L->comp_to_m);
+    count_launch(3 + ((rows && rows->n_rows > 0) ? 1 : 0));
     if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(scr, s); return fail(cuda_fail(cudaGetLastError(), "prepare scan launch")); }
 
     unsigned long long host[4];
@@ -332,6 +333,7 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     }
     int64_t blocks = min((int64_t)sms * 16, (dim * 32 + 255) / 256);
     fill_int_to_comp<<<(unsigned)blocks, 256, 0, s>>>(L->comp_to_m, dim, L->int_to_comp, L->cell_pack);
+    count_launch();
     if (cudaGetLastError() != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "fill IntToComp launch"));
     *out = L;
     return WMH_OK;
