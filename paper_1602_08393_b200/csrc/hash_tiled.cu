@@ -132,12 +132,21 @@ __device__ __forceinline__ int rounds_row_parallel(const TiledParams &p, const H
                 const int r = active ? cur[i] : 0;
                 uint32_t h = C;
                 if (active) {
+                    // first green among the C draws: NCH independent select
+                    // chains over interleaved draws (ILP), combined by min.
+                    constexpr int NCH = C >= 16 ? 4 : 2;
                     const uint8_t *row = srow_bytes + r * SW4;
+                    uint32_t hc[NCH];
+#pragma unroll
+                    for (int c = 0; c < NCH; c++) hc[c] = C;
 #pragma unroll
                     for (int tt = C - 1; tt >= 0; tt--) {
                         const uint32_t v = row[dc[tt]];
-                        h = (v > doff[tt]) ? (uint32_t)tt : h;
+                        hc[tt % NCH] = (v > doff[tt]) ? (uint32_t)tt : hc[tt % NCH];
                     }
+                    h = hc[0];
+#pragma unroll
+                    for (int c = 1; c < NCH; c++) h = min(h, hc[c]);
                 }
                 const bool still = active && h == C;
                 if (active && !still)
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
     uint16_t *spend_all = reinterpret_cast<uint16_t *>(swin_all + NW * 32);   // [NW][2][R]
     uint16_t *salive = spend_all + NW * 2 * R;                          // [R] alive row list
     uint8_t *sflag = reinterpret_cast<uint8_t *>(salive + R);           // [R] row has |x|_1 > 0
-    __shared__ long long s_item;
+    __shared__ long long s_item, s_next;
     __shared__ int s_hash, s_nalive;
     __shared__ unsigned long long s_xsum;
 
@@ -178,11 +187,13 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
     const uint8_t *srow_bytes = reinterpret_cast<const uint8_t *>(srows);
     unsigned long long sat = 0;
     const bool vec16 = (p.D % 16 == 0) && ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(p.item_ctr, 1ull);
 
     for (;;) {
         __syncthreads();                                    // previous item fully done with smem
         if (threadIdx.x == 0) {
-            s_item = (long long)atomicAdd(p.item_ctr, 1ull);
+            s_item = s_next;                                // claimed one item ahead
+            s_next = (long long)atomicAdd(p.item_ctr, 1ull);
             s_hash = 0;
             s_xsum = 0;
             s_nalive = 0;
@@ -190,6 +201,13 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hash_tiled_dense_kern
         __syncthreads();
         const long long item = s_item;
         if (item >= p.n_items) break;
+        if (s_next < p.n_items) {                           // warm L2 with the next item's rows
+            const int64_t nrow0 = (s_next / p.n_hchunks) * R;
+            const int64_t nbytes = min((int64_t)R, p.n_rows - nrow0) * (int64_t)p.D;
+            const char *base = reinterpret_cast<const char *>(p.x + nrow0 * (int64_t)p.D);
+            for (int64_t off = (int64_t)threadIdx.x * 128; off < nbytes; off += (int64_t)NT * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        }
         const int64_t tile = item / p.n_hchunks;
         const int hc = (int)(item % p.n_hchunks);
         const int64_t row0 = tile * R;
@@ -380,7 +398,7 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
         NT = ctas == 2 ? 256 : 512;
         size_t budget = min((size_t)smem_optin, (size_t)smem_sm / ctas - 1024);
         R = 256;
-        while (R >= 32 && tiled_smem(R, SW, NT / 32) > budget) R -= 16;
+        while (R >= 32 && tiled_smem(R, SW, NT / 32) > budget) R -= 4;   // R % 4 == 0 keeps sbuf 16B-aligned
         if (R >= 32) break;
     }
     if (R < 32) return WMH_OK;                            // rows too long for a 32-row tile
