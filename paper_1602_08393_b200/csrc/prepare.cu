@@ -8,32 +8,57 @@
 namespace wmh {
 
 // ------------------------------------------------------------ a1: colmax
-// Dense: each thread owns 16 consecutive columns (one uint4 per row) and a
-// slice of rows; per-byte max with __vmaxu4, then one atomicMax per column.
-// Reads N*D bytes once (HBM-bound).
-__global__ void colmax_dense_vec16(const uint8_t *__restrict__ x, int64_t n_rows, int64_t dim,
-                                   int64_t rows_per_slice, uint32_t *__restrict__ colmax) {
-    const int64_t nvec = dim / 16;
-    const int64_t cv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (cv >= nvec) return;
-    const int64_t r0 = (int64_t)blockIdx.y * rows_per_slice;
-    const int64_t r1 = min(n_rows, r0 + rows_per_slice);
+// Dense, 16-byte vectors: a 256-thread block owns a contiguous row range; its
+// threads are (row phase g, column vector v) with V = D/16 vectors per row and
+// G = 256 / V row phases, so consecutive threads read consecutive 16 B of a
+// row (coalesced) and each thread keeps a per-byte running max (__vmaxu4)
+// over rows g, g+G, ... with 4 loads in flight.  The G phases are merged in
+// shared memory, then one atomicMax per nonzero column per block.  Reads
+// N*D bytes once (HBM-bound).  Requires V <= 256.
+__global__ void __launch_bounds__(256) colmax_dense_vec16(const uint8_t *__restrict__ x, int64_t n_rows,
+                                                          int64_t dim, int64_t rows_per_block,
+                                                          uint32_t *__restrict__ colmax) {
+    __shared__ uint4 part[256];
+    const int V = (int)(dim / 16), G = 256 / V;
+    const int v = threadIdx.x % V, g = threadIdx.x / V;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t r1 = min(n_rows, r0 + rows_per_block);
     uint4 acc = make_uint4(0, 0, 0, 0);
-    for (int64_t n = r0; n < r1; n++) {
-        uint4 v = __ldg(reinterpret_cast<const uint4 *>(x + n * dim) + cv);
-        acc.x = __vmaxu4(acc.x, v.x);
-        acc.y = __vmaxu4(acc.y, v.y);
-        acc.z = __vmaxu4(acc.z, v.z);
-        acc.w = __vmaxu4(acc.w, v.w);
-    }
-    uint32_t w[4] = {acc.x, acc.y, acc.z, acc.w};
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-            uint32_t v = (w[q] >> (8 * b)) & 0xFFu;
-            if (v) atomicMax(&colmax[cv * 16 + q * 4 + b], v);
+    if (g < G) {
+        const uint4 *base = reinterpret_cast<const uint4 *>(x) + v;
+        const int64_t stride = (int64_t)V;            // uint4s per row
+        int64_t n = r0 + g;
+        for (; n + 3 * G < r1; n += 4 * G) {
+            const uint4 a = __ldg(base + n * stride), b = __ldg(base + (n + G) * stride);
+            const uint4 c = __ldg(base + (n + 2 * G) * stride), d = __ldg(base + (n + 3 * G) * stride);
+            acc.x = __vmaxu4(__vmaxu4(acc.x, a.x), __vmaxu4(__vmaxu4(b.x, c.x), d.x));
+            acc.y = __vmaxu4(__vmaxu4(acc.y, a.y), __vmaxu4(__vmaxu4(b.y, c.y), d.y));
+            acc.z = __vmaxu4(__vmaxu4(acc.z, a.z), __vmaxu4(__vmaxu4(b.z, c.z), d.z));
+            acc.w = __vmaxu4(__vmaxu4(acc.w, a.w), __vmaxu4(__vmaxu4(b.w, c.w), d.w));
         }
+        for (; n < r1; n += G) {
+            const uint4 a = __ldg(base + n * stride);
+            acc.x = __vmaxu4(acc.x, a.x); acc.y = __vmaxu4(acc.y, a.y);
+            acc.z = __vmaxu4(acc.z, a.z); acc.w = __vmaxu4(acc.w, a.w);
+        }
+    }
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (g == 0) {
+        for (int q = 1; q < G; q++) {
+            const uint4 o = part[q * V + v];
+            acc.x = __vmaxu4(acc.x, o.x); acc.y = __vmaxu4(acc.y, o.y);
+            acc.z = __vmaxu4(acc.z, o.z); acc.w = __vmaxu4(acc.w, o.w);
+        }
+        const uint32_t w[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const uint32_t m = (w[q] >> (8 * b)) & 0xFFu;
+                if (m) atomicMax(&colmax[(int64_t)v * 16 + q * 4 + b], m);
+            }
+    }
 }
 
 // Generic byte path (any dim / alignment).
@@ -220,20 +245,22 @@ extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *s
     if (rows->n_rows == 0) return WMH_OK;
     if (rows->kind == WMH_DENSE) {
         const int sms = num_sms();
-        bool vec = (rows->dim % 16 == 0) && ((uintptr_t)rows->dense % 16 == 0);
-        int64_t cols_units = vec ? rows->dim / 16 : rows->dim;
-        int threads = 128;
-        int64_t gx = (cols_units + threads - 1) / threads;
-        int64_t want_blocks = (int64_t)sms * 8;
-        int64_t gy = max((int64_t)1, min(rows->n_rows, want_blocks / max((int64_t)1, gx)));
-        gy = min(gy, (int64_t)65535);
-        int64_t per = (rows->n_rows + gy - 1) / gy;
-        gy = (rows->n_rows + per - 1) / per;
-        dim3 grid((unsigned)gx, (unsigned)gy);
-        if (vec)
-            colmax_dense_vec16<<<grid, threads, 0, s>>>(rows->dense, rows->n_rows, rows->dim, per, colmax);
-        else
-            colmax_dense_bytes<<<grid, threads, 0, s>>>(rows->dense, rows->n_rows, rows->dim, per, colmax);
+        const bool vec = (rows->dim % 16 == 0) && (rows->dim / 16 <= 256) && ((uintptr_t)rows->dense % 16 == 0);
+        if (vec) {
+            const int64_t blocks = min(rows->n_rows, (int64_t)sms * 16);
+            const int64_t per = (rows->n_rows + blocks - 1) / blocks;
+            colmax_dense_vec16<<<(unsigned)((rows->n_rows + per - 1) / per), 256, 0, s>>>(rows->dense, rows->n_rows,
+                                                                                     rows->dim, per, colmax);
+        } else {
+            const int threads = 128;
+            const int64_t gx = (rows->dim + threads - 1) / threads;
+            int64_t gy = max((int64_t)1, min(rows->n_rows, (int64_t)sms * 8 / max((int64_t)1, gx)));
+            gy = min(gy, (int64_t)65535);
+            const int64_t per = (rows->n_rows + gy - 1) / gy;
+            gy = (rows->n_rows + per - 1) / per;
+            colmax_dense_bytes<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, s>>>(rows->dense, rows->n_rows,
+                                                                                  rows->dim, per, colmax);
+        }
     } else {
         if (rows->nnz > 0) {
             int64_t blocks = min((int64_t)num_sms() * 16, (rows->nnz + 255) / 256);
