@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(256) colmax_dense_vec16(const uint8_t *__restr
 #pragma unroll
             for (int b = 0; b < 4; b++) {
                 const uint32_t m = (w[q] >> (8 * b)) & 0xFFu;
-                if (m) atomicMax(&colmax[(int64_t)v * 16 + q * 4 + b], m);
+                uint32_t *dst = &colmax[(int64_t)v * 16 + q * 4 + b];
+                if (m > *((volatile uint32_t *)dst)) atomicMax(dst, m);   // skip when already reached
             }
     }
 }
@@ -91,6 +92,13 @@ __global__ void check_dense_bounds(const uint8_t *__restrict__ x, int64_t n_rows
     for (int64_t n = blockIdx.x; n < n_rows; n += gridDim.x)
         for (int64_t c = threadIdx.x; c < dim; c += blockDim.x)
             if (x[n * dim + c] > bounds[c]) atomicMin(first_bad, (unsigned long long)(n * dim + c));
+}
+
+// Any column whose maximum exceeds its bound marks *bad (exact location later).
+__global__ void colmax_exceeds(const uint32_t *__restrict__ cm, const uint32_t *__restrict__ bounds, int64_t dim,
+                               unsigned long long *bad) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < dim && cm[c] > bounds[c]) atomicMin(bad, (unsigned long long)c);
 }
 
 // One warp per row: row_ptr monotone, columns in range and strictly
@@ -247,7 +255,7 @@ extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *s
         const int sms = num_sms();
         const bool vec = (rows->dim % 16 == 0) && (rows->dim / 16 <= 256) && ((uintptr_t)rows->dense % 16 == 0);
         if (vec) {
-            const int64_t blocks = min(rows->n_rows, (int64_t)sms * 16);
+            const int64_t blocks = min(rows->n_rows, (int64_t)sms * 4);
             const int64_t per = (rows->n_rows + blocks - 1) / blocks;
             colmax_dense_vec16<<<(unsigned)((rows->n_rows + per - 1) / per), 256, 0, s>>>(rows->dense, rows->n_rows,
                                                                                      rows->dim, per, colmax);
@@ -300,9 +308,9 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
         return fail(cuda_fail(cudaGetLastError(), "copy bounds"));
 
     const int64_t nb = (dim + SCAN_B - 1) / SCAN_B;
-    // scratch: sums[nb], M, first_bad, mn, mx
+    // scratch: sums[nb], M, first_bad, mn, mx, colmax[dim] (dense validation)
     unsigned long long *scr = nullptr;
-    size_t scr_bytes = sizeof(unsigned long long) * (nb + 4);
+    size_t scr_bytes = sizeof(unsigned long long) * (nb + 4) + sizeof(uint32_t) * dim;
     if (cudaMallocAsync((void **)&scr, scr_bytes, s) != cudaSuccess) {
         set_error("wmh_prepare: scratch alloc failed");
         return fail(WMH_ENOMEM);
@@ -314,9 +322,14 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
 
     const int sms = num_sms();
     if (rows && rows->n_rows > 0) {
-        if (rows->kind == WMH_DENSE)
-            check_dense_bounds<<<sms * 8, 256, 0, s>>>(rows->dense, rows->n_rows, dim, L->bounds, bad);
-        else
+        if (rows->kind == WMH_DENSE) {
+            // fast path: column maxima (one HBM pass) against the bounds; the
+            // exact first offender is located only when a column fails
+            uint32_t *cm = reinterpret_cast<uint32_t *>(scr + nb + 4);
+            wmh_status cst = wmh_colmax(rows, cm, stream);
+            if (cst != WMH_OK) { cudaFreeAsync(scr, s); return fail(cst); }
+            colmax_exceeds<<<(unsigned)((dim + 255) / 256), 256, 0, s>>>(cm, L->bounds, dim, bad);
+        } else
             check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, rows->val, rows->n_rows, dim, rows->nnz,
                                               L->bounds, bad);
     }
@@ -337,7 +350,17 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     if (mx > 255) { set_error("wmh_prepare: a bound is %u > 255 (weights are uint8)", mx); return fail(WMH_EINVAL); }
     if (first_bad != ~0ull) {
         if (rows->kind == WMH_DENSE) {
-            long long r = (long long)(first_bad / (unsigned long long)dim), c = (long long)(first_bad % (unsigned long long)dim);
+            // slow path: locate the first offending (row, col)
+            unsigned long long *b2 = nullptr, fb = ~0ull;
+            if (cudaMallocAsync((void **)&b2, sizeof fb, s) != cudaSuccess) return fail(WMH_ENOMEM);
+            cudaMemcpyAsync(b2, &fb, sizeof fb, cudaMemcpyHostToDevice, s);
+            check_dense_bounds<<<sms * 8, 256, 0, s>>>(rows->dense, rows->n_rows, dim, L->bounds, b2);
+            count_launch();
+            cudaMemcpyAsync(&fb, b2, sizeof fb, cudaMemcpyDeviceToHost, s);
+            cudaError_t e3 = cudaStreamSynchronize(s);
+            cudaFreeAsync(b2, s);
+            if (e3 != cudaSuccess) return fail(cuda_fail(e3, "prepare bound check"));
+            long long r = (long long)(fb / (unsigned long long)dim), c = (long long)(fb % (unsigned long long)dim);
             set_error("wmh_prepare: weight x[%lld][%lld] exceeds its bound", r, c);
             return fail(WMH_EBOUND);
         }
