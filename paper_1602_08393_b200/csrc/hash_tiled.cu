@@ -26,7 +26,7 @@
 namespace wmh {
 
 constexpr int T0 = 256;                 // draws per hash kept in the per-launch table
-constexpr int STRAG_MAX = 16;           // max pending rows handled draw-parallel (threshold: p.strag)
+constexpr int STRAG_MAX = 4;            // max pending rows handled draw-parallel (threshold: p.strag)
 
 // Packed cell of draw r: (c << 8) | (r - CompToM[c])  (Alg. 5 in one value).
 __device__ __forceinline__ uint32_t cell_of(uint32_t r, const uint32_t *__restrict__ pack, uint32_t uni_m) {

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrPara
     uint32_t *bm = reinterpret_cast<uint32_t *>(slots + H);                    // [bm_words]
     uint32_t *best_all = bm + p.bm_words;                                      // [NW][RB]
     uint32_t *found_all = best_all + CSR_NW * CSR_RB;                          // [NW]
-    uint16_t *trow = reinterpret_cast<uint16_t *>(found_all + CSR_NW);         // [RB+1] sub-tile starts
+    uint2 *hq_all = reinterpret_cast<uint2 *>(found_all + CSR_NW);             // [NW][64] queued hot draws
+    uint16_t *trow = reinterpret_cast<uint16_t *>(hq_all + CSR_NW * 64);       // [RB+1] sub-tile starts
     uint8_t *alive = reinterpret_cast<uint8_t *>(trow + CSR_RB + 2);           // [RB]
     __shared__ long long s_item;
     __shared__ int s_ntiles, s_hash, s_nalive;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrPara
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *best = best_all + warp * CSR_RB;
     volatile uint32_t *found = found_all + warp;
+    uint2 *hq = hq_all + warp * 64;
     unsigned long long sat = 0;
 
     for (;;) {
@@ -191,25 +193,41 @@ __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrPara
                 if (lane == 0) *found = 0;
                 __syncwarp();
                 const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
-                for (uint32_t t0 = 0; t0 < p.cap && (int)*found < nalive; t0 += 32) {
-                    const uint32_t t = t0 + lane;
-                    const uint32_t r = mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M);
-                    const uint32_t bk = r >> p.bshift;
-                    const bool hot = t < p.cap && ((bm[bk >> 5] >> (bk & 31)) & 1u);
-                    if (hot) {
-                        const uint32_t cell = csr_cell(p, r);
+                // Draws that pass the bucket filter are queued (per warp) and
+                // resolved 32 at a time, so the exact check -- an L2 lookup of
+                // the packed cell and a table probe -- runs with every lane busy.
+                // The first green per row is a min over t, so order is free.
+                auto resolve = [&](int count) {
+                    if (lane < count) {
+                        const uint2 q = hq[lane];                     // (r, t)
+                        const uint32_t cell = csr_cell(p, q.x);
                         const uint32_t c = cell >> 8, off = cell & 0xFFu;
                         for (uint32_t s = col_hash(c, p.hbits);; s = (s + 1) & (H - 1)) {
                             const unsigned long long e = slots[s];
                             if (e == CSR_EMPTY) break;
                             if ((uint32_t)(e >> 24) == c && (uint32_t)(e & 0xFFu) > off) {
                                 const uint32_t row = (uint32_t)(e >> 8) & 0xFFFFu;
-                                if (atomicMin(&best[row], t) == 0xFFFFFFFFu) atomicAdd((uint32_t *)found, 1u);
+                                if (atomicMin(&best[row], q.y) == 0xFFFFFFFFu) atomicAdd((uint32_t *)found, 1u);
                             }
                         }
                     }
                     __syncwarp();
+                    if (lane < 32 && count < 64) hq[lane] = hq[lane + 32];   // keep the overflow
+                    __syncwarp();
+                };
+                int qn = 0;
+                for (uint32_t t0 = 0; t0 < p.cap && (int)*found < nalive; t0 += 32) {
+                    const uint32_t t = t0 + lane;
+                    const uint32_t r = mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M);
+                    const uint32_t bk = r >> p.bshift;
+                    const bool hot = t < p.cap && ((bm[bk >> 5] >> (bk & 31)) & 1u);
+                    const unsigned hm = __ballot_sync(0xFFFFFFFFu, hot);
+                    if (hot) hq[qn + __popc(hm & ((1u << lane) - 1))] = make_uint2(r, t);
+                    qn += __popc(hm);
+                    __syncwarp();
+                    if (qn >= 32) { resolve(32); qn -= 32; }
                 }
+                if (qn > 0) resolve(qn);                              // flush (the loop may end early)
                 // ---- a9: first green t + 1, or the cap ----------------------------
                 for (int i = lane; i < nt_rows; i += 32) {
                     const uint32_t bt = best[i];
@@ -239,7 +257,8 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     int bshift = 0;
     while (((uint64_t)M + (1ull << bshift) - 1) >> bshift > (1ull << 19)) bshift++;
     const int bm_words = (int)((((uint64_t)M + (1ull << bshift) - 1) >> bshift) + 31) / 32;
-    const size_t fixed = (size_t)bm_words * 4 + (size_t)CSR_NW * CSR_RB * 4 + CSR_NW * 4 + (CSR_RB + 2) * 2 + CSR_RB + 64;
+    const size_t fixed = (size_t)bm_words * 4 + (size_t)CSR_NW * CSR_RB * 4 + CSR_NW * 4 + (size_t)CSR_NW * 64 * 8 +
+                         (CSR_RB + 2) * 2 + CSR_RB + 64;
     if ((size_t)smem_optin < fixed + 8 * 1024) return WMH_OK;
     int hbits = 0;
     while (((size_t)8 << (hbits + 1)) + fixed <= (size_t)smem_optin) hbits++;
@@ -254,13 +273,15 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     p.val = a.rows.val;
     p.n_rows = a.rows.n_rows;
     const double avg = a.rows.n_rows ? (double)a.rows.nnz / (double)a.rows.n_rows : 1.0;
-    p.cap_nnz = (int)(H * 0.7);
+    p.cap_nnz = (int)(H * 0.6);
     int rb = (int)min(256.0, max(32.0, 8.0 * p.cap_nnz / max(avg, 1.0)));
     rb = (rb + 31) / 32 * 32;
     p.rb = min(rb, CSR_RB);
     p.n_blocks = (a.rows.n_rows + p.rb - 1) / p.rb;
     const int sms = num_sms();
-    int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 16, ((int64_t)sms * 6 + p.n_blocks - 1) / p.n_blocks));
+    // hash chunks: enough items to balance the SMs, but >= 4 hashes per warp so
+    // the warps of a CTA stay busy between the per-sub-tile barriers
+    int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / (4 * CSR_NW), ((int64_t)sms * 6 + p.n_blocks - 1) / p.n_blocks));
     const int hchunk = (int)((a.k + n_hchunks - 1) / n_hchunks);
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
     p.n_hchunks = n_hchunks;
