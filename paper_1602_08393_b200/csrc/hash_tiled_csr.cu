@@ -256,7 +256,8 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     // cell-bucket filter: <= 2^19 bits (64 KB)
     int bshift = 0;
     while (((uint64_t)M + (1ull << bshift) - 1) >> bshift > (1ull << 19)) bshift++;
-    const int bm_words = (int)((((uint64_t)M + (1ull << bshift) - 1) >> bshift) + 31) / 32;
+    // bitmap words rounded to 16 B so the arrays after it stay 8/16-byte aligned
+    const int bm_words = (((int)((((uint64_t)M + (1ull << bshift) - 1) >> bshift) + 31) / 32) + 3) & ~3;
     const size_t fixed = (size_t)bm_words * 4 + (size_t)CSR_NW * CSR_RB * 4 + CSR_NW * 4 + (size_t)CSR_NW * 64 * 8 +
                          (CSR_RB + 2) * 2 + CSR_RB + 64;
     if ((size_t)smem_optin < fixed + 8 * 1024) return WMH_OK;
