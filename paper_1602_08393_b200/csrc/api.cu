@@ -148,7 +148,10 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     a.n_sat = reinterpret_cast<unsigned long long *>(n_saturated);
     a.stream = s;
     a.chunk = chunk;
-    if (algo == WMH_ALGO_AUTO || algo == WMH_ALGO_TILED) {
+    // tiny batches (<= 2^20 row-hash pairs, e.g. config c1) are launch-bound:
+    // the single-launch SIMPLE kernel beats the table + tiled pair there
+    const bool tiny = (unsigned long long)rows->n_rows * k <= (1ull << 20);
+    if (algo == WMH_ALGO_TILED || (algo == WMH_ALGO_AUTO && !tiny)) {
         bool handled = false;
         wmh_status st = launch_hash_tiled(a, &handled);
         if (handled) *algo_used = WMH_ALGO_TILED;

@@ -72,6 +72,21 @@ __device__ __forceinline__ uint32_t draw_r(uint64_t S, uint32_t j, uint32_t t, u
     return mulhi_range(splitmix64(key), M);
 }
 
+// ------------------------------------------------- draws shared by a tile
+constexpr int T0 = 256;                 // draws per hash kept in the per-launch table
+
+// Packed cell of draw r: (c << 8) | (r - CompToM[c]) -- Alg. 5's two lookups in
+// one value (bounds <= 255).  Uniform bounds: IntToComp[r] = r / m.
+__device__ __forceinline__ uint32_t cell_of(uint32_t r, const uint32_t *__restrict__ pack, uint32_t uni_m) {
+    if (uni_m) {
+        uint32_t c = r / uni_m;
+        return (c << 8) | (r - c * uni_m);
+    }
+    return __ldg(pack + r);
+}
+
+__device__ __forceinline__ uint2 unpack_cell(uint32_t cell) { return make_uint2(cell >> 8, cell & 0xFFu); }
+
 // ------------------------------------------------------------ launchers
 struct HashArgs {
     const wmh_layout *L;
@@ -88,5 +103,8 @@ struct HashArgs {
 wmh_status launch_hash_simple(const HashArgs &a);
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled);
+wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled);
+wmh_status launch_draw_table(uint2 *table, uint32_t k, uint64_t S, uint32_t M, const uint32_t *pack, uint32_t uni_m,
+                             uint32_t cmul, cudaStream_t s);
 
 }  // namespace wmh

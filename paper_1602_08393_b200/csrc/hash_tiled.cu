@@ -25,28 +25,27 @@
 
 namespace wmh {
 
-constexpr int T0 = 256;                 // draws per hash kept in the per-launch table
 constexpr int STRAG_MAX = 4;            // max pending rows handled draw-parallel (threshold: p.strag)
 
-// Packed cell of draw r: (c << 8) | (r - CompToM[c])  (Alg. 5 in one value).
-__device__ __forceinline__ uint32_t cell_of(uint32_t r, const uint32_t *__restrict__ pack, uint32_t uni_m) {
-    if (uni_m) {                        // uniform bounds: IntToComp[r] = r / m
-        uint32_t c = r / uni_m;
-        return (c << 8) | (r - c * uni_m);
-    }
-    return __ldg(pack + r);
-}
-
-__device__ __forceinline__ uint2 unpack_cell(uint32_t cell) { return make_uint2(cell >> 8, cell & 0xFFu); }
-
-// table[j * T0 + t] = (c, r_t - CompToM[c]) of draw r_t of hash j, t < T0.
+// table[j * T0 + t] = (c * cmul, r_t - CompToM[c]) of draw r_t of hash j, t < T0
+// (cmul = 1 for row-major tiles, the column stride for column-major ones).
 __global__ void draw_table_kernel(uint2 *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
-                                  const uint32_t *__restrict__ pack, uint32_t uni_m) {
+                                  const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t cmul) {
     const int64_t total = (int64_t)k * T0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
-        table[i] = unpack_cell(cell_of(draw_r(S, j, t, M), pack, uni_m));
+        const uint2 d = unpack_cell(cell_of(draw_r(S, j, t, M), pack, uni_m));
+        table[i] = make_uint2(d.x * cmul, d.y);
     }
+}
+
+wmh_status launch_draw_table(uint2 *table, uint32_t k, uint64_t S, uint32_t M, const uint32_t *pack, uint32_t uni_m,
+                             uint32_t cmul, cudaStream_t s) {
+    const int64_t total = (int64_t)k * T0;
+    const int blocks = (int)min((int64_t)num_sms() * 8, (total + 255) / 256);
+    draw_table_kernel<<<blocks, 256, 0, s>>>(table, k, S, M, pack, uni_m, cmul);
+    WMH_LAUNCH_CHECK("draw table launch");
+    return WMH_OK;
 }
 
 struct TiledParams {
@@ -382,6 +381,13 @@ static wmh_status launch_tiled(const TiledParams &p, size_t smem, int grid, cuda
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     *handled = false;
     if (a.rows.kind != WMH_DENSE) return launch_hash_tiled_csr(a, handled);
+    // column-major tile with the SIMD first round (hash_tiled_cm.cu) unless
+    // WMH_TILED_RM=1 selects this row-major kernel
+    static const bool force_rm = getenv("WMH_TILED_RM") != nullptr;
+    if (!force_rm) {
+        const wmh_status cst = launch_hash_tiled_cm(a, handled);
+        if (cst != WMH_OK || *handled) return cst;
+    }
     const int D = (int)a.rows.dim;
     const int SW = (((D + 3) >> 2) | 1);                  // odd word stride: conflict-free lane=row tests
     int dev = 0;
@@ -425,10 +431,8 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
     const uint32_t M = (uint32_t)a.L->M;
     {
-        const int64_t total = (int64_t)a.k * T0;
-        const int blocks = (int)min((int64_t)sms * 8, (total + 255) / 256);
-        draw_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, M, a.L->cell_pack, uni_m);
-        WMH_LAUNCH_CHECK("draw table launch");
+        const wmh_status tst = launch_draw_table(table, a.k, a.S, M, a.L->cell_pack, uni_m, 1u, a.stream);
+        if (tst != WMH_OK) { cudaFreeAsync(scratch, a.stream); return tst; }
     }
     TiledParams p;
     p.x = a.rows.dense;

@@ -1,0 +1,445 @@
+// hash_tiled_cm.cu -- WMH_ALGO_TILED for dense rows, column-major tile (default).
+//
+// Same algorithm as hash_tiled.cu (each draw r_t of hash j is shared by the
+// tile's rows, because the draw stream does not depend on x), but
+// the tile is stored column-major -- x[row][c] at byte c * Rp + row -- so
+// one 32-bit shared load returns column c of FOUR rows.  That makes the first
+// round of every hash (draws t = 0..31, which every row must see and which
+// resolve ~80% of the rows at s ~ 0.05) a SIMD-within-a-register test:
+//
+//   green(x, off)  <=>  x > off  <=>  x + (255 - off) >= 256
+//
+// computed for 4 bytes at once as the carry out of bit 7:
+//   s = (a & 0x7F7F7F7F) + K,  K = ((255 - off) & 0x7F) * 0x01010101
+//   g = MAJ(a, B, s)           B = (255 - off) * 0x01010101    (one LOP3)
+//   m = PRMT(g, msb-replicate)  -> 0xFF in every green byte
+//   h = (h & ~m) | (i * 0x01010101 & m)   (draws visited in descending i)
+// i.e. 7 instructions and one LDS per draw for 4 rows, against 4 and one per
+// draw per row for the row-major kernel.  Rows still without a green after
+// round 0 continue on the warp's pending list exactly as in hash_tiled.cu
+// (lane = row, C draws per re-queue, then draw-parallel stragglers), with
+// addresses c * Rp + row.  First green t gives h = t + 1 (Alg. 3 / Def.,
+// P:166-188); rows still pending at the cap get h = cap (reading R9).
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+
+namespace wmh {
+
+constexpr int CM_NT = 512;
+constexpr int CM_NW = CM_NT / 32;
+constexpr int CM_STRAG = 4;
+
+struct CmParams {
+    const uint8_t *x;
+    int64_t n_rows;
+    int D, R, Rp;                // dim, rows per tile, column stride (bytes, Rp % 4 == 0, Rp/4 odd)
+    int n_hchunks, hchunk;
+    int64_t n_items;
+    uint32_t k, cap, M, uni_m;
+    uint64_t S;
+    int chunk;                   // 0 = auto (from the tile's effective sparsity)
+    const uint2 *table;          // [k][T0] (c * Rp, off)
+    const uint32_t *pack;
+    void *sig;
+    unsigned long long *n_sat;
+    unsigned long long *item_ctr;
+};
+
+template <int SIGB>
+__device__ __forceinline__ void cm_store(void *sig, int64_t idx, uint32_t h) {
+    if (SIGB == 1) reinterpret_cast<uint8_t *>(sig)[idx] = (uint8_t)h;
+    else reinterpret_cast<uint16_t *>(sig)[idx] = (uint16_t)h;
+}
+
+__device__ __forceinline__ uint2 cm_late(const CmParams &p, uint64_t keyj, uint32_t t) {
+    const uint2 d = unpack_cell(cell_of(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m));
+    return make_uint2(d.x * (uint32_t)p.Rp, d.y);
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+// Rounds 1.. over the pending list: lane = row, C draws per re-queue.
+template <int SIGB, int C>
+__device__ __forceinline__ int cm_rounds(const CmParams &p, const uint2 *buf, uint2 *win, const uint8_t *xs,
+                                         uint32_t j, uint64_t keyj, int64_t row0, const uint16_t *&cur,
+                                         uint16_t *own0, uint16_t *own1, int npend, uint32_t *q_io) {
+    const int lane = threadIdx.x & 31;
+    uint32_t q = *q_io;
+    int flip = 0;
+    while (npend > CM_STRAG && q * 32 < p.cap) {
+        const uint2 *src;
+        if (q * 32 < (uint32_t)T0) {
+            src = buf + q * 32;
+        } else {
+            const uint2 d = cm_late(p, keyj, q * 32 + lane);
+            __syncwarp();
+            win[lane] = d;
+            __syncwarp();
+            src = win;
+        }
+        const bool cap_round = q * 32 + 32 > p.cap;
+#pragma unroll
+        for (int sub = 0; sub < 32 / C; sub++) {
+            if (npend == 0) break;
+            uint32_t dc[C], doff[C];
+#pragma unroll
+            for (int i = 0; i < C / 2; i++) {
+                const uint4 v = reinterpret_cast<const uint4 *>(src + sub * C)[i];
+                dc[2 * i] = v.x; doff[2 * i] = v.y; dc[2 * i + 1] = v.z; doff[2 * i + 1] = v.w;
+            }
+            if (cap_round) {
+#pragma unroll
+                for (int tt = 0; tt < C; tt++)
+                    if (q * 32 + sub * C + tt >= p.cap) doff[tt] = 0xFFFFFFFFu;
+            }
+            uint16_t *nxt = flip ? own1 : own0;
+            flip ^= 1;
+            int nn = 0;
+            for (int base = 0; base < npend; base += 32) {
+                const int i = base + lane;
+                const bool active = i < npend;
+                const int r = active ? cur[i] : 0;
+                uint32_t h = C;
+                if (active) {
+                    constexpr int NCH = C >= 16 ? 4 : 2;
+                    uint32_t hc[NCH];
+#pragma unroll
+                    for (int c = 0; c < NCH; c++) hc[c] = C;
+#pragma unroll
+                    for (int tt = C - 1; tt >= 0; tt--) {
+                        const uint32_t v = xs[dc[tt] + r];
+                        hc[tt % NCH] = (v > doff[tt]) ? (uint32_t)tt : hc[tt % NCH];
+                    }
+                    h = hc[0];
+#pragma unroll
+                    for (int c = 1; c < NCH; c++) h = min(h, hc[c]);
+                }
+                const bool still = active && h == C;
+                if (active && !still) cm_store<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + j, q * 32 + sub * C + h + 1);
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, still);
+                if (still) nxt[nn + __popc(m & ((1u << lane) - 1))] = (uint16_t)r;
+                nn += __popc(m);
+            }
+            __syncwarp();
+            cur = nxt;
+            npend = nn;
+        }
+        q++;
+    }
+    *q_io = q;
+    return npend;
+}
+
+template <int SIGB>
+__global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams p) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int R = p.R, Rp = p.Rp;
+    uint8_t *xs = reinterpret_cast<uint8_t *>(smem);                               // [D][Rp]
+    const size_t xs_bytes = ((size_t)p.D * Rp + 15) & ~(size_t)15;
+    uint2 *sbuf_all = reinterpret_cast<uint2 *>(xs + xs_bytes);                     // [NW][T0]
+    uint2 *swin_all = sbuf_all + CM_NW * T0;                                        // [NW][32]
+    uint4 *sr0_all = reinterpret_cast<uint4 *>(swin_all + CM_NW * 32);              // [NW][32] round-0 consts
+    uint32_t *sres_all = reinterpret_cast<uint32_t *>(sr0_all + CM_NW * 32);        // [NW][2][R/4]
+    uint16_t *spend_all = reinterpret_cast<uint16_t *>(sres_all + CM_NW * 2 * (R / 4));   // [NW][2][R]
+    uint8_t *sflag = reinterpret_cast<uint8_t *>(spend_all + CM_NW * 2 * R);        // [R]
+    __shared__ long long s_item, s_next;
+    __shared__ int s_hash, s_nalive;
+    __shared__ unsigned long long s_xsum;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint2 *sbuf = sbuf_all + warp * T0;
+    uint2 *swin = swin_all + warp * 32;
+    uint4 *sr0 = sr0_all + warp * 32;
+    uint32_t *sres = sres_all + warp * 2 * (R / 4);
+    uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
+    unsigned long long sat = 0;
+    const int words = p.D >> 2;                        // D % 4 == 0 (launcher)
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(p.item_ctr, 1ull);
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_item = s_next;
+            s_next = (long long)atomicAdd(p.item_ctr, 1ull);
+            s_hash = 0;
+            s_xsum = 0;
+            s_nalive = 0;
+        }
+        __syncthreads();
+        const long long item = s_item;
+        if (item >= p.n_items) break;
+        if (s_next < p.n_items) {                      // warm L2 with the next item's rows
+            const int64_t nrow0 = (s_next / p.n_hchunks) * R;
+            const int64_t nbytes = min((int64_t)R, p.n_rows - nrow0) * (int64_t)p.D;
+            const char *base = reinterpret_cast<const char *>(p.x + nrow0 * (int64_t)p.D);
+            for (int64_t off = (int64_t)threadIdx.x * 128; off < nbytes; off += (int64_t)CM_NT * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        }
+        const int64_t tile = item / p.n_hchunks;
+        const int hc = (int)(item % p.n_hchunks);
+        const int64_t row0 = tile * R;
+        const int nr = (int)min((int64_t)R, p.n_rows - row0);
+        const uint32_t j0 = (uint32_t)hc * p.hchunk, j1 = min(p.k, j0 + (uint32_t)p.hchunk);
+        const int nw = (nr + 3) >> 2;                  // 4-row words
+
+        // ---- a5: stage transposed: 4 rows x 4 columns per lane, 8 PRMTs --------
+        for (int g = warp; g < nw; g += CM_NW) {
+            const uint32_t *rp[4];
+            bool ok[4];
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                ok[b] = 4 * g + b < nr;
+                rp[b] = reinterpret_cast<const uint32_t *>(p.x + (row0 + 4 * g + (ok[b] ? b : 0)) * (int64_t)p.D);
+            }
+            uint32_t acc[4] = {0, 0, 0, 0};
+            for (int cg = lane; cg < words; cg += 32) {
+                uint32_t v[4];
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    v[b] = ok[b] ? __ldg(rp[b] + cg) : 0u;
+                    acc[b] = __dp4a(v[b], 0x01010101u, acc[b]);
+                }
+                const uint32_t t0 = prmt(v[0], v[1], 0x5140), t1 = prmt(v[0], v[1], 0x7362);
+                const uint32_t t2 = prmt(v[2], v[3], 0x5140), t3 = prmt(v[2], v[3], 0x7362);
+                uint32_t *col = reinterpret_cast<uint32_t *>(xs + (size_t)(4 * cg) * Rp) + g;
+                const int st = Rp >> 2;                // words per column
+                col[0] = prmt(t0, t2, 0x5410);
+                col[st] = prmt(t0, t2, 0x7632);
+                col[2 * st] = prmt(t1, t3, 0x5410);
+                col[3 * st] = prmt(t1, t3, 0x7632);
+            }
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                uint32_t a = acc[b];
+                for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+                if (lane == 0 && ok[b]) {
+                    sflag[4 * g + b] = a != 0;
+                    if (a) { atomicAdd(&s_xsum, (unsigned long long)a); atomicAdd(&s_nalive, 1); }
+                }
+            }
+        }
+        __syncthreads();
+        const int nalive = s_nalive;
+        int C = p.chunk;
+        if (C == 0) {
+            const double s = nalive ? (double)s_xsum / ((double)nalive * (double)p.M) : 1.0;
+            C = s > 0.2 ? 8 : s > 0.1 ? 16 : 32;
+        }
+
+        // ---- hashes: one warp per hash, next hash's draws prefetched --------------
+        auto grab = [&]() {
+            int jj = 0;
+            if (lane == 0) jj = atomicAdd(&s_hash, 1);
+            return j0 + (uint32_t)__shfl_sync(0xFFFFFFFFu, jj, 0);
+        };
+        uint32_t j = grab();
+        uint4 pre[4];
+        if (j < j1) {
+            const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0);
+#pragma unroll
+            for (int i = 0; i < 4; i++) pre[i] = __ldg(t4 + 32 * i + lane);
+        }
+        while (j < j1) {
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
+            __syncwarp();
+            const uint32_t jn = grab();
+            if (jn < j1) {
+                const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0);
+#pragma unroll
+                for (int i = 0; i < 4; i++) pre[i] = __ldg(t4 + 32 * i + lane);
+            }
+            const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
+
+            // ---- round 0 (draws 0..31) for all rows, 4 rows per 32-bit word ----
+            {
+                const uint2 d = sbuf[lane];
+                const uint32_t nb = (uint32_t)lane < p.cap ? 255u - d.y : 0u;   // t >= cap: never green
+                sr0[lane] = make_uint4(d.x, (nb & 0x7Fu) * 0x01010101u, nb * 0x01010101u, 0u);
+            }
+            __syncwarp();
+            for (int u = lane; u < 2 * nw; u += 32) {
+                const int half = u >= nw, w = u - half * nw;
+                const uint4 *e = sr0 + 16 * half;
+                const uint8_t *xw = xs + 4 * w;                // this lane's 4-row word of every column
+                uint32_t h4 = 0xFFFFFFFFu;
+#pragma unroll
+                for (int i = 15; i >= 0; i--) {
+                    const uint4 ei = e[i];
+                    const uint32_t a = *reinterpret_cast<const uint32_t *>(xw + ei.x);
+                    const uint32_t s = (a & 0x7F7F7F7Fu) + ei.y;
+                    const uint32_t g = (a & ei.z) | (a & s) | (ei.z & s);       // carry out of bit 7 (MAJ)
+                    const uint32_t m = prmt(g, 0u, 0xBA98);                    // msb -> whole byte
+                    h4 = (h4 & ~m) | ((uint32_t)i * 0x01010101u & m);
+                }
+                sres[half * nw + w] = h4;
+            }
+            __syncwarp();
+            int npend = 0;
+            for (int wb = 0; wb < nw; wb += 32) {
+                const int w = wb + lane;
+                const uint32_t r0w = w < nw ? sres[w] : 0xFFFFFFFFu, r1w = w < nw ? sres[nw + w] : 0xFFFFFFFFu;
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int row = 4 * w + b;
+                    const bool live = w < nw && row < nr && sflag[row];
+                    const uint32_t v0 = (r0w >> (8 * b)) & 0xFFu, v1 = (r1w >> (8 * b)) & 0xFFu;
+                    const uint32_t h = v0 != 0xFFu ? v0 + 1 : (v1 != 0xFFu ? 17 + v1 : 0u);
+                    if (live && h) cm_store<SIGB>(p.sig, (row0 + row) * (int64_t)p.k + j, h);
+                    const bool pend = live && !h;
+                    const unsigned pm = __ballot_sync(0xFFFFFFFFu, pend);
+                    if (pend) own1[npend + __popc(pm & ((1u << lane) - 1))] = (uint16_t)row;
+                    npend += __popc(pm);
+                }
+            }
+            __syncwarp();
+            const uint16_t *cur = own1;
+            uint32_t q = 1;
+            // rounds 1.. (own0/own1 alternate; round 0's list is in own1)
+            switch (C) {
+                case 8: npend = cm_rounds<SIGB, 8>(p, sbuf, swin, xs, j, keyj, row0, cur, own0, own1, npend, &q); break;
+                case 16: npend = cm_rounds<SIGB, 16>(p, sbuf, swin, xs, j, keyj, row0, cur, own0, own1, npend, &q); break;
+                default: npend = cm_rounds<SIGB, 32>(p, sbuf, swin, xs, j, keyj, row0, cur, own0, own1, npend, &q); break;
+            }
+            if (npend > 0 && q * 32 >= p.cap) {        // a9: no green draw before the cap
+                for (int i = lane; i < npend; i += 32) {
+                    cm_store<SIGB>(p.sig, (row0 + cur[i]) * (int64_t)p.k + j, p.cap);
+                    sat++;
+                }
+                npend = 0;
+            }
+            if (npend > 0) {                           // draw-parallel stragglers (<= CM_STRAG)
+                int rr[CM_STRAG];
+                unsigned live = 0;
+#pragma unroll
+                for (int i = 0; i < CM_STRAG; i++) {
+                    rr[i] = i < npend ? (int)cur[i] : 0;
+                    if (i < npend) live |= 1u << i;
+                }
+                for (; live && q * 32 < p.cap; q++) {
+                    const uint32_t t = q * 32 + lane;
+                    const uint2 d = t < (uint32_t)T0 ? sbuf[t] : cm_late(p, keyj, t);
+                    const uint32_t off = t < p.cap ? d.y : 0xFFFFFFFFu;
+#pragma unroll
+                    for (int i = 0; i < CM_STRAG; i++) {
+                        if (live & (1u << i)) {
+                            const uint32_t v = xs[d.x + rr[i]];
+                            const unsigned gm = __ballot_sync(0xFFFFFFFFu, v > off);
+                            if (gm) {
+                                if (lane == 0) cm_store<SIGB>(p.sig, (row0 + rr[i]) * (int64_t)p.k + j, q * 32 + __ffs(gm));
+                                live &= ~(1u << i);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < CM_STRAG; i++)
+                    if ((live & (1u << i)) && lane == 0) {
+                        cm_store<SIGB>(p.sig, (row0 + rr[i]) * (int64_t)p.k + j, p.cap);
+                        sat++;
+                    }
+            }
+            j = jn;
+        }
+        if (nalive < nr) {                             // all-zero rows: h = cap for every hash (R12)
+            __syncthreads();
+            for (int r = warp; r < nr; r += CM_NW) {
+                if (sflag[r]) continue;
+                for (uint32_t jj = j0 + lane; jj < j1; jj += 32) {
+                    cm_store<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + jj, p.cap);
+                    sat++;
+                }
+            }
+        }
+    }
+    if (p.n_sat) {
+        for (int o = 16; o; o >>= 1) sat += __shfl_xor_sync(0xFFFFFFFFu, sat, o);
+        if (lane == 0 && sat) atomicAdd(p.n_sat, sat);
+    }
+}
+
+static size_t cm_smem(int D, int R, int Rp) {
+    return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 8 + (size_t)CM_NW * 32 * 16 +
+           (size_t)CM_NW * 2 * (R / 4) * 4 + (size_t)CM_NW * 2 * R * 2 + R + 16;
+}
+
+wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
+    *handled = false;
+    const int D = (int)a.rows.dim;
+    if (a.rows.kind != WMH_DENSE || (D & 3) || ((uintptr_t)a.rows.dense & 3)) return WMH_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // rows per tile: multiple of 16, column stride Rp = R + 4 (Rp/4 odd: draw-
+    // parallel accesses to random columns spread over the banks)
+    int R = 256, Rp = 0;
+    for (; R >= 32; R -= 16) {
+        Rp = R + 4;
+        if (cm_smem(D, R, Rp) <= (size_t)smem_optin) break;
+    }
+    if (R < 32) return WMH_OK;
+    const size_t smem = cm_smem(D, R, Rp);
+    *handled = true;
+
+    const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
+    const int sms = num_sms();
+    int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 8, ((int64_t)sms * 8 + n_tiles - 1) / n_tiles));
+    const int hchunk = (int)((a.k + n_hchunks - 1) / n_hchunks);
+    n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
+
+    uint8_t *scratch = nullptr;
+    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint2);
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "tiled scratch alloc");
+    uint2 *table = reinterpret_cast<uint2 *>(scratch);
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
+    WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "tiled counter memset");
+    const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
+    const uint32_t M = (uint32_t)a.L->M;
+    wmh_status st = launch_draw_table(table, a.k, a.S, M, a.L->cell_pack, uni_m, (uint32_t)Rp, a.stream);
+    if (st != WMH_OK) { cudaFreeAsync(scratch, a.stream); return st; }
+
+    CmParams p;
+    p.x = a.rows.dense;
+    p.n_rows = a.rows.n_rows;
+    p.D = D;
+    p.R = R;
+    p.Rp = Rp;
+    p.n_hchunks = n_hchunks;
+    p.hchunk = hchunk;
+    p.n_items = n_tiles * n_hchunks;
+    p.k = a.k;
+    p.cap = a.cap;
+    p.M = M;
+    p.uni_m = uni_m;
+    p.S = a.S;
+    p.chunk = a.chunk == 4 ? 8 : a.chunk;
+    p.table = table;
+    p.pack = a.L->cell_pack;
+    p.sig = a.sig;
+    p.n_sat = a.n_sat;
+    p.item_ctr = ctr;
+    const int grid = (int)min((int64_t)sms, p.n_items);
+    if (a.sig_bytes == 1) {
+        cudaFuncSetAttribute(hash_tiled_cm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        hash_tiled_cm_kernel<1><<<grid, CM_NT, smem, a.stream>>>(p);
+    } else {
+        cudaFuncSetAttribute(hash_tiled_cm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        hash_tiled_cm_kernel<2><<<grid, CM_NT, smem, a.stream>>>(p);
+    }
+    WMH_LAUNCH_CHECK("hash_tiled_cm launch");
+    if (getenv("WMH_TILED_STATS"))
+        fprintf(stderr, "[wmh tiled cm] R=%d Rp=%d grid=%d items=%lld hchunk=%d smem=%zu\n", R, Rp, grid,
+                (long long)p.n_items, hchunk, smem);
+    cudaFreeAsync(scratch, a.stream);
+    return WMH_OK;
+}
+
+}  // namespace wmh
