@@ -14,12 +14,14 @@
 //   g = MAJ(a, B, s)           B = (255 - off) * 0x01010101    (one LOP3)
 //   m = PRMT(g, msb-replicate)  -> 0xFF in every green byte
 //   h = (h & ~m) | (i * 0x01010101 & m)   (draws visited in descending i)
-// i.e. 7 instructions and one LDS per draw for 4 rows, against 4 and one per
-// draw per row for the row-major kernel.  Rows still without a green after
-// round 0 continue on the warp's pending list exactly as in hash_tiled.cu
-// (lane = row, C draws per re-queue, then draw-parallel stragglers), with
-// addresses c * Rp + row.  First green t gives h = t + 1 (Alg. 3 / Def.,
-// P:166-188); rows still pending at the cap get h = cap (reading R9).
+// -- one LDS and ~8 instructions per draw for 4 rows.  The tile holds
+// R = 32 * 4 / P rows (P = 1, 2, 4) so that round 0 is exactly one (4-row word,
+// 32/P-draw part) unit per lane.  Rows still without a green continue on the
+// warp's pending list (lane = row, C draws per re-queue, then draw-parallel
+// stragglers) with addresses c * Rp + row.  Results go to a per-warp shared
+// row h[R] and are flushed to the signatures once per hash.  First green t
+// gives h = t + 1 (Alg. 3 / Def.); no green before the cap gives
+// h = cap (reading R9); all-zero rows get cap (R12).
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -30,11 +32,12 @@ namespace wmh {
 constexpr int CM_NT = 512;
 constexpr int CM_NW = CM_NT / 32;
 constexpr int CM_STRAG = 4;
+constexpr int CM_RMAX = 128;
 
 struct CmParams {
     const uint8_t *x;
     int64_t n_rows;
-    int D, R, Rp;                // dim, rows per tile, column stride (bytes, Rp % 4 == 0, Rp/4 odd)
+    int D, R, Rp;                // dim, rows per tile (128/64/32), column stride (bytes, Rp/4 odd)
     int n_hchunks, hchunk;
     int64_t n_items;
     uint32_t k, cap, M, uni_m;
@@ -47,12 +50,6 @@ struct CmParams {
     unsigned long long *item_ctr;
 };
 
-template <int SIGB>
-__device__ __forceinline__ void cm_store(void *sig, int64_t idx, uint32_t h) {
-    if (SIGB == 1) reinterpret_cast<uint8_t *>(sig)[idx] = (uint8_t)h;
-    else reinterpret_cast<uint16_t *>(sig)[idx] = (uint16_t)h;
-}
-
 __device__ __forceinline__ uint2 cm_late(const CmParams &p, uint64_t keyj, uint32_t t) {
     const uint2 d = unpack_cell(cell_of(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m));
     return make_uint2(d.x * (uint32_t)p.Rp, d.y);
@@ -64,11 +61,12 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return d;
 }
 
-// Rounds 1.. over the pending list: lane = row, C draws per re-queue.
-template <int SIGB, int C>
+// Rounds 1.. over the pending list: lane = row, C draws per re-queue;
+// results to the warp's shared row hres[].
+template <int C>
 __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint2 *buf, uint2 *win, const uint8_t *xs,
-                                         uint32_t j, uint64_t keyj, int64_t row0, const uint16_t *&cur,
-                                         uint16_t *own0, uint16_t *own1, int npend, uint32_t *q_io) {
+                                         uint64_t keyj, uint16_t *hres, const uint16_t *&cur, uint16_t *own0,
+                                         uint16_t *own1, int npend, uint32_t *q_io) {
     const int lane = threadIdx.x & 31;
     uint32_t q = *q_io;
     int flip = 0;
@@ -121,7 +119,7 @@ __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint2 *buf, ui
                     for (int c = 1; c < NCH; c++) h = min(h, hc[c]);
                 }
                 const bool still = active && h == C;
-                if (active && !still) cm_store<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + j, q * 32 + sub * C + h + 1);
+                if (active && !still) hres[r] = (uint16_t)(q * 32 + sub * C + h + 1);
                 const unsigned m = __ballot_sync(0xFFFFFFFFu, still);
                 if (still) nxt[nn + __popc(m & ((1u << lane) - 1))] = (uint16_t)r;
                 nn += __popc(m);
@@ -136,18 +134,20 @@ __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint2 *buf, ui
     return npend;
 }
 
-template <int SIGB>
+template <int SIGB, int P>
 __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams p) {
+    constexpr int R = 128 / P, NWD = R / 4, PD = 32 / P;   // rows, 4-row words (NWD * P == 32), draws per part
     extern __shared__ __align__(16) uint32_t smem[];
-    const int R = p.R, Rp = p.Rp;
+    const int Rp = p.Rp;
     uint8_t *xs = reinterpret_cast<uint8_t *>(smem);                               // [D][Rp]
     const size_t xs_bytes = ((size_t)p.D * Rp + 15) & ~(size_t)15;
     uint2 *sbuf_all = reinterpret_cast<uint2 *>(xs + xs_bytes);                     // [NW][T0]
     uint2 *swin_all = sbuf_all + CM_NW * T0;                                        // [NW][32]
     uint4 *sr0_all = reinterpret_cast<uint4 *>(swin_all + CM_NW * 32);              // [NW][32] round-0 consts
-    uint32_t *sres_all = reinterpret_cast<uint32_t *>(sr0_all + CM_NW * 32);        // [NW][2][R/4]
-    uint16_t *spend_all = reinterpret_cast<uint16_t *>(sres_all + CM_NW * 2 * (R / 4));   // [NW][2][R]
-    uint8_t *sflag = reinterpret_cast<uint8_t *>(spend_all + CM_NW * 2 * R);        // [R]
+    uint32_t *spart_all = reinterpret_cast<uint32_t *>(sr0_all + CM_NW * 32);       // [NW][32] partial h4
+    uint16_t *hres_all = reinterpret_cast<uint16_t *>(spart_all + CM_NW * 32);      // [NW][R] results
+    uint16_t *spend_all = hres_all + CM_NW * R;                                     // [NW][2][R]
+    uint8_t *sflag4 = reinterpret_cast<uint8_t *>(spend_all + CM_NW * 2 * R);       // [NWD] live-row nibbles
     __shared__ long long s_item, s_next;
     __shared__ int s_hash, s_nalive;
     __shared__ unsigned long long s_xsum;
@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     uint2 *sbuf = sbuf_all + warp * T0;
     uint2 *swin = swin_all + warp * 32;
     uint4 *sr0 = sr0_all + warp * 32;
-    uint32_t *sres = sres_all + warp * 2 * (R / 4);
+    uint32_t *spart = spart_all + warp * 32;
+    uint16_t *hres = hres_all + warp * R;
     uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
     unsigned long long sat = 0;
     const int words = p.D >> 2;                        // D % 4 == 0 (launcher)
@@ -186,18 +187,19 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
         const int64_t row0 = tile * R;
         const int nr = (int)min((int64_t)R, p.n_rows - row0);
         const uint32_t j0 = (uint32_t)hc * p.hchunk, j1 = min(p.k, j0 + (uint32_t)p.hchunk);
-        const int nw = (nr + 3) >> 2;                  // 4-row words
 
         // ---- a5: stage transposed: 4 rows x 4 columns per lane, 8 PRMTs --------
-        for (int g = warp; g < nw; g += CM_NW) {
+        for (int g = warp; g < NWD; g += CM_NW) {
             const uint32_t *rp[4];
             bool ok[4];
 #pragma unroll
             for (int b = 0; b < 4; b++) {
                 ok[b] = 4 * g + b < nr;
-                rp[b] = reinterpret_cast<const uint32_t *>(p.x + (row0 + 4 * g + (ok[b] ? b : 0)) * (int64_t)p.D);
+                rp[b] = reinterpret_cast<const uint32_t *>(p.x + (row0 + (ok[b] ? 4 * g + b : 0)) * (int64_t)p.D);
             }
             uint32_t acc[4] = {0, 0, 0, 0};
+            const int st = Rp >> 2;                    // words per column
+#pragma unroll 2
             for (int cg = lane; cg < words; cg += 32) {
                 uint32_t v[4];
 #pragma unroll
@@ -208,21 +210,20 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
                 const uint32_t t0 = prmt(v[0], v[1], 0x5140), t1 = prmt(v[0], v[1], 0x7362);
                 const uint32_t t2 = prmt(v[2], v[3], 0x5140), t3 = prmt(v[2], v[3], 0x7362);
                 uint32_t *col = reinterpret_cast<uint32_t *>(xs + (size_t)(4 * cg) * Rp) + g;
-                const int st = Rp >> 2;                // words per column
                 col[0] = prmt(t0, t2, 0x5410);
                 col[st] = prmt(t0, t2, 0x7632);
                 col[2 * st] = prmt(t1, t3, 0x5410);
                 col[3 * st] = prmt(t1, t3, 0x7632);
             }
+            uint32_t live4 = 0;
 #pragma unroll
             for (int b = 0; b < 4; b++) {
                 uint32_t a = acc[b];
                 for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
-                if (lane == 0 && ok[b]) {
-                    sflag[4 * g + b] = a != 0;
-                    if (a) { atomicAdd(&s_xsum, (unsigned long long)a); atomicAdd(&s_nalive, 1); }
-                }
+                if (a) live4 |= 1u << b;
+                if (lane == 0 && a) { atomicAdd(&s_xsum, (unsigned long long)a); atomicAdd(&s_nalive, 1); }
             }
+            if (lane == 0) sflag4[g] = (uint8_t)live4;
         }
         __syncthreads();
         const int nalive = s_nalive;
@@ -258,42 +259,66 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             }
             const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
 
-            // ---- round 0 (draws 0..31) for all rows, 4 rows per 32-bit word ----
+            // ---- round 0 (draws 0..31): lane = (4-row word, 32/P-draw part) ---------
             {
                 const uint2 d = sbuf[lane];
                 const uint32_t nb = (uint32_t)lane < p.cap ? 255u - d.y : 0u;   // t >= cap: never green
                 sr0[lane] = make_uint4(d.x, (nb & 0x7Fu) * 0x01010101u, nb * 0x01010101u, 0u);
             }
             __syncwarp();
-            for (int u = lane; u < 2 * nw; u += 32) {
-                const int half = u >= nw, w = u - half * nw;
-                const uint4 *e = sr0 + 16 * half;
-                const uint8_t *xw = xs + 4 * w;                // this lane's 4-row word of every column
-                uint32_t h4 = 0xFFFFFFFFu;
+            const int w = lane % NWD, part = lane / NWD;
+            uint32_t h4 = 0xFFFFFFFFu;                 // per byte: first green draw within the part
+            {
+                const uint4 *e = sr0 + part * PD;
+                const uint8_t *xw = xs + 4 * w;
 #pragma unroll
-                for (int i = 15; i >= 0; i--) {
+                for (int i = PD - 1; i >= 0; i--) {
                     const uint4 ei = e[i];
                     const uint32_t a = *reinterpret_cast<const uint32_t *>(xw + ei.x);
                     const uint32_t s = (a & 0x7F7F7F7Fu) + ei.y;
                     const uint32_t g = (a & ei.z) | (a & s) | (ei.z & s);       // carry out of bit 7 (MAJ)
                     const uint32_t m = prmt(g, 0u, 0xBA98);                    // msb -> whole byte
-                    h4 = (h4 & ~m) | ((uint32_t)i * 0x01010101u & m);
+                    h4 = (h4 & ~m) | ((uint32_t)(part * PD + i) * 0x01010101u & m);
                 }
-                sres[half * nw + w] = h4;
             }
-            __syncwarp();
+            if (P > 1) {                                // first part with a green wins, per byte
+                spart[lane] = h4;
+                __syncwarp();
+                if (lane < NWD) {
+                    uint32_t hw = 0xFFFFFFFFu;
+#pragma unroll
+                    for (int q2 = P - 1; q2 >= 0; q2--) {
+                        const uint32_t o = spart[q2 * NWD + lane];
+                        const uint32_t m = prmt(~o, 0u, 0xBA98);            // bytes of o that are green (< 0x80)
+                        hw = (hw & ~m) | (o & m);
+                    }
+                    h4 = hw;
+                }
+                __syncwarp();
+            }
+            // ---- round-0 results -> hres, pending rows -> own1 --------------------
             int npend = 0;
-            for (int wb = 0; wb < nw; wb += 32) {
-                const int w = wb + lane;
-                const uint32_t r0w = w < nw ? sres[w] : 0xFFFFFFFFu, r1w = w < nw ? sres[nw + w] : 0xFFFFFFFFu;
+            {
+                const bool wl = lane < NWD;
+                const uint32_t live4 = wl ? (uint32_t)sflag4[w] : 0u;
+                // bytes: first green index (0..31) -> h = index + 1; 0xFF -> 0 (pending)
+                const uint32_t v = ((h4 & 0x7F7F7F7Fu) + 0x01010101u) & 0x7F7F7F7Fu;
+                if (wl) {
+                    const uint32_t lo = prmt(v, 0u, 0x4140), hi = prmt(v, 0u, 0x4342);
+                    // dead rows (all-zero) never turn green: h = cap
+                    uint32_t l2 = lo, h2 = hi;
+                    if (!(live4 & 1u)) l2 = (l2 & 0xFFFF0000u) | p.cap;
+                    if (!(live4 & 2u)) l2 = (l2 & 0x0000FFFFu) | (p.cap << 16);
+                    if (!(live4 & 4u)) h2 = (h2 & 0xFFFF0000u) | p.cap;
+                    if (!(live4 & 8u)) h2 = (h2 & 0x0000FFFFu) | (p.cap << 16);
+                    *reinterpret_cast<uint2 *>(hres + 4 * w) = make_uint2(l2, h2);
+                    const uint32_t valid4 = (4 * w + 4 <= nr) ? 0xFu : ((1u << max(0, nr - 4 * w)) - 1u);
+                    sat += __popc(valid4 & ~live4);
+                }
 #pragma unroll
                 for (int b = 0; b < 4; b++) {
                     const int row = 4 * w + b;
-                    const bool live = w < nw && row < nr && sflag[row];
-                    const uint32_t v0 = (r0w >> (8 * b)) & 0xFFu, v1 = (r1w >> (8 * b)) & 0xFFu;
-                    const uint32_t h = v0 != 0xFFu ? v0 + 1 : (v1 != 0xFFu ? 17 + v1 : 0u);
-                    if (live && h) cm_store<SIGB>(p.sig, (row0 + row) * (int64_t)p.k + j, h);
-                    const bool pend = live && !h;
+                    const bool pend = wl && row < nr && ((live4 >> b) & 1u) && ((v >> (8 * b)) & 0xFFu) == 0u;
                     const unsigned pm = __ballot_sync(0xFFFFFFFFu, pend);
                     if (pend) own1[npend + __popc(pm & ((1u << lane) - 1))] = (uint16_t)row;
                     npend += __popc(pm);
@@ -302,15 +327,14 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             __syncwarp();
             const uint16_t *cur = own1;
             uint32_t q = 1;
-            // rounds 1.. (own0/own1 alternate; round 0's list is in own1)
             switch (C) {
-                case 8: npend = cm_rounds<SIGB, 8>(p, sbuf, swin, xs, j, keyj, row0, cur, own0, own1, npend, &q); break;
-                case 16: npend = cm_rounds<SIGB, 16>(p, sbuf, swin, xs, j, keyj, row0, cur, own0, own1, npend, &q); break;
-                default: npend = cm_rounds<SIGB, 32>(p, sbuf, swin, xs, j, keyj, row0, cur, own0, own1, npend, &q); break;
+                case 8: npend = cm_rounds<8>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
+                case 16: npend = cm_rounds<16>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
+                default: npend = cm_rounds<32>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
             }
             if (npend > 0 && q * 32 >= p.cap) {        // a9: no green draw before the cap
                 for (int i = lane; i < npend; i += 32) {
-                    cm_store<SIGB>(p.sig, (row0 + cur[i]) * (int64_t)p.k + j, p.cap);
+                    hres[cur[i]] = (uint16_t)p.cap;
                     sat++;
                 }
                 npend = 0;
@@ -330,10 +354,10 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 #pragma unroll
                     for (int i = 0; i < CM_STRAG; i++) {
                         if (live & (1u << i)) {
-                            const uint32_t v = xs[d.x + rr[i]];
-                            const unsigned gm = __ballot_sync(0xFFFFFFFFu, v > off);
+                            const uint32_t xv = xs[d.x + rr[i]];
+                            const unsigned gm = __ballot_sync(0xFFFFFFFFu, xv > off);
                             if (gm) {
-                                if (lane == 0) cm_store<SIGB>(p.sig, (row0 + rr[i]) * (int64_t)p.k + j, q * 32 + __ffs(gm));
+                                if (lane == 0) hres[rr[i]] = (uint16_t)(q * 32 + __ffs(gm));
                                 live &= ~(1u << i);
                             }
                         }
@@ -342,21 +366,18 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 #pragma unroll
                 for (int i = 0; i < CM_STRAG; i++)
                     if ((live & (1u << i)) && lane == 0) {
-                        cm_store<SIGB>(p.sig, (row0 + rr[i]) * (int64_t)p.k + j, p.cap);
+                        hres[rr[i]] = (uint16_t)p.cap;
                         sat++;
                     }
             }
-            j = jn;
-        }
-        if (nalive < nr) {                             // all-zero rows: h = cap for every hash (R12)
-            __syncthreads();
-            for (int r = warp; r < nr; r += CM_NW) {
-                if (sflag[r]) continue;
-                for (uint32_t jj = j0 + lane; jj < j1; jj += 32) {
-                    cm_store<SIGB>(p.sig, (row0 + r) * (int64_t)p.k + jj, p.cap);
-                    sat++;
-                }
+            __syncwarp();
+            // ---- a9: flush this hash's column of signatures ----------------------
+            for (int r = lane; r < nr; r += 32) {
+                const int64_t idx = (row0 + r) * (int64_t)p.k + j;
+                if (SIGB == 1) reinterpret_cast<uint8_t *>(p.sig)[idx] = (uint8_t)hres[r];
+                else reinterpret_cast<uint16_t *>(p.sig)[idx] = hres[r];
             }
+            j = jn;
         }
     }
     if (p.n_sat) {
@@ -367,7 +388,13 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 
 static size_t cm_smem(int D, int R, int Rp) {
     return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 8 + (size_t)CM_NW * 32 * 16 +
-           (size_t)CM_NW * 2 * (R / 4) * 4 + (size_t)CM_NW * 2 * R * 2 + R + 16;
+           (size_t)CM_NW * 32 * 4 + (size_t)CM_NW * R * 2 + (size_t)CM_NW * 2 * R * 2 + (size_t)(R / 4) + 16;
+}
+
+template <int SIGB, int P>
+static void cm_launch(const CmParams &p, size_t smem, int grid, cudaStream_t s) {
+    cudaFuncSetAttribute(hash_tiled_cm_kernel<SIGB, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hash_tiled_cm_kernel<SIGB, P><<<grid, CM_NT, smem, s>>>(p);
 }
 
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
@@ -378,14 +405,15 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     cudaGetDevice(&dev);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    // rows per tile: multiple of 16, column stride Rp = R + 4 (Rp/4 odd: draw-
+    // rows per tile R = 128 / P; column stride Rp = R + 4 (Rp/4 odd: draw-
     // parallel accesses to random columns spread over the banks)
-    int R = 256, Rp = 0;
-    for (; R >= 32; R -= 16) {
+    int P = 1, R = 0, Rp = 0;
+    for (; P <= 4; P *= 2) {
+        R = 128 / P;
         Rp = R + 4;
         if (cm_smem(D, R, Rp) <= (size_t)smem_optin) break;
     }
-    if (R < 32) return WMH_OK;
+    if (P > 4) return WMH_OK;
     const size_t smem = cm_smem(D, R, Rp);
     *handled = true;
 
@@ -428,15 +456,17 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     p.item_ctr = ctr;
     const int grid = (int)min((int64_t)sms, p.n_items);
     if (a.sig_bytes == 1) {
-        cudaFuncSetAttribute(hash_tiled_cm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        hash_tiled_cm_kernel<1><<<grid, CM_NT, smem, a.stream>>>(p);
+        if (P == 1) cm_launch<1, 1>(p, smem, grid, a.stream);
+        else if (P == 2) cm_launch<1, 2>(p, smem, grid, a.stream);
+        else cm_launch<1, 4>(p, smem, grid, a.stream);
     } else {
-        cudaFuncSetAttribute(hash_tiled_cm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        hash_tiled_cm_kernel<2><<<grid, CM_NT, smem, a.stream>>>(p);
+        if (P == 1) cm_launch<2, 1>(p, smem, grid, a.stream);
+        else if (P == 2) cm_launch<2, 2>(p, smem, grid, a.stream);
+        else cm_launch<2, 4>(p, smem, grid, a.stream);
     }
     WMH_LAUNCH_CHECK("hash_tiled_cm launch");
     if (getenv("WMH_TILED_STATS"))
-        fprintf(stderr, "[wmh tiled cm] R=%d Rp=%d grid=%d items=%lld hchunk=%d smem=%zu\n", R, Rp, grid,
+        fprintf(stderr, "[wmh tiled cm] R=%d Rp=%d P=%d grid=%d items=%lld hchunk=%d smem=%zu\n", R, Rp, P, grid,
                 (long long)p.n_items, hchunk, smem);
     cudaFreeAsync(scratch, a.stream);
     return WMH_OK;
