@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    p.add_argument("--collide-pairs", type=int, default=0,
+                   help="also time wmh_collide (a10) on this many random pairs of the step's signatures")
     return p.parse_args()
 
 
@@ -321,6 +323,10 @@ def main():
     if not args.no_e2e:
         e2e = measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist)
 
+    coll = None
+    if args.collide_pairs > 0:
+        coll = measure_collide(wmh, sig, args.collide_pairs, cfg, dev, peaks)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r, cores, sample = oracle_rate(cfg, data, layout_bounds(cfg, data), args.cpu_seconds)
@@ -338,6 +344,7 @@ def main():
                              f"{sig.numel() * sig.element_size() / 2**20:.0f} MiB per step",
                        "expected_draws_per_step": draws * world},
             "roofline": roof,
+            "collide": coll,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
@@ -407,3 +414,29 @@ def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist):
 
 if __name__ == "__main__":
     sys.exit(main())
+
+
+def measure_collide(wmh, sig, n_pairs, cfg, dev, peaks):
+    """a10: wmh_collide on random row pairs of the step's signatures; HBM roofline
+    (2 * k * sig_bytes read per pair + 4 B match + 4 B J-hat written)."""
+    import datagen
+    import torch
+    pairs = torch.from_numpy(datagen.random_pairs(cfg.data_seed, sig.shape[0], n_pairs)).to(dev)
+    for _ in range(2):
+        wmh.collide(sig, pairs, check_pairs=False)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    a.record()
+    for _ in range(reps):
+        wmh.collide(sig, pairs, check_pairs=False)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    sig_bytes = sig.shape[1] * sig.element_size()
+    algo_bytes = n_pairs * (2 * sig_bytes + 8 + 16)
+    hbm = peaks.get("hbm_gbs", 6545.6)
+    gbs = algo_bytes / (ms / 1e3) / 1e9
+    return {"pairs": n_pairs, "ms": ms, "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+            "frac": gbs / hbm, "note": f"signatures {sig.numel() * sig.element_size() / 2**30:.2f} GiB "
+                                        f"({'fits' if sig.numel() * sig.element_size() < 100 * 2**20 else 'exceeds'} L2)"}

@@ -25,6 +25,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace wmh {
@@ -239,7 +241,10 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             if (lane == 0) jj = atomicAdd(&s_hash, 1);
             return j0 + (uint32_t)__shfl_sync(0xFFFFFFFFu, jj, 0);
         };
+        // hash indices are claimed two ahead so the shared atomic's latency is
+        // hidden behind a whole hash; the next hash's draws are prefetched
         uint32_t j = grab();
+        uint32_t jn = grab();
         uint4 pre[4];
         if (j < j1) {
             const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0);
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 #pragma unroll
             for (int i = 0; i < 4; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
             __syncwarp();
-            const uint32_t jn = grab();
+            const uint32_t jnn = jn < j1 ? grab() : j1;
             if (jn < j1) {
                 const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0);
 #pragma unroll
@@ -372,12 +377,14 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             }
             __syncwarp();
             // ---- a9: flush this hash's column of signatures ----------------------
-            for (int r = lane; r < nr; r += 32) {
-                const int64_t idx = (row0 + r) * (int64_t)p.k + j;
-                if (SIGB == 1) reinterpret_cast<uint8_t *>(p.sig)[idx] = (uint8_t)hres[r];
-                else reinterpret_cast<uint16_t *>(p.sig)[idx] = hres[r];
+            {
+                using sig_t = typename std::conditional<SIGB == 1, uint8_t, uint16_t>::type;
+                sig_t *ptr = reinterpret_cast<sig_t *>(p.sig) + (row0 + lane) * (int64_t)p.k + j;
+                const int64_t step = 32 * (int64_t)p.k;
+                for (int r = lane; r < nr; r += 32, ptr += step) *ptr = (sig_t)hres[r];
             }
             j = jn;
+            jn = jnn;
         }
     }
     if (p.n_sat) {
