@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    p.add_argument("--gpu-gen", action="store_true",
+                   help="c1/c5: generate the rows on the device (datagen/gen_kernels.cu) instead of the host")
     p.add_argument("--collide-pairs", type=int, default=0,
                    help="also time wmh_collide (a10) on this many random pairs of the step's signatures")
     return p.parse_args()
@@ -172,8 +174,8 @@ def oracle_rate(cfg, data, M_bounds, seconds: float):
     n = data.n_rows
 
     def run(rows):
-        if isinstance(data, datagen.Dense):
-            x = np.ascontiguousarray(data.x[rows])
+        if isinstance(data, (datagen.Dense, datagen.CounterRows)):
+            x = np.ascontiguousarray(data.rows(rows) if isinstance(data, datagen.CounterRows) else data.x[rows])
             t0 = time.perf_counter()
             L.hash_dense(x, cfg.seed, cfg.k, cfg.cap, threads=cores)
         else:
@@ -250,10 +252,24 @@ def main():
     build.build()
     import paper_1602_08393_b200 as wmh
 
-    cfg, n, data = workload(args.config, rank, args.rows)
-    # inputs resident in HBM before the timed region
     import datagen
-    if isinstance(data, datagen.Dense):
+    gpu_gen = args.gpu_gen and args.config in ("c1", "c5")
+    xd = None
+    if gpu_gen:       # counter-based configs generated on the device (bit-identical to the host recipe)
+        cfg = datagen.CONFIGS[args.config]
+        n = cfg.n_rows if args.rows is None else args.rows
+        xd = torch.empty((n, cfg.dim), dtype=torch.uint8, device=dev)
+        for a0 in range(0, n, 1 << 20):
+            b0 = min(n, a0 + (1 << 20))
+            xd[a0:b0] = datagen.gpu_counter_rows(args.config, cfg.data_seed, rank * n + a0, b0 - a0, cfg.dim, dev)
+        data = datagen.CounterRows(args.config, cfg.data_seed, rank * n, n, cfg.dim)
+    else:
+        cfg, n, data = workload(args.config, rank, args.rows)
+    # inputs resident in HBM before the timed region
+    if xd is not None:
+        rows = wmh.Rows.from_dense(xd)
+        in_bytes = xd.numel()
+    elif isinstance(data, datagen.Dense):
         rows = wmh.Rows.from_dense(torch.from_numpy(data.x).to(dev))
         in_bytes = data.x.nbytes
     else:
@@ -295,7 +311,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clocks.stop()
-    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_ms = sum(step_ms)
     t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -305,7 +322,7 @@ def main():
     ms_per_step = t_max_ms / args.steps
 
     # ---- roofline of the dominant (only) kernel of the step
-    x_sum = row_sums(data)
+    x_sum = xd.sum(1, dtype=torch.int64).cpu().numpy() if xd is not None else row_sums(data)
     draws = expected_draws(x_sum, M, cfg.k, cfg.cap)      # this rank's algorithmic draw-tests per launch
     kern_s = (t_ms / args.steps) / 1e3
     peaks = {}
@@ -321,7 +338,7 @@ def main():
     # ---- e2e: the public host-buffer API, H2D rows + hash + D2H signatures every step
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist)
+        e2e = measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd)
 
     coll = None
     if args.collide_pairs > 0:
@@ -329,7 +346,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r, cores, sample = oracle_rate(cfg, data, layout_bounds(cfg, data), args.cpu_seconds)
+        bnds = xd.amax(0).to(torch.int32).cpu().numpy().astype(np.uint32) if xd is not None \
+            else layout_bounds(cfg, data)
+        r, cores, sample = oracle_rate(cfg, data, bnds, args.cpu_seconds)
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
 
     if rank == 0:
@@ -342,7 +361,8 @@ def main():
                        "l2": "flushed between steps (256 MiB write outside the timed events); "
                              f"inputs {in_bytes / 2**20:.0f} MiB + signatures "
                              f"{sig.numel() * sig.element_size() / 2**20:.0f} MiB per step",
-                       "expected_draws_per_step": draws * world},
+                       "expected_draws_per_step": draws * world,
+                       "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)]},
             "roofline": roof,
             "collide": coll,
             "cpu_baseline": cpu,
@@ -378,10 +398,15 @@ def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
             "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3, "t_kernel_ms": kern_s * 1e3}
 
 
-def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist):
+def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd=None):
     import datagen
     import torch
-    if isinstance(data, datagen.Dense):
+    if xd is not None:                  # device-generated rows: e2e over the first <= 2^20 rows
+        n = min(n, 1 << 20)
+        hx = xd[:n].cpu().pin_memory()
+        hrows = wmh.Rows.from_dense(hx)
+        h2d = hx.numel()
+    elif isinstance(data, datagen.Dense):
         hx = torch.from_numpy(data.x).pin_memory()
         hrows = wmh.Rows.from_dense(hx)
         h2d = hx.numel()

@@ -201,6 +201,22 @@ class CSR:
 
 
 @dataclass
+class CounterRows:
+    """Lazy host view of a counter-based config's rows (c1 / c5): any row can be
+    regenerated alone, so full-size data need not live in host memory."""
+    name: str
+    data_seed: int
+    row0: int
+    n_rows: int
+    dim: int
+    kind = "dense"
+
+    def rows(self, idx) -> np.ndarray:
+        gen = {"c1": gen_counter_c1_rows, "c5": gen_counter_c5_rows}[self.name]
+        return gen(self.data_seed, self.row0 + np.asarray(idx, np.int64), self.dim)
+
+
+@dataclass
 class Config:
     name: str
     n_rows: int
