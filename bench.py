@@ -322,7 +322,10 @@ def main():
     ms_per_step = t_max_ms / args.steps
 
     # ---- roofline of the dominant (only) kernel of the step
-    x_sum = xd.sum(1, dtype=torch.int64).cpu().numpy() if xd is not None else row_sums(data)
+    if xd is not None:                  # row sums on the device, in chunks (no full int64 copy)
+        x_sum = torch.cat([xd[a0:a0 + 65536].sum(1, dtype=torch.int64) for a0 in range(0, n, 65536)]).cpu().numpy()
+    else:
+        x_sum = row_sums(data)
     draws = expected_draws(x_sum, M, cfg.k, cfg.cap)      # this rank's algorithmic draw-tests per launch
     kern_s = (t_ms / args.steps) / 1e3
     peaks = {}

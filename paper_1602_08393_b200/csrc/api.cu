@@ -38,6 +38,15 @@ int num_sms() {
         int v = 0;
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
         cached[dev] = v > 0 ? v : 148;
+        // The per-call scratch (draw tables, counters) comes from the device's
+        // default stream-ordered pool; keep freed blocks in the pool instead of
+        // returning them to the driver at every synchronisation, so a call never
+        // pays a re-map (seen as occasional 1-2 ms step outliers).
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     return cached[dev];
 }
