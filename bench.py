@@ -440,9 +440,6 @@ def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd=None):
             "api": "wmh_hash_host (pinned host rows -> H2D -> hash -> D2H signatures, synchronised)"}
 
 
-if __name__ == "__main__":
-    sys.exit(main())
-
 
 def measure_collide(wmh, sig, n_pairs, cfg, dev, peaks):
     """a10: wmh_collide on random row pairs of the step's signatures; HBM roofline
@@ -468,3 +465,7 @@ def measure_collide(wmh, sig, n_pairs, cfg, dev, peaks):
     return {"pairs": n_pairs, "ms": ms, "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
             "frac": gbs / hbm, "note": f"signatures {sig.numel() * sig.element_size() / 2**30:.2f} GiB "
                                         f"({'fits' if sig.numel() * sig.element_size() < 100 * 2**20 else 'exceeds'} L2)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

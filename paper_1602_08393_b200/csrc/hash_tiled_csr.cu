@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrPara
     uint32_t *bm = reinterpret_cast<uint32_t *>(slots + H);                    // [bm_words]
     uint32_t *best_all = bm + p.bm_words;                                      // [NW][RB]
     uint32_t *found_all = best_all + CSR_NW * CSR_RB;                          // [NW]
-    uint2 *hq_all = reinterpret_cast<uint2 *>(found_all + CSR_NW);             // [NW][64] queued hot draws
-    uint16_t *trow = reinterpret_cast<uint16_t *>(hq_all + CSR_NW * 64);       // [RB+1] sub-tile starts
+    uint2 *hq_all = reinterpret_cast<uint2 *>(found_all + CSR_NW);             // [NW][128] queued hot draws
+    uint16_t *trow = reinterpret_cast<uint16_t *>(hq_all + CSR_NW * 128);      // [RB+1] sub-tile starts
     uint8_t *alive = reinterpret_cast<uint8_t *>(trow + CSR_RB + 2);           // [RB]
     __shared__ long long s_item;
     __shared__ int s_ntiles, s_hash, s_nalive;
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrPara
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *best = best_all + warp * CSR_RB;
     volatile uint32_t *found = found_all + warp;
-    uint2 *hq = hq_all + warp * 64;
+    uint2 *hq = hq_all + warp * 128;
     unsigned long long sat = 0;
 
     for (;;) {
@@ -212,20 +212,31 @@ __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrPara
                         }
                     }
                     __syncwarp();
-                    if (lane < 32 && count < 64) hq[lane] = hq[lane + 32];   // keep the overflow
+                    const uint2 k1 = hq[lane + 32], k2 = hq[lane + 64], k3 = hq[lane + 96];   // keep the overflow
+                    __syncwarp();
+                    hq[lane] = k1;
+                    hq[lane + 32] = k2;
+                    hq[lane + 64] = k3;
                     __syncwarp();
                 };
                 int qn = 0;
-                for (uint32_t t0 = 0; t0 < p.cap && (int)*found < nalive; t0 += 32) {
-                    const uint32_t t = t0 + lane;
-                    const uint32_t r = mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M);
-                    const uint32_t bk = r >> p.bshift;
-                    const bool hot = t < p.cap && ((bm[bk >> 5] >> (bk & 31)) & 1u);
-                    const unsigned hm = __ballot_sync(0xFFFFFFFFu, hot);
-                    if (hot) hq[qn + __popc(hm & ((1u << lane) - 1))] = make_uint2(r, t);
-                    qn += __popc(hm);
+                const unsigned lt = (1u << lane) - 1;
+                // two independent draws per lane per iteration (t0 + lane, t0 + 32 + lane)
+                // give the scheduler two SplitMix64 chains to interleave
+                for (uint32_t t0 = 0; t0 < p.cap && (int)*found < nalive; t0 += 64) {
+                    const uint32_t ta = t0 + lane, tb = t0 + 32 + lane;
+                    const uint32_t ra = mulhi_range(splitmix64(keyj ^ (uint64_t)ta), p.M);
+                    const uint32_t rb = mulhi_range(splitmix64(keyj ^ (uint64_t)tb), p.M);
+                    const uint32_t ba = ra >> p.bshift, bb = rb >> p.bshift;
+                    const bool hota = ta < p.cap && ((bm[ba >> 5] >> (ba & 31)) & 1u);
+                    const bool hotb = tb < p.cap && ((bm[bb >> 5] >> (bb & 31)) & 1u);
+                    const unsigned ha = __ballot_sync(0xFFFFFFFFu, hota), hb = __ballot_sync(0xFFFFFFFFu, hotb);
+                    if (hota) hq[qn + __popc(ha & lt)] = make_uint2(ra, ta);
+                    qn += __popc(ha);
+                    if (hotb) hq[qn + __popc(hb & lt)] = make_uint2(rb, tb);
+                    qn += __popc(hb);
                     __syncwarp();
-                    if (qn >= 32) { resolve(32); qn -= 32; }
+                    while (qn >= 32) { resolve(32); qn -= 32; }
                 }
                 if (qn > 0) resolve(qn);                              // flush (the loop may end early)
                 // ---- a9: first green t + 1, or the cap ----------------------------
@@ -258,7 +269,7 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     while (((uint64_t)M + (1ull << bshift) - 1) >> bshift > (1ull << 19)) bshift++;
     // bitmap words rounded to 16 B so the arrays after it stay 8/16-byte aligned
     const int bm_words = (((int)((((uint64_t)M + (1ull << bshift) - 1) >> bshift) + 31) / 32) + 3) & ~3;
-    const size_t fixed = (size_t)bm_words * 4 + (size_t)CSR_NW * CSR_RB * 4 + CSR_NW * 4 + (size_t)CSR_NW * 64 * 8 +
+    const size_t fixed = (size_t)bm_words * 4 + (size_t)CSR_NW * CSR_RB * 4 + CSR_NW * 4 + (size_t)CSR_NW * 128 * 8 +
                          (CSR_RB + 2) * 2 + CSR_RB + 64;
     if ((size_t)smem_optin < fixed + 8 * 1024) return WMH_OK;
     int hbits = 0;
