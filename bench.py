@@ -337,6 +337,13 @@ def main():
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     algo_used = wmh.last_algo or args.algo
     roof = roofline(algo_used, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
+    try:                                 # DRAM bytes per launch of this kernel from the committed ncu capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"{cfg.name}/{n}/{algo_used}")
+        if tr:
+            roof["traffic"] = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            roof["traffic_source"] = tr["source"]
+    except (OSError, ValueError):
+        pass
 
     # ---- e2e: the public host-buffer API, H2D rows + hash + D2H signatures every step
     e2e = None

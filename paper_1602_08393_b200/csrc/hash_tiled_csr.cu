@@ -98,7 +98,7 @@ __device__ void big_row(const CsrParams &p, int64_t n, uint32_t j0, uint32_t j1,
     }
 }
 
-template <int SIGB>
+template <int SIGB, int DPL>   // DPL: draws per lane per loop iteration (independent SplitMix64 chains)
 __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrParams p) {
     extern __shared__ __align__(16) unsigned long long csmem[];
     const int H = 1 << p.hbits;
@@ -223,18 +223,22 @@ __global__ void __launch_bounds__(CSR_NT, 1) hash_tiled_csr_kernel(const CsrPara
                 const unsigned lt = (1u << lane) - 1;
                 // two independent draws per lane per iteration (t0 + lane, t0 + 32 + lane)
                 // give the scheduler two SplitMix64 chains to interleave
-                for (uint32_t t0 = 0; t0 < p.cap && (int)*found < nalive; t0 += 64) {
-                    const uint32_t ta = t0 + lane, tb = t0 + 32 + lane;
-                    const uint32_t ra = mulhi_range(splitmix64(keyj ^ (uint64_t)ta), p.M);
-                    const uint32_t rb = mulhi_range(splitmix64(keyj ^ (uint64_t)tb), p.M);
-                    const uint32_t ba = ra >> p.bshift, bb = rb >> p.bshift;
-                    const bool hota = ta < p.cap && ((bm[ba >> 5] >> (ba & 31)) & 1u);
-                    const bool hotb = tb < p.cap && ((bm[bb >> 5] >> (bb & 31)) & 1u);
-                    const unsigned ha = __ballot_sync(0xFFFFFFFFu, hota), hb = __ballot_sync(0xFFFFFFFFu, hotb);
-                    if (hota) hq[qn + __popc(ha & lt)] = make_uint2(ra, ta);
-                    qn += __popc(ha);
-                    if (hotb) hq[qn + __popc(hb & lt)] = make_uint2(rb, tb);
-                    qn += __popc(hb);
+                for (uint32_t t0 = 0; t0 < p.cap && (int)*found < nalive; t0 += 32 * DPL) {
+                    uint32_t rr[DPL];
+                    bool hot[DPL];
+#pragma unroll
+                    for (int u = 0; u < DPL; u++) {
+                        const uint32_t t = t0 + 32 * u + lane;
+                        rr[u] = mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M);
+                        const uint32_t bk = rr[u] >> p.bshift;
+                        hot[u] = t < p.cap && ((bm[bk >> 5] >> (bk & 31)) & 1u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < DPL; u++) {
+                        const unsigned hm = __ballot_sync(0xFFFFFFFFu, hot[u]);
+                        if (hot[u]) hq[qn + __popc(hm & lt)] = make_uint2(rr[u], t0 + 32 * u + lane);
+                        qn += __popc(hm);
+                    }
                     __syncwarp();
                     while (qn >= 32) { resolve(32); qn -= 32; }
                 }
@@ -317,13 +321,16 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "csr counter memset");
     p.item_ctr = ctr;
     const int grid = (int)min((int64_t)sms, p.n_items);
-    if (a.sig_bytes == 1) {
-        WMH_CUDA_TRY(cudaFuncSetAttribute(hash_tiled_csr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "csr smem attr");
-        hash_tiled_csr_kernel<1><<<grid, CSR_NT, smem, a.stream>>>(p);
-    } else {
-        WMH_CUDA_TRY(cudaFuncSetAttribute(hash_tiled_csr_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "csr smem attr");
-        hash_tiled_csr_kernel<2><<<grid, CSR_NT, smem, a.stream>>>(p);
-    }
+    static const int dpl = getenv("WMH_CSR_DPL") ? atoi(getenv("WMH_CSR_DPL")) : 1;
+    auto go = [&](auto kern) -> wmh_status {
+        WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "csr smem attr");
+        kern<<<grid, CSR_NT, smem, a.stream>>>(p);
+        return WMH_OK;
+    };
+    wmh_status lst;
+    if (a.sig_bytes == 1) lst = dpl == 2 ? go(hash_tiled_csr_kernel<1, 2>) : go(hash_tiled_csr_kernel<1, 1>);
+    else lst = dpl == 2 ? go(hash_tiled_csr_kernel<2, 2>) : go(hash_tiled_csr_kernel<2, 1>);
+    if (lst != WMH_OK) { cudaFreeAsync(ctr, a.stream); return lst; }
     WMH_LAUNCH_CHECK("hash_tiled_csr launch");
     if (getenv("WMH_TILED_STATS"))
         fprintf(stderr, "[wmh tiled csr] H=%d cap_nnz=%d rb=%d blocks=%lld hchunk=%d bshift=%d bm_words=%d smem=%zu\n", H,
