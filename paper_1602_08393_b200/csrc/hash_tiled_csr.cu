@@ -321,15 +321,17 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "csr counter memset");
     p.item_ctr = ctr;
     const int grid = (int)min((int64_t)sms, p.n_items);
-    static const int dpl = getenv("WMH_CSR_DPL") ? atoi(getenv("WMH_CSR_DPL")) : 1;
+    static const int dpl = getenv("WMH_CSR_DPL") ? atoi(getenv("WMH_CSR_DPL")) : 2;   // 2: measured best
     auto go = [&](auto kern) -> wmh_status {
         WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "csr smem attr");
         kern<<<grid, CSR_NT, smem, a.stream>>>(p);
         return WMH_OK;
     };
     wmh_status lst;
-    if (a.sig_bytes == 1) lst = dpl == 2 ? go(hash_tiled_csr_kernel<1, 2>) : go(hash_tiled_csr_kernel<1, 1>);
-    else lst = dpl == 2 ? go(hash_tiled_csr_kernel<2, 2>) : go(hash_tiled_csr_kernel<2, 1>);
+    if (a.sig_bytes == 1)
+        lst = dpl == 1 ? go(hash_tiled_csr_kernel<1, 1>) : dpl == 4 ? go(hash_tiled_csr_kernel<1, 4>) : go(hash_tiled_csr_kernel<1, 2>);
+    else
+        lst = dpl == 1 ? go(hash_tiled_csr_kernel<2, 1>) : dpl == 4 ? go(hash_tiled_csr_kernel<2, 4>) : go(hash_tiled_csr_kernel<2, 2>);
     if (lst != WMH_OK) { cudaFreeAsync(ctr, a.stream); return lst; }
     WMH_LAUNCH_CHECK("hash_tiled_csr launch");
     if (getenv("WMH_TILED_STATS"))
