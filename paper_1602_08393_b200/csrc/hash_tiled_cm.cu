@@ -34,7 +34,7 @@ namespace wmh {
 constexpr int CM_NT = 512;
 constexpr int CM_NW = CM_NT / 32;
 constexpr int CM_STRAG = 4;
-constexpr int CM_RMAX = 128;
+constexpr int CM_HB = 4;                 // hashes per claimed block (results flushed 4 per row-store)
 
 struct CmParams {
     const uint8_t *x;
@@ -45,6 +45,7 @@ struct CmParams {
     uint32_t k, cap, M, uni_m;
     uint64_t S;
     int chunk;                   // 0 = auto (from the tile's effective sparsity)
+    int vec_flush;               // k % 4 == 0 and sig aligned: 4-hash row stores
     const uint2 *table;          // [k][T0] (c * Rp, off)
     const uint32_t *pack;
     void *sig;
@@ -147,8 +148,8 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     uint2 *swin_all = sbuf_all + CM_NW * T0;                                        // [NW][32]
     uint4 *sr0_all = reinterpret_cast<uint4 *>(swin_all + CM_NW * 32);              // [NW][32] round-0 consts
     uint32_t *spart_all = reinterpret_cast<uint32_t *>(sr0_all + CM_NW * 32);       // [NW][32] partial h4
-    uint16_t *hres_all = reinterpret_cast<uint16_t *>(spart_all + CM_NW * 32);      // [NW][R] results
-    uint16_t *spend_all = hres_all + CM_NW * R;                                     // [NW][2][R]
+    uint16_t *hres_all = reinterpret_cast<uint16_t *>(spart_all + CM_NW * 32);      // [NW][HB][R] results
+    uint16_t *spend_all = hres_all + CM_NW * CM_HB * R;                             // [NW][2][R]
     uint8_t *sflag4 = reinterpret_cast<uint8_t *>(spend_all + CM_NW * 2 * R);       // [NWD] live-row nibbles
     __shared__ long long s_item, s_next;
     __shared__ int s_hash, s_nalive;
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     uint2 *swin = swin_all + warp * 32;
     uint4 *sr0 = sr0_all + warp * 32;
     uint32_t *spart = spart_all + warp * 32;
-    uint16_t *hres = hres_all + warp * R;
+    uint16_t *hres_blk = hres_all + warp * CM_HB * R;                              // [HB][R]
     uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
     unsigned long long sat = 0;
     const int words = p.D >> 2;                        // D % 4 == 0 (launcher)
@@ -235,16 +236,19 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             C = s > 0.2 ? 8 : s > 0.1 ? 16 : 32;
         }
 
-        // ---- hashes: one warp per hash, next hash's draws prefetched --------------
+        // ---- hashes: a warp claims blocks of CM_HB consecutive hashes (the next
+        //      block one block ahead, hiding the shared atomic), prefetches the
+        //      next hash's draws, and flushes a block's results with one store
+        //      per row -------------------------------------------------------------
         auto grab = [&]() {
-            int jj = 0;
-            if (lane == 0) jj = atomicAdd(&s_hash, 1);
-            return j0 + (uint32_t)__shfl_sync(0xFFFFFFFFu, jj, 0);
+            int bb = 0;
+            if (lane == 0) bb = atomicAdd(&s_hash, 1);
+            return min(j1, j0 + (uint32_t)CM_HB * (uint32_t)__shfl_sync(0xFFFFFFFFu, bb, 0));
         };
-        // hash indices are claimed two ahead so the shared atomic's latency is
-        // hidden behind a whole hash; the next hash's draws are prefetched
-        uint32_t j = grab();
-        uint32_t jn = grab();
+        uint32_t jb = grab();                          // current block [jb, je)
+        uint32_t je = min(j1, jb + CM_HB);
+        uint32_t jb_next = jb < j1 ? grab() : j1;      // next block's first hash
+        uint32_t j = jb;
         uint4 pre[4];
         if (j < j1) {
             const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0);
@@ -256,7 +260,8 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 #pragma unroll
             for (int i = 0; i < 4; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
             __syncwarp();
-            const uint32_t jnn = jn < j1 ? grab() : j1;
+            const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
+            uint16_t *hres = hres_blk + (j - jb) * R;
             if (jn < j1) {
                 const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0);
 #pragma unroll
@@ -376,15 +381,30 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
                     }
             }
             __syncwarp();
-            // ---- a9: flush this hash's column of signatures ----------------------
-            {
+            if (j + 1 == je) {
+                // ---- a9: flush the block: row r's hashes jb..je-1 are contiguous in
+                //      sig, one 4-hash store per row when the block is full and aligned
+                __syncwarp();
                 using sig_t = typename std::conditional<SIGB == 1, uint8_t, uint16_t>::type;
-                sig_t *ptr = reinterpret_cast<sig_t *>(p.sig) + (row0 + lane) * (int64_t)p.k + j;
+                sig_t *ptr = reinterpret_cast<sig_t *>(p.sig) + (row0 + lane) * (int64_t)p.k + jb;
                 const int64_t step = 32 * (int64_t)p.k;
-                for (int r = lane; r < nr; r += 32, ptr += step) *ptr = (sig_t)hres[r];
+                const int nh = (int)(je - jb);
+                if (nh == CM_HB && p.vec_flush) {
+                    for (int r = lane; r < nr; r += 32, ptr += step) {
+                        const uint32_t h0 = hres_blk[r], h1 = hres_blk[R + r], h2 = hres_blk[2 * R + r],
+                                       h3 = hres_blk[3 * R + r];
+                        if (SIGB == 2) *reinterpret_cast<uint2 *>(ptr) = make_uint2(h0 | (h1 << 16), h2 | (h3 << 16));
+                        else *reinterpret_cast<uint32_t *>(ptr) = h0 | (h1 << 8) | (h2 << 16) | (h3 << 24);
+                    }
+                } else {
+                    for (int r = lane; r < nr; r += 32, ptr += step)
+                        for (int u = 0; u < nh; u++) ptr[u] = (sig_t)hres_blk[u * R + r];
+                }
+                jb = jb_next;
+                je = min(j1, jb + CM_HB);
+                jb_next = jb < j1 ? grab() : j1;
             }
             j = jn;
-            jn = jnn;
         }
     }
     if (p.n_sat) {
@@ -395,7 +415,7 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 
 static size_t cm_smem(int D, int R, int Rp) {
     return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 8 + (size_t)CM_NW * 32 * 16 +
-           (size_t)CM_NW * 32 * 4 + (size_t)CM_NW * R * 2 + (size_t)CM_NW * 2 * R * 2 + (size_t)(R / 4) + 16;
+           (size_t)CM_NW * 32 * 4 + (size_t)CM_NW * CM_HB * R * 2 + (size_t)CM_NW * 2 * R * 2 + (size_t)(R / 4) + 16;
 }
 
 template <int SIGB, int P>
@@ -427,7 +447,7 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
     const int sms = num_sms();
     int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 8, ((int64_t)sms * 8 + n_tiles - 1) / n_tiles));
-    const int hchunk = (int)((a.k + n_hchunks - 1) / n_hchunks);
+    const int hchunk = (int)(((a.k + n_hchunks - 1) / n_hchunks + CM_HB - 1) / CM_HB * CM_HB);   // blocks stay 4-aligned
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
 
     uint8_t *scratch = nullptr;
@@ -456,6 +476,7 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     p.uni_m = uni_m;
     p.S = a.S;
     p.chunk = a.chunk == 4 ? 8 : a.chunk;
+    p.vec_flush = (a.k % CM_HB == 0) && ((uintptr_t)a.sig % (size_t)(CM_HB * a.sig_bytes) == 0);
     p.table = table;
     p.pack = a.L->cell_pack;
     p.sig = a.sig;

@@ -321,7 +321,8 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "csr counter memset");
     p.item_ctr = ctr;
     const int grid = (int)min((int64_t)sms, p.n_items);
-    static const int dpl = getenv("WMH_CSR_DPL") ? atoi(getenv("WMH_CSR_DPL")) : 2;   // 2: measured best
+    // independent SplitMix64 chains per lane: 4 measured best on c3 (119 vs 126 vs 141 ms for 4 / 2 / 1)
+    static const int dpl = getenv("WMH_CSR_DPL") ? atoi(getenv("WMH_CSR_DPL")) : 4;
     auto go = [&](auto kern) -> wmh_status {
         WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "csr smem attr");
         kern<<<grid, CSR_NT, smem, a.stream>>>(p);
