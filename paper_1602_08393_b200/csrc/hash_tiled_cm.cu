@@ -34,7 +34,7 @@ namespace wmh {
 constexpr int CM_NT = 512;
 constexpr int CM_NW = CM_NT / 32;
 constexpr int CM_STRAG = 4;
-constexpr int CM_HB = 4;                 // hashes per claimed block (results flushed 4 per row-store)
+constexpr int CM_HB = 8;                 // hashes per claimed block (results flushed 8 per row)
 
 struct CmParams {
     const uint8_t *x;
@@ -391,10 +391,22 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
                 const int nh = (int)(je - jb);
                 if (nh == CM_HB && p.vec_flush) {
                     for (int r = lane; r < nr; r += 32, ptr += step) {
-                        const uint32_t h0 = hres_blk[r], h1 = hres_blk[R + r], h2 = hres_blk[2 * R + r],
-                                       h3 = hres_blk[3 * R + r];
-                        if (SIGB == 2) *reinterpret_cast<uint2 *>(ptr) = make_uint2(h0 | (h1 << 16), h2 | (h3 << 16));
-                        else *reinterpret_cast<uint32_t *>(ptr) = h0 | (h1 << 8) | (h2 << 16) | (h3 << 24);
+                        uint32_t hv[CM_HB];
+#pragma unroll
+                        for (int u = 0; u < CM_HB; u++) hv[u] = hres_blk[u * R + r];
+                        if (SIGB == 2) {
+                            const uint4 v = make_uint4(hv[0] | (hv[1] << 16), hv[2] | (hv[3] << 16),
+                                                       hv[4] | (hv[5] << 16), hv[6] | (hv[7] << 16));
+                            if (p.vec_flush == 2) {
+                                *reinterpret_cast<uint4 *>(ptr) = v;               // 16-byte aligned rows
+                            } else {
+                                reinterpret_cast<uint2 *>(ptr)[0] = make_uint2(v.x, v.y);
+                                reinterpret_cast<uint2 *>(ptr)[1] = make_uint2(v.z, v.w);
+                            }
+                        } else {
+                            *reinterpret_cast<uint2 *>(ptr) = make_uint2(hv[0] | (hv[1] << 8) | (hv[2] << 16) | (hv[3] << 24),
+                                                                         hv[4] | (hv[5] << 8) | (hv[6] << 16) | (hv[7] << 24));
+                        }
                     }
                 } else {
                     for (int r = lane; r < nr; r += 32, ptr += step)
@@ -476,7 +488,12 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     p.uni_m = uni_m;
     p.S = a.S;
     p.chunk = a.chunk == 4 ? 8 : a.chunk;
-    p.vec_flush = (a.k % CM_HB == 0) && ((uintptr_t)a.sig % (size_t)(CM_HB * a.sig_bytes) == 0);
+    // vectorised block flush: 1 = 8-byte stores (k % 4 == 0, sig 8-aligned), 2 = one 16-byte
+    // store per row (uint16 rows 16-byte aligned: k % 8 == 0, sig 16-aligned); uint8 rows: 8 bytes
+    p.vec_flush = 0;
+    if (a.sig_bytes == 2 && a.k % 4 == 0 && (uintptr_t)a.sig % 8 == 0)
+        p.vec_flush = (a.k % 8 == 0 && (uintptr_t)a.sig % 16 == 0) ? 2 : 1;
+    if (a.sig_bytes == 1 && a.k % 8 == 0 && (uintptr_t)a.sig % 8 == 0) p.vec_flush = 1;
     p.table = table;
     p.pack = a.L->cell_pack;
     p.sig = a.sig;
