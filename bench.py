@@ -42,8 +42,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="c2", help="c1..c5 (default c2: the metric's workload, configs[1])")
     p.add_argument("--rows", type=int, default=None, help="rows per GPU (default: the config's N)")
-    p.add_argument("--algo", default="auto", choices=["auto", "simple", "tiled"])
+    p.add_argument("--algo", default="auto", choices=["auto", "simple", "tiled", "index"])
     p.add_argument("--chunk", type=int, default=0, help="tiled: draws per re-queue (0 = auto)")
+    p.add_argument("--horizon", type=int, default=0, help="index: draws filed per hash (0 = auto)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -286,7 +287,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig, chunk=args.chunk)
+        wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig, chunk=args.chunk,
+                 horizon=args.horizon)
 
     clocks = ClockSampler(dev.index if world == 1 else local)
     clocks.start()

@@ -135,7 +135,10 @@ wmh_status wmh_hash(const wmh_layout *layout, const wmh_rows *rows, uint64_t see
 typedef enum {
     WMH_ALGO_AUTO = 0,   /* pick per input (the default used by wmh_hash)         */
     WMH_ALGO_SIMPLE = 1, /* one thread per (row, j), global-table lookups         */
-    WMH_ALGO_TILED = 2   /* rows staged in shared memory, draws shared by a tile  */
+    WMH_ALGO_TILED = 2,  /* rows staged in shared memory, draws shared by a tile  */
+    WMH_ALGO_INDEX = 3   /* draws (j, t < T) filed once per call under their cell; a
+                            row visits only its green draws, then Alg. 3's loop from
+                            t = T for hashes still unresolved (k <= 65536)           */
 } wmh_algo;
 
 typedef struct {
@@ -144,7 +147,11 @@ typedef struct {
                             0 (auto: picked per tile from its effective sparsity
                             s = |x|_1 / M, Eq. 17), 4, 8, 16, 32 */
     int32_t algo_used;   /* OUTPUT: written by wmh_hash_ex with the kernel that ran (wmh_algo) */
-    int32_t reserved[5]; /* must be zero */
+    uint32_t horizon;    /* INDEX: draws t < horizon of every hash are filed (0 = auto:
+                            from the row-sum statistics wmh_prepare gathered, else cap);
+                            clamped to [1, cap].  Performance only: results do not depend
+                            on it */
+    int32_t reserved[4]; /* must be zero */
 } wmh_hash_opts;
 
 wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k,

@@ -186,12 +186,12 @@ def prepare(rows: Rows | None = None, bounds: torch.Tensor | None = None, group=
     return Layout(h.value)
 
 
-last_algo = None     # name of the kernel the last hash() call ran ('simple' / 'tiled')
+last_algo = None     # name of the kernel the last hash() call ran ('simple' / 'tiled' / 'index')
 
 
 def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
          algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
-         chunk: int = 0, stream=None) -> torch.Tensor:
+         chunk: int = 0, horizon: int = 0, stream=None) -> torch.Tensor:
     """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16)."""
     if sig_bytes is None:
         sig_bytes = 1 if cap <= 255 else 2
@@ -203,7 +203,7 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
         raise ValueError("out has the wrong dtype or size")
     if n_saturated is not None and (n_saturated.dtype not in (torch.int64, torch.uint64) or not n_saturated.is_cuda):
         raise ValueError("n_saturated must be a CUDA int64 tensor")
-    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk)
+    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon)
     _lib.check(_lib.load().wmh_hash_ex(layout.handle, ctypes.byref(rows._c()), seed & (2**64 - 1), k, cap, sig_bytes,
                                        _ptr(out), _ptr(n_saturated), ctypes.byref(opts), _stream(stream)))
     global last_algo

@@ -10,7 +10,7 @@ SO_PATH = os.path.join(_HERE, "libwmh.so")
 
 WMH_OK, WMH_EINVAL, WMH_EBOUND, WMH_EEMPTY, WMH_EOVERFLOW, WMH_ECUDA, WMH_ENOMEM = range(7)
 WMH_DENSE, WMH_CSR = 0, 1
-ALGOS = {"auto": 0, "simple": 1, "tiled": 2}
+ALGOS = {"auto": 0, "simple": 1, "tiled": 2, "index": 3}
 STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 4: "WMH_EOVERFLOW",
                 5: "WMH_ECUDA", 6: "WMH_ENOMEM"}
 
@@ -28,7 +28,7 @@ class WmhRows(ctypes.Structure):
 
 class WmhHashOpts(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("chunk", ctypes.c_int32), ("algo_used", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("horizon", ctypes.c_uint32), ("reserved", ctypes.c_int32 * 4)]
 
 
 class WmhError(RuntimeError):

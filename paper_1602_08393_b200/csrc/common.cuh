@@ -17,6 +17,7 @@ struct wmh_layout {
     uint32_t *comp_to_m = nullptr;    // [dim + 1]   CompToM, exclusive prefix (Eq. 3)
     uint32_t *int_to_comp = nullptr;  // [M]         IntToComp (Alg. 4)
     uint32_t *cell_pack = nullptr;    // [M]         (c << 8) | (t - CompToM[c]): Alg. 5 in one load
+    uint64_t rowsum_q = 0;            // 0.1% quantile (power of two) of prepare's nonzero row sums; 0 = unknown
     int device = 0;
 };
 
@@ -98,12 +99,15 @@ struct HashArgs {
     unsigned long long *n_sat;   // may be null
     cudaStream_t stream;
     int chunk;           // TILED: 0 = auto, else 4/8/16/32
+    uint32_t horizon;    // INDEX: draws filed per hash (0 = auto)
 };
 
 wmh_status launch_hash_simple(const HashArgs &a);
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled);
+wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon);
+uint32_t index_horizon(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t hint);
 wmh_status launch_draw_table(uint2 *table, uint32_t k, uint64_t S, uint32_t M, const uint32_t *pack, uint32_t uni_m,
                              uint32_t cmul, cudaStream_t s);
 

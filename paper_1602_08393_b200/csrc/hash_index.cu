@@ -1,0 +1,623 @@
+// hash_index.cu -- WMH_ALGO_INDEX: the draw stream, filed by cell.
+//
+// The draws r_{j,t} of hash j do not depend on the vector: the paper requires
+// the same random sequence for every vector, and Theorem 1's proof
+// rests on exactly that.  So instead of drawing until green for
+// every (row, j) -- Alg. 3, expected 1/s draws per hash (Theorem 2)
+// -- a call draws every (j, t < T) ONCE and files it under its cell r_{j,t}.
+// The green cells of a row x are the intervals [CompToM[c], CompToM[c] + x_c)
+// of its nonzero coordinates (Eq. 4; reading R2), so
+//
+//     h_j(x) = 1 + min { t < T_x : (j, t) filed under a green cell of x }
+//
+// is Alg. 3's first green draw, found by visiting only the row's green draws
+// (k * T_x * s of them in expectation, s = |x|_1 / M, Eq. 17) instead of
+// testing k / s draws.  A hash with no green draw below T_x continues with
+// Alg. 3's own loop from t = T_x (draw-parallel: lane = draw, ballot, first
+// set lane) up to the cap (reading R9).  Both parts compute min{t : r_t green}
+// -- bit-identical to the oracle by construction, for any T_x.
+//
+// The per-call index (device scratch), NESTED epochs:
+//   epoch e holds every draw t < B[e+1];  B = 32, 128, 512, ... (x4), T
+//   key     = e * M + r                    (epoch-major, then cell)
+//   pos     uint32[E*M + 1]: epoch e's entries of cells [lo, hi) are
+//           vals[pos[e*M + lo] .. pos[e*M + hi])
+//   vals    uint32: (j << 16) | t          (k <= 65536, t < cap <= 65535)
+// A row picks ONE epoch e_x from its own s before visiting (T_x = B[e_x + 1]):
+// the one minimising the expected entries k*T*s plus the expected fallback
+// draws k*(1-s)^T*min(1/s, cap - T) (reading R17: a scheduling choice; the
+// result does not depend on it), then reads one range per nonzero coordinate.
+//
+// Build, without global atomics (a two-pass partition + per-chunk counting
+// sort): keys are cut into chunks of 2^cb consecutive keys;
+//   A  each CTA counts its slice of the draws per chunk (shared histogram)
+//   -  exclusive scan of the (chunk, CTA) counts, chunk-major
+//   B  each CTA re-draws its slice and writes (local key, val) pairs to its
+//      private cursor inside each chunk's bucket
+//   C  one CTA per chunk: counting sort of its bucket by local key in shared
+//      memory; writes pos[] of the chunk's keys and the sorted vals.
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace wmh {
+
+constexpr int IX_MAXE = 8;
+constexpr uint32_t IX_NONE = 0xFFFFFFFFu;      // no green draw below the row's horizon yet
+constexpr uint32_t IX_SAT = 0xFFFFFFFEu;       // no green draw below the cap
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+struct IxEpochs {
+    int E;
+    uint32_t B[IX_MAXE + 1];                   // B[0] = 0, epoch e holds t < B[e + 1]
+};
+
+// first epoch that holds draw t (it is also in every later one)
+__device__ __forceinline__ int ix_first_epoch(uint32_t t, const IxEpochs &ep) {
+    int e = 0;
+#pragma unroll
+    for (int i = 1; i < IX_MAXE; i++)
+        if (i < ep.E && t >= ep.B[i]) e = i;
+    return e;
+}
+
+// ------------------------------------------------------------------ build
+struct IxBuild {
+    uint64_t S;
+    uint32_t k, T, M;
+    IxEpochs ep;
+    int cb;                      // chunk = 2^cb consecutive keys
+    uint32_t n_chunks;
+    uint64_t n_keys;             // E * M
+    uint64_t n_draws;            // k * T
+    uint64_t per_cta;            // draws per CTA slice (passes A and B)
+    int n_cta;
+};
+
+template <bool WRITE>
+__global__ void __launch_bounds__(512) ix_partition(const IxBuild b, uint32_t *__restrict__ H,
+                                                    unsigned long long *__restrict__ tmp) {
+    extern __shared__ uint32_t cnt[];          // [n_chunks]: counts (A) or cursors (B)
+    for (uint32_t i = threadIdx.x; i < b.n_chunks; i += blockDim.x)
+        cnt[i] = WRITE ? H[(uint64_t)i * b.n_cta + blockIdx.x] : 0u;
+    __syncthreads();
+    const uint64_t d0 = (uint64_t)blockIdx.x * b.per_cta;
+    const uint64_t d1 = min(b.n_draws, d0 + b.per_cta);
+    for (uint64_t d = d0 + threadIdx.x; d < d1; d += blockDim.x) {
+        const uint32_t j = (uint32_t)(d / b.T), t = (uint32_t)(d - (uint64_t)j * b.T);
+        const uint32_t r = mulhi_range(splitmix64(b.S ^ ((uint64_t)j << 32) ^ (uint64_t)t), b.M);
+        for (int e = ix_first_epoch(t, b.ep); e < b.ep.E; e++) {
+            const uint64_t key = (uint64_t)e * b.M + r;
+            const uint32_t c = (uint32_t)(key >> b.cb);
+            if (WRITE) {
+                const uint32_t p = atomicAdd(cnt + c, 1u);
+                tmp[p] = ((unsigned long long)(key & ((1u << b.cb) - 1)) << 32) | ((j << 16) | t);
+            } else {
+                atomicAdd(cnt + c, 1u);
+            }
+        }
+    }
+    if (!WRITE) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < b.n_chunks; i += blockDim.x)
+            H[1 + (uint64_t)i * b.n_cta + blockIdx.x] = cnt[i];
+    }
+}
+
+constexpr int SC_T = 1024, SC_V = 8, SC_TILE = SC_T * SC_V;
+
+// block-wide exclusive scan (SC_T threads); *total (optional) gets the sum
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *total) {
+    __shared__ uint32_t ws[SC_T / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(FULL, wi, o);
+            if (lane >= o) wi += u;
+        }
+        ws[lane] = wi - w;
+        if (total && lane == 31) *total = wi;
+    }
+    __syncthreads();
+    const uint32_t r = ws[warp] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+// C: one CTA (SC_T threads) per chunk
+__global__ void __launch_bounds__(SC_T) ix_chunk_sort(const IxBuild b, const uint32_t *__restrict__ H,
+                                                      const unsigned long long *__restrict__ tmp,
+                                                      uint32_t *__restrict__ pos, uint32_t *__restrict__ vals) {
+    extern __shared__ uint32_t cnt[];          // [2^cb]
+    const uint32_t c = blockIdx.x, nloc = 1u << b.cb;
+    const uint32_t beg = H[(uint64_t)c * b.n_cta];
+    const uint32_t end = c + 1 < b.n_chunks ? H[(uint64_t)(c + 1) * b.n_cta] : (uint32_t)H[(uint64_t)b.n_chunks * b.n_cta];
+    for (uint32_t i = threadIdx.x; i < nloc; i += SC_T) cnt[i] = 0;
+    __syncthreads();
+    for (uint32_t p = beg + threadIdx.x; p < end; p += SC_T) atomicAdd(cnt + (uint32_t)(tmp[p] >> 32), 1u);
+    __syncthreads();
+    // exclusive scan of cnt[0..nloc): each thread owns nloc / SC_T consecutive counters
+    const uint32_t per = (nloc + SC_T - 1) / SC_T, i0 = threadIdx.x * per;
+    uint32_t s = 0;
+    for (uint32_t i = i0; i < min(nloc, i0 + per); i++) s += cnt[i];
+    uint32_t run = beg + block_excl_scan(s, nullptr);
+    const uint64_t key0 = (uint64_t)c << b.cb;
+    for (uint32_t i = i0; i < min(nloc, i0 + per); i++) {
+        const uint32_t v = cnt[i];
+        cnt[i] = run;
+        if (key0 + i < b.n_keys) pos[key0 + i] = run;
+        run += v;
+    }
+    if (c + 1 == b.n_chunks && threadIdx.x == 0) pos[b.n_keys] = end;
+    __syncthreads();
+    for (uint32_t p = beg + threadIdx.x; p < end; p += SC_T) {
+        const unsigned long long e = tmp[p];
+        vals[atomicAdd(cnt + (uint32_t)(e >> 32), 1u)] = (uint32_t)e;
+    }
+}
+
+// In-place inclusive scan of uint32 a[0..n): tile sums, a one-block scan of
+// the sums, per-tile scans with the carried offset.
+__global__ void __launch_bounds__(SC_T) scan_tile_sums(const uint32_t *__restrict__ a, int64_t n,
+                                                       uint32_t *__restrict__ sums) {
+    const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_V;
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SC_V; i++)
+        if (base + i < n) s += a[base + i];
+    __shared__ uint32_t tot;
+    block_excl_scan(s, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SC_T) scan_sums_excl(uint32_t *__restrict__ sums, int64_t nt) {
+    __shared__ uint32_t carry_s;
+    uint32_t carry = 0;
+    for (int64_t b0 = 0; b0 < nt; b0 += SC_T) {
+        const int64_t i = b0 + threadIdx.x;
+        const uint32_t v = i < nt ? sums[i] : 0u;
+        const uint32_t ex = block_excl_scan(v, &carry_s);
+        if (i < nt) sums[i] = carry + ex;
+        carry += carry_s;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(SC_T) scan_tile_apply(uint32_t *__restrict__ a, int64_t n,
+                                                        const uint32_t *__restrict__ sums) {
+    const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_V;
+    uint32_t v[SC_V], s = 0;
+#pragma unroll
+    for (int i = 0; i < SC_V; i++) {
+        v[i] = base + i < n ? a[base + i] : 0u;
+        s += v[i];
+    }
+    uint32_t run = sums[blockIdx.x] + block_excl_scan(s, nullptr);
+#pragma unroll
+    for (int i = 0; i < SC_V; i++) {
+        run += v[i];
+        if (base + i < n) a[base + i] = run;
+    }
+}
+
+static wmh_status scan_inplace(uint32_t *a, int64_t n, uint32_t *sums, cudaStream_t s) {
+    const int64_t nt = (n + SC_TILE - 1) / SC_TILE;
+    if (nt == 0) return WMH_OK;
+    scan_tile_sums<<<(unsigned)nt, SC_T, 0, s>>>(a, n, sums);
+    WMH_LAUNCH_CHECK("index scan sums");
+    scan_sums_excl<<<1, SC_T, 0, s>>>(sums, nt);
+    WMH_LAUNCH_CHECK("index scan of sums");
+    scan_tile_apply<<<(unsigned)nt, SC_T, 0, s>>>(a, n, sums);
+    WMH_LAUNCH_CHECK("index scan apply");
+    return WMH_OK;
+}
+
+// ------------------------------------------------------------- the rows
+struct IxParams {
+    const uint8_t *x;            // dense rows (n_rows x D) or null
+    const int64_t *row_ptr;      // CSR
+    const int32_t *col;
+    const uint8_t *val;
+    int64_t n_rows, D;
+    const uint32_t *comp_to_m, *pack;
+    uint32_t uni_m, M;
+    const uint32_t *pos, *vals;
+    IxEpochs ep;
+    uint64_t S;
+    uint32_t k, cap;
+    int capn;                    // CSR rows with nnz <= capn stage their columns in shared memory
+    float cf_dense, cf_smem, cf_global;   // cost of one fallback draw / one index entry
+    void *sig;
+    unsigned long long *n_sat;
+    unsigned long long *row_ctr;
+};
+
+// Visit the entries vals[a_i .. a_i + len_i) of the 32 lanes' ranges with all
+// 32 lanes busy: lane f of a window takes flat index base + f, its owner found
+// by a binary search over the inclusive prefix of the lengths; two windows per
+// iteration so every lane has two loads in flight.
+__device__ __forceinline__ void ix_visit(const uint32_t *__restrict__ vals, uint32_t a, uint32_t len,
+                                         uint32_t *h) {
+    const int lane = threadIdx.x & 31;
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += u;
+    }
+    const uint32_t total = __shfl_sync(FULL, incl, 31);
+    const uint32_t start = a - (incl - len);      // entry of flat index f: start_owner + f (mod 2^32)
+    for (uint32_t base = 0; base < total; base += 64) {
+        const uint32_t f0 = base + lane, f1 = f0 + 32;
+        int l0 = 0, l1 = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+            const uint32_t v0 = __shfl_sync(FULL, incl, l0 + step - 1);
+            const uint32_t v1 = __shfl_sync(FULL, incl, l1 + step - 1);
+            if (v0 <= f0) l0 += step;
+            if (v1 <= f1) l1 += step;
+        }
+        const uint32_t s0 = __shfl_sync(FULL, start, l0 & 31), s1 = __shfl_sync(FULL, start, l1 & 31);
+        uint32_t v0 = IX_NONE, v1 = IX_NONE;
+        if (f0 < total) v0 = __ldg(vals + (s0 + f0));
+        if (f1 < total) v1 = __ldg(vals + (s1 + f1));
+        if (f0 < total) atomicMin(h + (v0 >> 16), v0 & 0xFFFFu);
+        if (f1 < total) atomicMin(h + (v1 >> 16), v1 & 0xFFFFu);
+    }
+}
+
+// x_c of the current row: dense byte, or a lower_bound over the CSR slice
+// (its columns staged in shared memory when the row is short enough).
+template <bool CSR>
+__device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const uint8_t *xrow, const uint32_t *scol,
+                                             int64_t e0, int n, uint32_t c) {
+    if (!CSR) return xrow[c];
+    int lo = 0, hi = n;
+    if (scol) {
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (scol[mid] < c) lo = mid + 1;
+            else hi = mid;
+        }
+        return (lo < n && scol[lo] == c) ? (uint32_t)__ldg(p.val + e0 + lo) : 0u;
+    }
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((uint32_t)__ldg(p.col + e0 + mid) < c) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < n && (uint32_t)__ldg(p.col + e0 + lo) == c) ? (uint32_t)__ldg(p.val + e0 + lo) : 0u;
+}
+
+template <int NW>
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long a) {
+    __shared__ unsigned long long ra[NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(FULL, a, o);
+    if (lane == 0) ra[warp] = a;
+    __syncthreads();
+    a = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) a += ra[w];
+    __syncthreads();
+    return a;
+}
+
+// The row's epoch: minimise k*T*s (entries) + k*(1-s)^T * per-hash fallback draws * cf.
+__device__ __forceinline__ int ix_plan(const IxParams &p, float s, float cf) {
+    if (s >= 1.f) return 0;
+    const float l2 = log2f(1.f - s);
+    int best_e = 0;
+    float best = INFINITY;
+    for (int e = 0; e < p.ep.E; e++) {
+        const float T = (float)p.ep.B[e + 1];
+        const float rest = T >= (float)p.cap ? 0.f : fmaxf(32.f, fminf(1.f / s, (float)p.cap - T));
+        const float cost = (float)p.k * (T * s + exp2f(T * l2) * rest * cf);
+        if (cost < best) { best = cost; best_e = e; }
+    }
+    return best_e;
+}
+
+// One CTA of NW warps per row (rows claimed from a counter); h[k] in shared memory.
+template <int SIGB, bool CSR, int NW>
+__global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
+    extern __shared__ uint32_t h[];              // [k] first green t per hash, then [capn] staged columns
+    uint32_t *scol_buf = h + p.k;
+    __shared__ long long s_row;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NT = NW * 32;
+    unsigned long long sat = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_row = (long long)atomicAdd(p.row_ctr, 1ull);
+        for (uint32_t j = threadIdx.x; j < p.k; j += NT) h[j] = IX_NONE;
+        __syncthreads();
+        const long long row = s_row;
+        if (row >= p.n_rows) break;
+        int64_t e0 = 0;
+        int n;
+        const uint8_t *xrow = nullptr;
+        if (CSR) {
+            e0 = p.row_ptr[row];
+            n = (int)(p.row_ptr[row + 1] - e0);
+        } else {
+            xrow = p.x + row * p.D;
+            n = (int)p.D;
+        }
+        const bool staged = CSR && n <= p.capn;
+        // ---- |x|_1 (and the columns of a short CSR row into shared memory)
+        unsigned long long xs = 0;
+        if (CSR) {
+            for (int i = threadIdx.x; i < n; i += NT) {
+                xs += __ldg(p.val + e0 + i);
+                if (staged) scol_buf[i] = (uint32_t)__ldg(p.col + e0 + i);
+            }
+        } else if ((p.D & 3) == 0) {
+            const uint32_t *x4 = reinterpret_cast<const uint32_t *>(xrow);
+            for (int i = threadIdx.x; i < n / 4; i += NT) xs += __dp4a(__ldg(x4 + i), 0x01010101u, 0u);
+        } else {
+            for (int i = threadIdx.x; i < n; i += NT) xs += __ldg(xrow + i);
+        }
+        xs = block_sum<NW>(xs);
+        if (xs == 0) {                           // an all-zero row never turns green (reading R12)
+            for (uint32_t j = threadIdx.x; j < p.k; j += NT) h[j] = IX_SAT;
+        } else {
+            const float s = (float)((double)xs / (double)p.M);
+            const int e = ix_plan(p, s, CSR ? (staged ? p.cf_smem : p.cf_global) : p.cf_dense);
+            const uint32_t T = p.ep.B[e + 1];
+            const uint64_t ebase = (uint64_t)e * p.M;
+            // ---- visit the row's green draws t < T: one range per nonzero coordinate
+            for (int c0 = warp * 32; c0 < n; c0 += NT) {
+                const int i = c0 + lane;
+                uint32_t c = 0, x = 0;
+                if (i < n) {
+                    if (CSR) {
+                        c = staged ? scol_buf[i] : (uint32_t)__ldg(p.col + e0 + i);
+                        x = __ldg(p.val + e0 + i);
+                    } else {
+                        c = (uint32_t)i;
+                        x = __ldg(xrow + i);
+                    }
+                }
+                uint32_t a = 0, len = 0;
+                if (x) {                         // green cells of coordinate c: [lo, lo + x)
+                    const uint32_t lo = p.uni_m ? c * p.uni_m : __ldg(p.comp_to_m + c);
+                    a = __ldg(p.pos + ebase + lo);
+                    len = __ldg(p.pos + ebase + lo + x) - a;
+                }
+                ix_visit(p.vals, a, len, h);
+            }
+            __syncthreads();
+            if (T < p.cap) {
+                // ---- Alg. 3's loop from t = T for the hashes still without a green draw
+                const uint32_t *scol = staged ? scol_buf : nullptr;
+                for (uint32_t jb = warp * 32; jb < p.k; jb += NT) {
+                    const uint32_t jl = jb + lane;
+                    unsigned m = __ballot_sync(FULL, jl < p.k && h[jl] == IX_NONE);
+                    while (m) {
+                        const uint32_t jj = jb + __ffs(m) - 1;
+                        m &= m - 1;
+                        const uint64_t keyj = p.S ^ ((uint64_t)jj << 32);
+                        uint32_t res = IX_SAT;
+                        for (uint32_t t0 = T; t0 < p.cap; t0 += 32) {
+                            const uint32_t t = t0 + lane;
+                            bool g = false;
+                            if (t < p.cap) {
+                                const uint32_t r = mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M);
+                                const uint32_t cell = cell_of(r, p.pack, p.uni_m);
+                                g = (cell & 0xFFu) < ix_row_x<CSR>(p, xrow, scol, e0, n, cell >> 8);
+                            }
+                            const unsigned gm = __ballot_sync(FULL, g);
+                            if (gm) {
+                                res = t0 + __ffs(gm) - 1;
+                                break;
+                            }
+                        }
+                        if (lane == 0) h[jj] = res;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- a9: h = t + 1, or the cap
+        using sig_t = typename std::conditional<SIGB == 1, uint8_t, uint16_t>::type;
+        sig_t *out = reinterpret_cast<sig_t *>(p.sig) + row * (int64_t)p.k;
+        for (uint32_t j = threadIdx.x; j < p.k; j += NT) {
+            const uint32_t v = h[j];
+            const bool s = v >= IX_SAT;
+            sat += s;
+            out[j] = (sig_t)(s ? p.cap : v + 1);
+        }
+    }
+    if (p.n_sat) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sat += __shfl_xor_sync(FULL, sat, o);
+        if (lane == 0 && sat) atomicAdd(p.n_sat, sat);
+    }
+}
+
+template <int SIGB, bool CSR, int NW>
+static wmh_status ix_launch(IxParams p, cudaStream_t s) {
+    auto kern = hash_index_kernel<SIGB, CSR, NW>;
+    int dev = 0, smem_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    // stage CSR columns while 2048/(32*NW) rows still fit per SM
+    if (CSR) {
+        const int rows_sm = 2048 / (32 * NW);
+        const int64_t budget = (int64_t)smem_sm / rows_sm - 1024 - (int64_t)p.k * 4;
+        p.capn = (int)std::max<int64_t>(0, std::min<int64_t>(8192, budget / 4));
+    } else {
+        p.capn = 0;
+    }
+    const size_t smem = (size_t)p.k * 4 + (size_t)p.capn * 4;
+    WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "index smem attr");
+    int per_sm = 0;
+    WMH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem), "index occupancy");
+    if (per_sm < 1) { set_error("wmh_hash: k=%u needs %zu B of shared memory per row", p.k, smem); return WMH_EINVAL; }
+    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, p.n_rows);
+    kern<<<(unsigned)grid, NW * 32, smem, s>>>(p);
+    WMH_LAUNCH_CHECK("hash_index launch");
+    if (getenv("WMH_INDEX_STATS")) {
+        fprintf(stderr, "[wmh index] NW=%d per_sm=%d grid=%lld capn=%d E=%d B=", NW, per_sm, (long long)grid, p.capn,
+                p.ep.E);
+        for (int e = 1; e <= p.ep.E; e++) fprintf(stderr, "%u%s", p.ep.B[e], e < p.ep.E ? "," : "\n");
+    }
+    return WMH_OK;
+}
+
+template <int SIGB, bool CSR>
+static wmh_status ix_launch_nw(const IxParams &p, int nw, cudaStream_t s) {
+    switch (nw) {
+        case 2: return ix_launch<SIGB, CSR, 2>(p, s);
+        case 4: return ix_launch<SIGB, CSR, 4>(p, s);
+        default: return ix_launch<SIGB, CSR, 8>(p, s);
+    }
+}
+
+// Index horizon T: draws t < T are filed.  0 = automatic: from the layout's
+// row-sum statistics (the 0.1% quantile s_q of prepare's rows) T covers
+// ln(4k) / s_q draws, i.e. the k hashes of a row at s_q almost all resolve in
+// the index; without statistics T = cap.
+uint32_t index_horizon(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t hint) {
+    uint64_t T = hint ? hint : cap;
+    if (!hint && L->rowsum_q > 0) {
+        const double s = std::min(0.999, (double)L->rowsum_q / (double)L->M);
+        T = (uint64_t)ceil(log(4.0 * k) / -log1p(-s));
+    }
+    T = std::max<uint64_t>(1, std::min<uint64_t>(T, cap));
+    const uint64_t max_entries = 1ull << 29;     // nested epochs hold <= 4/3 k T entries
+    if ((uint64_t)k * T > max_entries) T = std::max<uint64_t>(1, max_entries / k);
+    return (uint32_t)T;
+}
+
+static IxEpochs index_epochs(uint32_t T) {
+    IxEpochs ep;
+    ep.B[0] = 0;
+    int E = 0;
+    for (uint64_t b = 32; b < T && E < IX_MAXE - 1; b *= 4) ep.B[++E] = (uint32_t)b;
+    // a last step shorter than half the previous boundary is merged into it
+    if (E > 0 && (uint64_t)T * 2 < (uint64_t)ep.B[E] * 3) E--;
+    ep.B[++E] = T;
+    ep.E = E;
+    for (int i = E + 1; i <= IX_MAXE; i++) ep.B[i] = T;
+    return ep;
+}
+
+wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
+    if (a.k > 65536) { set_error("wmh_hash: the index kernel takes k <= 65536"); return WMH_EINVAL; }
+    const wmh_layout *L = a.L;
+    const uint32_t M = (uint32_t)L->M;
+    const uint32_t T = index_horizon(L, a.k, a.cap, horizon);
+    const IxEpochs ep = index_epochs(T);
+
+    IxBuild b;
+    b.S = a.S;
+    b.k = a.k;
+    b.T = T;
+    b.M = M;
+    b.ep = ep;
+    b.n_keys = (uint64_t)ep.E * M;
+    b.n_draws = (uint64_t)a.k * T;
+    uint64_t n_inst = 0;
+    for (int e = 0; e < ep.E; e++) n_inst += (uint64_t)a.k * ep.B[e + 1];
+    if (n_inst >= (1ull << 32)) { set_error("wmh_hash: index too large (k*T)"); return WMH_EINVAL; }
+    const int sms = num_sms();
+    int cb = 8;
+    while (cb < 15 && ((b.n_keys >> cb) > 16383 || (b.n_keys >> cb) > (uint64_t)4 * sms * 8)) cb++;
+    if ((b.n_keys >> cb) > 16383) { set_error("wmh_hash: index key space too large (E*M = %llu)", (unsigned long long)b.n_keys); return WMH_EINVAL; }
+    b.cb = cb;
+    b.n_chunks = (uint32_t)((b.n_keys + (1ull << cb) - 1) >> cb);
+    b.n_cta = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * 2, (b.n_draws + 4095) / 4096));
+    b.per_cta = (b.n_draws + b.n_cta - 1) / b.n_cta;
+
+    const uint64_t n_h = (uint64_t)b.n_chunks * b.n_cta + 1;
+    const int64_t nt = (int64_t)((n_h + SC_TILE - 1) / SC_TILE);
+    auto al = [](uint64_t v) { return (v + 255) & ~(uint64_t)255; };
+    const uint64_t pos_b = al((b.n_keys + 1) * 4), vals_b = al(n_inst * 4), tmp_b = al(n_inst * 8),
+                   h_b = al(n_h * 4), sums_b = al((uint64_t)nt * 4 + 4);
+    uint8_t *scr = nullptr;
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, pos_b + vals_b + tmp_b + h_b + sums_b + 256, a.stream), "index alloc");
+    uint32_t *pos = reinterpret_cast<uint32_t *>(scr);
+    uint32_t *vals = reinterpret_cast<uint32_t *>(scr + pos_b);
+    unsigned long long *tmp = reinterpret_cast<unsigned long long *>(scr + pos_b + vals_b);
+    uint32_t *H = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b + tmp_b);
+    uint32_t *sums = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b + tmp_b + h_b);
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b);
+    wmh_status st = WMH_OK;
+    do {
+        if (cudaMemsetAsync(H, 0, 4, a.stream) != cudaSuccess || cudaMemsetAsync(ctr, 0, 8, a.stream) != cudaSuccess) {
+            st = cuda_fail(cudaGetLastError(), "index memset");
+            break;
+        }
+        const size_t psm = (size_t)b.n_chunks * 4;
+        cudaFuncSetAttribute(ix_partition<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+        cudaFuncSetAttribute(ix_partition<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+        ix_partition<false><<<b.n_cta, 512, psm, a.stream>>>(b, H, tmp);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index count"); break; }
+        if ((st = scan_inplace(H + 1, (int64_t)(n_h - 1), sums, a.stream)) != WMH_OK) break;
+        ix_partition<true><<<b.n_cta, 512, psm, a.stream>>>(b, H, tmp);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index partition"); break; }
+        const size_t csm = (size_t)4 << cb;
+        cudaFuncSetAttribute(ix_chunk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+        ix_chunk_sort<<<b.n_chunks, SC_T, csm, a.stream>>>(b, H, tmp, pos, vals);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index sort"); break; }
+
+        IxParams p;
+        const bool csr = a.rows.kind == WMH_CSR;
+        p.x = a.rows.dense;
+        p.row_ptr = a.rows.row_ptr;
+        p.col = a.rows.col;
+        p.val = a.rows.val;
+        p.n_rows = a.rows.n_rows;
+        p.D = a.rows.dim;
+        p.comp_to_m = L->comp_to_m;
+        p.pack = L->cell_pack;
+        p.uni_m = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
+        p.M = M;
+        p.pos = pos;
+        p.vals = vals;
+        p.ep = ep;
+        p.S = a.S;
+        p.k = a.k;
+        p.cap = a.cap;
+        p.capn = 0;
+        static const float cfs = getenv("WMH_INDEX_CF") ? (float)atof(getenv("WMH_INDEX_CF")) : 0.f;
+        p.cf_dense = cfs > 0 ? cfs : 2.f;
+        p.cf_smem = cfs > 0 ? cfs : 3.f;
+        p.cf_global = cfs > 0 ? cfs : 12.f;
+        p.sig = a.sig;
+        p.n_sat = a.n_sat;
+        p.row_ctr = ctr;
+        // warps per row: >= 2; keep <= ~128 KiB of h[] per SM at 64 resident warps
+        static const int nw_env = getenv("WMH_INDEX_NW") ? atoi(getenv("WMH_INDEX_NW")) : 0;
+        int nw = 2;
+        while (nw < 8 && (uint64_t)(64 / nw) * a.k * 4 > (128u << 10)) nw *= 2;
+        if (nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
+        if (a.sig_bytes == 1) st = csr ? ix_launch_nw<1, true>(p, nw, a.stream) : ix_launch_nw<1, false>(p, nw, a.stream);
+        else st = csr ? ix_launch_nw<2, true>(p, nw, a.stream) : ix_launch_nw<2, false>(p, nw, a.stream);
+    } while (0);
+    cudaFreeAsync(scr, a.stream);
+    return st;
+}
+
+}  // namespace wmh

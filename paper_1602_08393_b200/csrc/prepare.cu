@@ -244,6 +244,35 @@ __global__ void fill_int_to_comp(const uint32_t *__restrict__ comp_to_m, int64_t
 using namespace wmh;
 
 // ===================================================================== C ABI
+// ------------------------------------------------ row-sum statistics
+// hist[b] += 1 for a row with |x|_1 in [2^b, 2^(b+1)); hist[64] counts empty
+// rows.  Warp per row.  The index kernel sizes its draw horizon from the
+// 0.1% quantile (Theorem 2: a row needs ~1/s draws, s = |x|_1 / M, Eq. 17).
+__global__ void __launch_bounds__(256) rowsum_hist(const uint8_t *__restrict__ dense, const int64_t *__restrict__ row_ptr,
+                                                   const uint8_t *__restrict__ val, int64_t n_rows, int64_t dim,
+                                                   unsigned long long *__restrict__ hist) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < n_rows; r += nw) {
+        unsigned long long s = 0;
+        if (dense) {
+            const uint8_t *x = dense + r * dim;
+            if ((dim & 3) == 0 && ((uintptr_t)dense & 3) == 0) {
+                const uint32_t *x4 = reinterpret_cast<const uint32_t *>(x);
+                for (int64_t i = lane; i < dim / 4; i += 32) s += __dp4a(__ldg(x4 + i), 0x01010101u, 0u);
+            } else {
+                for (int64_t i = lane; i < dim; i += 32) s += __ldg(x + i);
+            }
+        } else {
+            const int64_t a = row_ptr[r], b = row_ptr[r + 1];
+            for (int64_t i = a + lane; i < b; i += 32) s += __ldg(val + i);
+        }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        if (lane == 0) atomicAdd(hist + (s ? 63 - __clzll((long long)s) : 64), 1ull);
+    }
+}
+
 extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *stream) {
     wmh_status st = check_rows(rows, true);
     if (st != WMH_OK) return st;
@@ -333,6 +362,16 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
             check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, rows->val, rows->n_rows, dim, rows->nnz,
                                               L->bounds, bad);
     }
+    unsigned long long *hist = nullptr, hhist[65] = {0};
+    const bool stats = rows && rows->n_rows > 0;
+    if (stats) {
+        if (cudaMallocAsync((void **)&hist, sizeof hhist, s) != cudaSuccess) { cudaFreeAsync(scr, s); set_error("wmh_prepare: scratch alloc failed"); return fail(WMH_ENOMEM); }
+        cudaMemsetAsync(hist, 0, sizeof hhist, s);
+        rowsum_hist<<<sms * 8, 256, 0, s>>>(rows->kind == WMH_DENSE ? rows->dense : nullptr, rows->row_ptr, rows->val,
+                                            rows->n_rows, dim, hist);
+        count_launch();
+        cudaMemcpyAsync(hhist, hist, sizeof hhist, cudaMemcpyDeviceToHost, s);
+    }
     scan_block_sums<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, mnmx, mnmx + 1);
     scan_sums_single<<<1, SCAN_B, 0, s>>>(sums, nb, Mdev);
     scan_apply<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, Mdev, L->comp_to_m);
@@ -343,7 +382,16 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     cudaError_t e1 = cudaMemcpyAsync(host, Mdev, sizeof(host), cudaMemcpyDeviceToHost, s);
     cudaError_t e2 = cudaStreamSynchronize(s);
     cudaFreeAsync(scr, s);
+    if (hist) cudaFreeAsync(hist, s);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(cuda_fail(e1 != cudaSuccess ? e1 : e2, "prepare readback"));
+    if (stats) {             // 0.1% quantile of the nonzero row sums, as the bin's lower end 2^b
+        unsigned long long nz = 0, run = 0;
+        for (int b = 0; b < 64; b++) nz += hhist[b];
+        for (int b = 0; b < 64 && nz; b++) {
+            run += hhist[b];
+            if (run * 1000 > nz) { L->rowsum_q = 1ull << b; break; }
+        }
+    }
     const unsigned long long M = host[0], first_bad = host[1];
     const unsigned int mn = (unsigned int)(host[2] & 0xFFFFFFFFu), mx = (unsigned int)(host[2] >> 32);
 

@@ -13,7 +13,7 @@ from tests.helpers import oracle_bounds, oracle_hash, to_rows
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["simple", "tiled", "auto"]
+ALGOS = ["simple", "tiled", "index", "auto"]
 
 
 @pytest.fixture(scope="module")
@@ -35,7 +35,7 @@ def _assert_sig_equal(gpu, ref, what=""):
                              f"oracle {ref[r, j]}")
 
 
-def _run(wmh, data, cfg, k, cap, sig_bytes, algo, seed=None, fixed_bound=None):
+def _run(wmh, data, cfg, k, cap, sig_bytes, algo, seed=None, fixed_bound=None, horizon=0):
     rows = to_rows(data)
     seed = cfg.seed if seed is None else seed
     m = oracle_bounds(data, fixed_bound)
@@ -46,7 +46,7 @@ def _run(wmh, data, cfg, k, cap, sig_bytes, algo, seed=None, fixed_bound=None):
     L = oracle.Layout(m)
     assert layout.M == L.M
     try:
-        sig = wmh.hash(layout, rows, seed, k, cap, sig_bytes, algo=algo)
+        sig = wmh.hash(layout, rows, seed, k, cap, sig_bytes, algo=algo, horizon=horizon)
     except wmh.WmhError as e:
         if algo == "tiled" and "does not take" in str(e):
             pytest.skip("tiled kernel does not take this shape")
@@ -129,6 +129,18 @@ def test_hash_parity_configs(wmh, name, n, k, cap, sb, algo):
     sig, L, _ = _run(wmh, data, cfg, k, cap, sb, algo, fixed_bound=cfg.fixed_bound)
     ref = oracle_hash(L, data, cfg.seed, k, cap)
     _assert_sig_equal(sig, ref, f"{name}/{algo}")
+
+
+@pytest.mark.parametrize("horizon", [1, 31, 33, 200, 0, 65535])
+@pytest.mark.parametrize("name,n,k", [("c2", 400, 500), ("c3", 60, 200), ("c4", 30, 4000), ("c5", 300, 1500)])
+def test_index_horizons(wmh, name, n, k, horizon):
+    """INDEX: any horizon T (the filed draws t < T, then Alg. 3's loop from T)
+    gives the oracle's signatures -- T = 1 is all fallback, T = cap all index;
+    k = 4000 / 1500 / 500 select 8 / 4 / 1 warps per row."""
+    cfg, data = datagen.make(name, n_rows=n)
+    sig, L, _ = _run(wmh, data, cfg, k, cfg.cap, cfg.sig_bytes, "index", fixed_bound=cfg.fixed_bound,
+                     horizon=horizon)
+    _assert_sig_equal(sig, oracle_hash(L, data, cfg.seed, k, cfg.cap), f"{name}/index T={horizon}")
 
 
 @pytest.mark.parametrize("algo", ALGOS)
