@@ -51,6 +51,7 @@ constexpr int IX_MAXE = 8;
 constexpr uint32_t IX_NONE = 0xFFFFFFFFu;      // no green draw below the row's horizon yet
 constexpr uint32_t IX_SAT = 0xFFFFFFFEu;       // no green draw below the cap
 constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int IX_U = 8;                        // windows in flight per warp step
 
 struct IxEpochs {
     int E;
@@ -248,40 +249,6 @@ struct IxParams {
     unsigned long long *row_ctr;
 };
 
-// Visit the entries vals[a_i .. a_i + len_i) of the 32 lanes' ranges with all
-// 32 lanes busy: lane f of a window takes flat index base + f, its owner found
-// by a binary search over the inclusive prefix of the lengths; two windows per
-// iteration so every lane has two loads in flight.
-__device__ __forceinline__ void ix_visit(const uint32_t *__restrict__ vals, uint32_t a, uint32_t len,
-                                         uint32_t *h) {
-    const int lane = threadIdx.x & 31;
-    uint32_t incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += u;
-    }
-    const uint32_t total = __shfl_sync(FULL, incl, 31);
-    const uint32_t start = a - (incl - len);      // entry of flat index f: start_owner + f (mod 2^32)
-    for (uint32_t base = 0; base < total; base += 64) {
-        const uint32_t f0 = base + lane, f1 = f0 + 32;
-        int l0 = 0, l1 = 0;
-#pragma unroll
-        for (int step = 16; step; step >>= 1) {
-            const uint32_t v0 = __shfl_sync(FULL, incl, l0 + step - 1);
-            const uint32_t v1 = __shfl_sync(FULL, incl, l1 + step - 1);
-            if (v0 <= f0) l0 += step;
-            if (v1 <= f1) l1 += step;
-        }
-        const uint32_t s0 = __shfl_sync(FULL, start, l0 & 31), s1 = __shfl_sync(FULL, start, l1 & 31);
-        uint32_t v0 = IX_NONE, v1 = IX_NONE;
-        if (f0 < total) v0 = __ldg(vals + (s0 + f0));
-        if (f1 < total) v1 = __ldg(vals + (s1 + f1));
-        if (f0 < total) atomicMin(h + (v0 >> 16), v0 & 0xFFFFu);
-        if (f1 < total) atomicMin(h + (v1 >> 16), v1 & 0xFFFFu);
-    }
-}
-
 // x_c of the current row: dense byte, or a lower_bound over the CSR slice
 // (its columns staged in shared memory when the row is short enough).
 template <bool CSR>
@@ -335,14 +302,50 @@ __device__ __forceinline__ int ix_plan(const IxParams &p, float s, float cf) {
     return best_e;
 }
 
-// One CTA of NW warps per row (rows claimed from a counter); h[k] in shared memory.
+// Block-wide exclusive scan of a 64-bit value (NW warps); *total gets the sum.
+template <int NW>
+__device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long long v, unsigned long long *total) {
+    __shared__ unsigned long long ws[NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long u = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    unsigned long long before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+        const unsigned long long t = ws[w];
+        if (w < warp) before += t;
+        all += t;
+    }
+    __syncthreads();
+    *total = all;
+    return before + incl - v;
+}
+
+// One CTA of NW warps per row (rows claimed from a counter).  Per batch of up
+// to NT*8 nonzero coordinates: (1) every thread resolves the ranges of its 8
+// coordinates (all pos[] loads in flight together) and the non-empty ranges
+// are compacted into shared memory with the exclusive prefix of their lengths;
+// (2) the warps walk the concatenated entries 32 at a time -- lane f takes
+// flat index base + f, its range found from the boundaries that fall inside
+// the window (one shared load, one OR-reduction, one popc) -- and fold each
+// (j, t) into h[j] = min(h[j], t) with a shared-memory atomic.
 template <int SIGB, bool CSR, int NW>
 __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
-    extern __shared__ uint32_t h[];              // [k] first green t per hash, then [capn] staged columns
-    uint32_t *scol_buf = h + p.k;
+    constexpr int NT = NW * 32, ITEMS = 8, CAPR = NT * ITEMS;
+    extern __shared__ uint32_t smem[];
+    uint32_t *h = smem;                          // [k] first green t per hash
+    uint32_t *ra = h + p.k;                      // [CAPR] range start (index into vals)
+    uint32_t *rp = ra + CAPR;                    // [CAPR + 33] exclusive prefix of range lengths, FULL-padded
+    uint32_t *scol_buf = rp + CAPR + 33;         // [capn] staged CSR columns
     __shared__ long long s_row;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NT = NW * 32;
+    const uint32_t lanemask_le = lane == 31 ? FULL : ((2u << lane) - 1u);
     unsigned long long sat = 0;
     for (;;) {
         if (threadIdx.x == 0) s_row = (long long)atomicAdd(p.row_ctr, 1ull);
@@ -381,29 +384,91 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
             const float s = (float)((double)xs / (double)p.M);
             const int e = ix_plan(p, s, CSR ? (staged ? p.cf_smem : p.cf_global) : p.cf_dense);
             const uint32_t T = p.ep.B[e + 1];
-            const uint64_t ebase = (uint64_t)e * p.M;
-            // ---- visit the row's green draws t < T: one range per nonzero coordinate
-            for (int c0 = warp * 32; c0 < n; c0 += NT) {
-                const int i = c0 + lane;
-                uint32_t c = 0, x = 0;
-                if (i < n) {
-                    if (CSR) {
-                        c = staged ? scol_buf[i] : (uint32_t)__ldg(p.col + e0 + i);
-                        x = __ldg(p.val + e0 + i);
-                    } else {
-                        c = (uint32_t)i;
-                        x = __ldg(xrow + i);
+            const uint32_t *pe = p.pos + (uint64_t)e * p.M;
+            for (int b0 = 0; b0 < n; b0 += CAPR) {
+                // ---- (1) ranges of this thread's 8 coordinates
+                const int i0 = b0 + threadIdx.x * ITEMS;
+                uint32_t xv[ITEMS], lo[ITEMS];
+                if (!CSR && ((p.D & 7) == 0) && i0 + ITEMS <= n) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(xrow + i0));
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++) xv[q] = ((q < 4 ? w.x : w.y) >> (8 * (q & 3))) & 0xFFu;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++)
+                        xv[q] = i0 + q < n ? (CSR ? (uint32_t)__ldg(p.val + e0 + i0 + q) : (uint32_t)__ldg(xrow + i0 + q)) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++) {
+                    uint32_t c = (uint32_t)(i0 + q);
+                    if (CSR && xv[q]) c = staged ? scol_buf[i0 + q] : (uint32_t)__ldg(p.col + e0 + i0 + q);
+                    lo[q] = xv[q] ? (p.uni_m ? c * p.uni_m : __ldg(p.comp_to_m + c)) : 0u;
+                }
+                uint32_t a[ITEMS], len[ITEMS];
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++) {
+                    a[q] = xv[q] ? __ldg(pe + lo[q]) : 0u;
+                    len[q] = xv[q] ? __ldg(pe + lo[q] + xv[q]) : 0u;
+                }
+                uint32_t cnt = 0, sum = 0;
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++) {
+                    len[q] -= a[q];
+                    cnt += len[q] != 0;
+                    sum += len[q];
+                }
+                unsigned long long tot;
+                const unsigned long long ex = block_excl_scan64<NW>(((unsigned long long)cnt << 32) | sum, &tot);
+                uint32_t slot = (uint32_t)(ex >> 32), f = (uint32_t)ex;
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++)
+                    if (len[q]) {
+                        ra[slot] = a[q];
+                        rp[slot] = f;
+                        slot++;
+                        f += len[q];
+                    }
+                const uint32_t nr = (uint32_t)(tot >> 32), L = (uint32_t)tot;
+                if (threadIdx.x < 33) rp[nr + threadIdx.x] = threadIdx.x ? FULL : L;   // end + padding
+                __syncthreads();
+                // ---- (2) walk the entries, 32 per window, warps on contiguous window blocks
+                const uint32_t nwin = (L + 31) >> 5, per = (nwin + NW - 1) / NW;
+                const uint32_t w0 = warp * per, w1 = min(nwin, w0 + per);
+                if (w0 < w1) {
+                    uint32_t base = w0 << 5;
+                    uint32_t o = 0, hi = nr;             // owner of base: last o with rp[o] <= base
+                    while (hi - o > 1) {
+                        const uint32_t mid = (o + hi) >> 1;
+                        if (rp[mid] <= base) o = mid;
+                        else hi = mid;
+                    }
+                    // IX_U windows per step: their ranges are found first (shared loads
+                    // only), then all IX_U vals loads are issued, then the atomics --
+                    // so a lane keeps IX_U global loads in flight
+                    const uint32_t lim = min(L, w1 << 5);
+                    for (uint32_t w = w0; w < w1; w += IX_U) {
+                        uint32_t addr[IX_U];
+#pragma unroll
+                        for (int u = 0; u < IX_U; u++) {
+                            const uint32_t bu = base + 32u * u;
+                            const uint32_t d = rp[o + 1 + lane] - bu;     // padded with FULL past nr
+                            const uint32_t m = __reduce_or_sync(FULL, d < 32 ? (1u << d) : 0u);
+                            const uint32_t own = o + __popc(m & lanemask_le);
+                            addr[u] = ra[own] + (bu + lane - rp[own]);
+                            o = __shfl_sync(FULL, own, 31);
+                        }
+                        uint32_t v[IX_U];
+#pragma unroll
+                        for (int u = 0; u < IX_U; u++)
+                            v[u] = base + 32u * u + lane < lim ? __ldg(p.vals + addr[u]) : IX_NONE;
+#pragma unroll
+                        for (int u = 0; u < IX_U; u++)
+                            if (v[u] != IX_NONE) atomicMin(h + (v[u] >> 16), v[u] & 0xFFFFu);
+                        base += 32u * IX_U;
                     }
                 }
-                uint32_t a = 0, len = 0;
-                if (x) {                         // green cells of coordinate c: [lo, lo + x)
-                    const uint32_t lo = p.uni_m ? c * p.uni_m : __ldg(p.comp_to_m + c);
-                    a = __ldg(p.pos + ebase + lo);
-                    len = __ldg(p.pos + ebase + lo + x) - a;
-                }
-                ix_visit(p.vals, a, len, h);
+                __syncthreads();
             }
-            __syncthreads();
             if (T < p.cap) {
                 // ---- Alg. 3's loop from t = T for the hashes still without a green draw
                 const uint32_t *scol = staged ? scol_buf : nullptr;
@@ -461,12 +526,12 @@ static wmh_status ix_launch(IxParams p, cudaStream_t s) {
     // stage CSR columns while 2048/(32*NW) rows still fit per SM
     if (CSR) {
         const int rows_sm = 2048 / (32 * NW);
-        const int64_t budget = (int64_t)smem_sm / rows_sm - 1024 - (int64_t)p.k * 4;
+        const int64_t budget = (int64_t)smem_sm / rows_sm - 1024 - (int64_t)p.k * 4 - (int64_t)(2 * NW * 32 * 8 + 33) * 4;
         p.capn = (int)std::max<int64_t>(0, std::min<int64_t>(8192, budget / 4));
     } else {
         p.capn = 0;
     }
-    const size_t smem = (size_t)p.k * 4 + (size_t)p.capn * 4;
+    const size_t smem = (size_t)p.k * 4 + (size_t)(2 * NW * 32 * 8 + 33) * 4 + (size_t)p.capn * 4;
     WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "index smem attr");
     int per_sm = 0;
     WMH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem), "index occupancy");
@@ -604,7 +669,7 @@ wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
         static const float cfs = getenv("WMH_INDEX_CF") ? (float)atof(getenv("WMH_INDEX_CF")) : 0.f;
         p.cf_dense = cfs > 0 ? cfs : 2.f;
         p.cf_smem = cfs > 0 ? cfs : 3.f;
-        p.cf_global = cfs > 0 ? cfs : 12.f;
+        p.cf_global = cfs > 0 ? cfs : 16.f;
         p.sig = a.sig;
         p.n_sat = a.n_sat;
         p.row_ctr = ctr;
