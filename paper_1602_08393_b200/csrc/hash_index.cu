@@ -18,7 +18,7 @@
 // -- bit-identical to the oracle by construction, for any T_x.
 //
 // The per-call index (device scratch), NESTED epochs:
-//   epoch e holds every draw t < B[e+1];  B = 32, 128, 512, ... (x4), T
+//   epoch e holds every draw t < B[e+1];  B = 32, 64, ..., 512 (x2), 2048, ... (x4), T
 //   key     = e * M + r                    (epoch-major, then cell)
 //   pos     uint32[E*M + 1]: epoch e's entries of cells [lo, hi) are
 //           vals[pos[e*M + lo] .. pos[e*M + hi])
@@ -47,11 +47,12 @@
 
 namespace wmh {
 
-constexpr int IX_MAXE = 8;
+constexpr int IX_MAXE = 10;
 constexpr uint32_t IX_NONE = 0xFFFFFFFFu;      // no green draw below the row's horizon yet
 constexpr uint32_t IX_SAT = 0xFFFFFFFEu;       // no green draw below the cap
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int IX_U = 8;                        // windows in flight per warp step
+constexpr int IX_FB = 4;                       // fallback hashes per warp at once
 
 struct IxEpochs {
     int E;
@@ -72,7 +73,9 @@ struct IxBuild {
     uint64_t S;
     uint32_t k, T, M;
     IxEpochs ep;
-    int cb;                      // chunk = 2^cb consecutive keys
+    int cb[IX_MAXE];             // epoch e is cut into chunks of 2^cb[e] consecutive cells
+    uint32_t cbase[IX_MAXE + 1]; // first chunk of epoch e; cbase[E] = n_chunks
+    int cb_max;
     uint32_t n_chunks;
     uint64_t n_keys;             // E * M
     uint64_t n_draws;            // k * T
@@ -82,7 +85,7 @@ struct IxBuild {
 
 template <bool WRITE>
 __global__ void __launch_bounds__(512) ix_partition(const IxBuild b, uint32_t *__restrict__ H,
-                                                    unsigned long long *__restrict__ tmp) {
+                                                    uint32_t *__restrict__ tmp) {
     extern __shared__ uint32_t cnt[];          // [n_chunks]: counts (A) or cursors (B)
     for (uint32_t i = threadIdx.x; i < b.n_chunks; i += blockDim.x)
         cnt[i] = WRITE ? H[(uint64_t)i * b.n_cta + blockIdx.x] : 0u;
@@ -93,14 +96,9 @@ __global__ void __launch_bounds__(512) ix_partition(const IxBuild b, uint32_t *_
         const uint32_t j = (uint32_t)(d / b.T), t = (uint32_t)(d - (uint64_t)j * b.T);
         const uint32_t r = mulhi_range(splitmix64(b.S ^ ((uint64_t)j << 32) ^ (uint64_t)t), b.M);
         for (int e = ix_first_epoch(t, b.ep); e < b.ep.E; e++) {
-            const uint64_t key = (uint64_t)e * b.M + r;
-            const uint32_t c = (uint32_t)(key >> b.cb);
-            if (WRITE) {
-                const uint32_t p = atomicAdd(cnt + c, 1u);
-                tmp[p] = ((unsigned long long)(key & ((1u << b.cb) - 1)) << 32) | ((j << 16) | t);
-            } else {
-                atomicAdd(cnt + c, 1u);
-            }
+            const uint32_t c = b.cbase[e] + (r >> b.cb[e]);
+            if (WRITE) tmp[atomicAdd(cnt + c, 1u)] = (j << 16) | t;   // the cell is re-drawn in C
+            else atomicAdd(cnt + c, 1u);
         }
     }
     if (!WRITE) {
@@ -141,35 +139,48 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *total)
     return r;
 }
 
-// C: one CTA (SC_T threads) per chunk
+// C: one CTA (SC_T threads) per chunk: counting sort of the chunk's entries by
+// cell (each entry's cell re-drawn from its (j, t)), pos[] of the chunk's cells,
+// entries scattered into their sorted slots.
 __global__ void __launch_bounds__(SC_T) ix_chunk_sort(const IxBuild b, const uint32_t *__restrict__ H,
-                                                      const unsigned long long *__restrict__ tmp,
-                                                      uint32_t *__restrict__ pos, uint32_t *__restrict__ vals) {
-    extern __shared__ uint32_t cnt[];          // [2^cb]
-    const uint32_t c = blockIdx.x, nloc = 1u << b.cb;
+                                                      const uint32_t *__restrict__ tmp, uint32_t *__restrict__ pos,
+                                                      uint32_t *__restrict__ vals) {
+    extern __shared__ uint32_t cnt[];          // [2^cb[e]]
+    const uint32_t c = blockIdx.x;
+    int e = 0;
+    for (int i = 1; i < b.ep.E; i++)
+        if (c >= b.cbase[i]) e = i;
+    const int cb = b.cb[e];
+    const uint32_t r0 = (c - b.cbase[e]) << cb;
+    const uint32_t nloc = min(1u << cb, b.M - r0);
     const uint32_t beg = H[(uint64_t)c * b.n_cta];
-    const uint32_t end = c + 1 < b.n_chunks ? H[(uint64_t)(c + 1) * b.n_cta] : (uint32_t)H[(uint64_t)b.n_chunks * b.n_cta];
+    const uint32_t end = H[(uint64_t)(c + 1) * b.n_cta];
     for (uint32_t i = threadIdx.x; i < nloc; i += SC_T) cnt[i] = 0;
     __syncthreads();
-    for (uint32_t p = beg + threadIdx.x; p < end; p += SC_T) atomicAdd(cnt + (uint32_t)(tmp[p] >> 32), 1u);
+    for (uint32_t p = beg + threadIdx.x; p < end; p += SC_T) {
+        const uint32_t v = tmp[p];
+        const uint32_t r = mulhi_range(splitmix64(b.S ^ ((uint64_t)(v >> 16) << 32) ^ (uint64_t)(v & 0xFFFFu)), b.M);
+        atomicAdd(cnt + (r - r0), 1u);
+    }
     __syncthreads();
-    // exclusive scan of cnt[0..nloc): each thread owns nloc / SC_T consecutive counters
+    // exclusive scan of cnt[0..nloc): each thread owns consecutive counters
     const uint32_t per = (nloc + SC_T - 1) / SC_T, i0 = threadIdx.x * per;
     uint32_t s = 0;
     for (uint32_t i = i0; i < min(nloc, i0 + per); i++) s += cnt[i];
     uint32_t run = beg + block_excl_scan(s, nullptr);
-    const uint64_t key0 = (uint64_t)c << b.cb;
+    const uint64_t key0 = (uint64_t)e * b.M + r0;
     for (uint32_t i = i0; i < min(nloc, i0 + per); i++) {
         const uint32_t v = cnt[i];
         cnt[i] = run;
-        if (key0 + i < b.n_keys) pos[key0 + i] = run;
+        pos[key0 + i] = run;
         run += v;
     }
     if (c + 1 == b.n_chunks && threadIdx.x == 0) pos[b.n_keys] = end;
     __syncthreads();
     for (uint32_t p = beg + threadIdx.x; p < end; p += SC_T) {
-        const unsigned long long e = tmp[p];
-        vals[atomicAdd(cnt + (uint32_t)(e >> 32), 1u)] = (uint32_t)e;
+        const uint32_t v = tmp[p];
+        const uint32_t r = mulhi_range(splitmix64(b.S ^ ((uint64_t)(v >> 16) << 32) ^ (uint64_t)(v & 0xFFFFu)), b.M);
+        vals[atomicAdd(cnt + (r - r0), 1u)] = v;
     }
 }
 
@@ -239,6 +250,7 @@ struct IxParams {
     const uint32_t *comp_to_m, *pack;
     uint32_t uni_m, M;
     const uint32_t *pos, *vals;
+    const uint2 *table;          // (c, r - CompToM[c]) of draws t < T0 of every hash
     IxEpochs ep;
     uint64_t S;
     uint32_t k, cap;
@@ -254,7 +266,7 @@ struct IxParams {
 template <bool CSR>
 __device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const uint8_t *xrow, const uint32_t *scol,
                                              int64_t e0, int n, uint32_t c) {
-    if (!CSR) return xrow[c];
+    if (!CSR) return scol ? reinterpret_cast<const uint8_t *>(scol)[c] : __ldg(xrow + c);
     int lo = 0, hi = n;
     if (scol) {
         while (lo < hi) {
@@ -344,6 +356,7 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
     uint32_t *rp = ra + CAPR;                    // [CAPR + 33] exclusive prefix of range lengths, FULL-padded
     uint32_t *scol_buf = rp + CAPR + 33;         // [capn] staged CSR columns
     __shared__ long long s_row;
+    __shared__ uint32_t s_nu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lanemask_le = lane == 31 ? FULL : ((2u << lane) - 1u);
     unsigned long long sat = 0;
@@ -363,7 +376,7 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
             xrow = p.x + row * p.D;
             n = (int)p.D;
         }
-        const bool staged = CSR && n <= p.capn;
+        const bool staged = CSR ? n <= p.capn : (p.D & 3) == 0 && (n >> 2) <= p.capn;
         // ---- |x|_1 (and the columns of a short CSR row into shared memory)
         unsigned long long xs = 0;
         if (CSR) {
@@ -373,7 +386,11 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
             }
         } else if ((p.D & 3) == 0) {
             const uint32_t *x4 = reinterpret_cast<const uint32_t *>(xrow);
-            for (int i = threadIdx.x; i < n / 4; i += NT) xs += __dp4a(__ldg(x4 + i), 0x01010101u, 0u);
+            for (int i = threadIdx.x; i < n / 4; i += NT) {
+                const uint32_t w = __ldg(x4 + i);
+                xs += __dp4a(w, 0x01010101u, 0u);
+                if (staged) scol_buf[i] = w;             // the dense row, for the fallback lookups
+            }
         } else {
             for (int i = threadIdx.x; i < n; i += NT) xs += __ldg(xrow + i);
         }
@@ -470,32 +487,74 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
                 __syncthreads();
             }
             if (T < p.cap) {
-                // ---- Alg. 3's loop from t = T for the hashes still without a green draw
+                // ---- Alg. 3's loop from t = T for the hashes still without a green
+                //      draw: their ids are gathered into a shared list (ra[] is free
+                //      now), and each warp runs IX_FB of them at once, lane = draw
+                //      (IX_FB independent lookups in flight per lane)
                 const uint32_t *scol = staged ? scol_buf : nullptr;
-                for (uint32_t jb = warp * 32; jb < p.k; jb += NT) {
-                    const uint32_t jl = jb + lane;
-                    unsigned m = __ballot_sync(FULL, jl < p.k && h[jl] == IX_NONE);
-                    while (m) {
-                        const uint32_t jj = jb + __ffs(m) - 1;
-                        m &= m - 1;
-                        const uint64_t keyj = p.S ^ ((uint64_t)jj << 32);
-                        uint32_t res = IX_SAT;
-                        for (uint32_t t0 = T; t0 < p.cap; t0 += 32) {
+                uint32_t *list = ra;
+                for (;;) {
+                    if (threadIdx.x == 0) s_nu = 0;
+                    __syncthreads();
+                    for (uint32_t jb = warp * 32; jb < p.k; jb += NT) {
+                        const uint32_t jl = jb + lane;
+                        const bool need = jl < p.k && h[jl] == IX_NONE;
+                        const unsigned m = __ballot_sync(FULL, need);
+                        uint32_t base = 0;
+                        if (lane == 0 && m) base = atomicAdd(&s_nu, (uint32_t)__popc(m));
+                        base = __shfl_sync(FULL, base, 0);
+                        const uint32_t slot = base + __popc(m & (lanemask_le >> 1));
+                        if (need && slot < (uint32_t)CAPR) list[slot] = jl;
+                    }
+                    __syncthreads();
+                    const uint32_t U = min(s_nu, (uint32_t)CAPR);
+                    if (U == 0) break;
+                    for (uint32_t ub = warp * IX_FB; ub < U; ub += NT / 32 * IX_FB) {
+                        uint32_t jq[IX_FB];
+                        unsigned live = 0;
+#pragma unroll
+                        for (int q = 0; q < IX_FB; q++) {
+                            jq[q] = ub + q < U ? list[ub + q] : 0u;
+                            if (ub + q < U) live |= 1u << q;
+                        }
+                        uint32_t t0 = T;
+                        for (; live && t0 < p.cap; t0 += 32) {
                             const uint32_t t = t0 + lane;
-                            bool g = false;
-                            if (t < p.cap) {
-                                const uint32_t r = mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M);
-                                const uint32_t cell = cell_of(r, p.pack, p.uni_m);
-                                g = (cell & 0xFFu) < ix_row_x<CSR>(p, xrow, scol, e0, n, cell >> 8);
+                            uint32_t c[IX_FB], off[IX_FB];
+#pragma unroll
+                            for (int q = 0; q < IX_FB; q++) {
+                                c[q] = 0;
+                                off[q] = 0xFFFFFFFFu;
+                                if ((live >> q) & 1u) {
+                                    if (t < (uint32_t)T0) {            // the call's table of the first draws
+                                        const uint2 d = __ldg(p.table + (uint64_t)jq[q] * T0 + t);
+                                        c[q] = d.x;
+                                        off[q] = d.y;
+                                    } else if (t < p.cap) {
+                                        const uint32_t cell = cell_of(
+                                            mulhi_range(splitmix64(p.S ^ ((uint64_t)jq[q] << 32) ^ (uint64_t)t), p.M),
+                                            p.pack, p.uni_m);
+                                        c[q] = cell >> 8;
+                                        off[q] = cell & 0xFFu;
+                                    }
+                                }
                             }
-                            const unsigned gm = __ballot_sync(FULL, g);
-                            if (gm) {
-                                res = t0 + __ffs(gm) - 1;
-                                break;
+#pragma unroll
+                            for (int q = 0; q < IX_FB; q++) {
+                                const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR>(p, xrow, scol, e0, n, c[q]);
+                                const unsigned gm = __ballot_sync(FULL, g);
+                                if (gm) {
+                                    if (lane == 0) h[jq[q]] = t0 + __ffs(gm) - 1;
+                                    live &= ~(1u << q);
+                                }
                             }
                         }
-                        if (lane == 0) h[jj] = res;
+#pragma unroll
+                        for (int q = 0; q < IX_FB; q++)
+                            if (((live >> q) & 1u) && lane == 0) h[jq[q]] = IX_SAT;   // no green draw before the cap
                     }
+                    __syncthreads();
+                    if (s_nu <= (uint32_t)CAPR) break;
                 }
             }
         }
@@ -529,7 +588,10 @@ static wmh_status ix_launch(IxParams p, cudaStream_t s) {
         const int64_t budget = (int64_t)smem_sm / rows_sm - 1024 - (int64_t)p.k * 4 - (int64_t)(2 * NW * 32 * 8 + 33) * 4;
         p.capn = (int)std::max<int64_t>(0, std::min<int64_t>(8192, budget / 4));
     } else {
-        p.capn = 0;
+        // the dense row staged as words for the fallback lookups, when short
+        // (measured: 4 KiB rows cost more in occupancy than they save)
+        static const int stage_max = getenv("WMH_INDEX_STAGE_MAX") ? atoi(getenv("WMH_INDEX_STAGE_MAX")) : 1024;
+        p.capn = p.D <= stage_max ? (int)((p.D + 3) / 4) : 0;
     }
     const size_t smem = (size_t)p.k * 4 + (size_t)(2 * NW * 32 * 8 + 33) * 4 + (size_t)p.capn * 4;
     WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "index smem attr");
@@ -576,7 +638,8 @@ static IxEpochs index_epochs(uint32_t T) {
     IxEpochs ep;
     ep.B[0] = 0;
     int E = 0;
-    for (uint64_t b = 32; b < T && E < IX_MAXE - 1; b *= 4) ep.B[++E] = (uint32_t)b;
+    // x2 steps up to 512 draws (dense rows at s ~ 0.05 stop there), x4 beyond
+    for (uint64_t b = 32; b < T && E < IX_MAXE - 1; b *= (b < 512 ? 2 : 4)) ep.B[++E] = (uint32_t)b;
     // a last step shorter than half the previous boundary is merged into it
     if (E > 0 && (uint64_t)T * 2 < (uint64_t)ep.B[E] * 3) E--;
     ep.B[++E] = T;
@@ -604,27 +667,47 @@ wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
     for (int e = 0; e < ep.E; e++) n_inst += (uint64_t)a.k * ep.B[e + 1];
     if (n_inst >= (1ull << 32)) { set_error("wmh_hash: index too large (k*T)"); return WMH_EINVAL; }
     const int sms = num_sms();
-    int cb = 8;
-    while (cb < 15 && ((b.n_keys >> cb) > 16383 || (b.n_keys >> cb) > (uint64_t)4 * sms * 8)) cb++;
-    if ((b.n_keys >> cb) > 16383) { set_error("wmh_hash: index key space too large (E*M = %llu)", (unsigned long long)b.n_keys); return WMH_EINVAL; }
-    b.cb = cb;
-    b.n_chunks = (uint32_t)((b.n_keys + (1ull << cb) - 1) >> cb);
+    // chunks of ~equal entry counts: epoch e holds k*B[e+1]/M entries per cell
+    // in expectation (the cells are equiprobable), so its chunks span
+    // 2^cb[e] ~ target / density cells; <= 16383 chunks (the partition's
+    // shared cursors), <= 2^15 cells per chunk (the sort's shared histogram).
+    // Fewer, larger chunks measured faster (the partition's scattered stores
+    // dominate): target = n_inst / 1000 (c3: 2.7 ms build, c4: 8.1 ms)
+    static const double chunks_env = getenv("WMH_INDEX_CHUNKS") ? atof(getenv("WMH_INDEX_CHUNKS")) : 0.0;
+    for (double target = std::max(4096.0, (double)n_inst / (chunks_env > 0 ? chunks_env : 1000.0));; target *= 2) {
+        uint64_t nc = 0;
+        b.cb_max = 0;
+        for (int e = 0; e < ep.E; e++) {
+            const double dens = (double)a.k * ep.B[e + 1] / (double)M;
+            int cb = (int)floor(log2(std::max(1.0, target / dens)));
+            cb = std::max(6, std::min(15, cb));
+            b.cb[e] = cb;
+            b.cb_max = std::max(b.cb_max, cb);
+            b.cbase[e] = (uint32_t)nc;
+            nc += ((uint64_t)M + (1ull << cb) - 1) >> cb;
+        }
+        b.cbase[ep.E] = (uint32_t)nc;
+        if (nc <= 16383) { b.n_chunks = (uint32_t)nc; break; }
+        if (target > 1e12) { set_error("wmh_hash: index key space too large (E*M = %llu)", (unsigned long long)b.n_keys); return WMH_EINVAL; }
+    }
     b.n_cta = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * 2, (b.n_draws + 4095) / 4096));
     b.per_cta = (b.n_draws + b.n_cta - 1) / b.n_cta;
 
     const uint64_t n_h = (uint64_t)b.n_chunks * b.n_cta + 1;
     const int64_t nt = (int64_t)((n_h + SC_TILE - 1) / SC_TILE);
     auto al = [](uint64_t v) { return (v + 255) & ~(uint64_t)255; };
-    const uint64_t pos_b = al((b.n_keys + 1) * 4), vals_b = al(n_inst * 4), tmp_b = al(n_inst * 8),
-                   h_b = al(n_h * 4), sums_b = al((uint64_t)nt * 4 + 4);
+    const uint64_t pos_b = al((b.n_keys + 1) * 4), vals_b = al(n_inst * 4), tmp_b = al(n_inst * 4),
+                   h_b = al(n_h * 4), sums_b = al((uint64_t)nt * 4 + 4), tab_b = al((uint64_t)a.k * T0 * 8);
     uint8_t *scr = nullptr;
-    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, pos_b + vals_b + tmp_b + h_b + sums_b + 256, a.stream), "index alloc");
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, pos_b + vals_b + tmp_b + h_b + sums_b + tab_b + 256, a.stream),
+                 "index alloc");
     uint32_t *pos = reinterpret_cast<uint32_t *>(scr);
     uint32_t *vals = reinterpret_cast<uint32_t *>(scr + pos_b);
-    unsigned long long *tmp = reinterpret_cast<unsigned long long *>(scr + pos_b + vals_b);
+    uint32_t *tmp = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b);
     uint32_t *H = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b + tmp_b);
     uint32_t *sums = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b + tmp_b + h_b);
-    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b);
+    uint2 *table = reinterpret_cast<uint2 *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b);
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b + tab_b);
     wmh_status st = WMH_OK;
     do {
         if (cudaMemsetAsync(H, 0, 4, a.stream) != cudaSuccess || cudaMemsetAsync(ctr, 0, 8, a.stream) != cudaSuccess) {
@@ -641,11 +724,14 @@ wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
         ix_partition<true><<<b.n_cta, 512, psm, a.stream>>>(b, H, tmp);
         count_launch();
         if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index partition"); break; }
-        const size_t csm = (size_t)4 << cb;
+        const size_t csm = (size_t)4 << b.cb_max;
         cudaFuncSetAttribute(ix_chunk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         ix_chunk_sort<<<b.n_chunks, SC_T, csm, a.stream>>>(b, H, tmp, pos, vals);
         count_launch();
         if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index sort"); break; }
+
+        const uint32_t uni = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
+        if ((st = launch_draw_table(table, a.k, a.S, M, L->cell_pack, uni, 1u, a.stream)) != WMH_OK) break;
 
         IxParams p;
         const bool csr = a.rows.kind == WMH_CSR;
@@ -661,6 +747,7 @@ wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
         p.M = M;
         p.pos = pos;
         p.vals = vals;
+        p.table = table;
         p.ep = ep;
         p.S = a.S;
         p.k = a.k;
