@@ -286,9 +286,9 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step(timed=False):
         wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig, chunk=args.chunk,
-                 horizon=args.horizon)
+                 horizon=args.horizon, time_kernel=timed)
 
     clocks = ClockSampler(dev.index if world == 1 else local)
     clocks.start()
@@ -301,13 +301,15 @@ def main():
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches = 0
+    kern_ms = []
     for a, b in evs:
         flush.zero_()                        # L2 flush outside the timed events
         a.record(stream)
         l0 = wmh.kernel_launches()
-        step()
+        step(timed=True)                     # + CUDA events around the dominant kernel, on its stream
         launches += wmh.kernel_launches() - l0
         b.record(stream)
+        kern_ms.append(wmh.last_kernel_ms())  # waits for the kernel (after b is queued)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -329,7 +331,7 @@ def main():
     else:
         x_sum = row_sums(data)
     draws = expected_draws(x_sum, M, cfg.k, cfg.cap)      # this rank's algorithmic draw-tests per launch
-    kern_s = (t_ms / args.steps) / 1e3
+    kern_s = statistics.mean(kern_ms) / 1e3               # the dominant kernel's average launch (events)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -339,6 +341,17 @@ def main():
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     algo_used = wmh.last_algo or args.algo
     roof = roofline(algo_used, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
+    if algo_used == "index":
+        if xd is not None:
+            nnz = sum(int((xd[a0:a0 + 65536] != 0).sum().item()) for a0 in range(0, n, 65536))
+        elif isinstance(data, datagen.Dense):
+            nnz = int(np.count_nonzero(data.x))
+        else:
+            nnz = int(len(data.col))
+        roof = roofline_index(x_sum, nnz, M, cfg, wmh.last_horizon, kern_s, in_bytes,
+                              sig.numel() * sig.element_size(), peaks, draws, n_sm, sm_mhz,
+                              dense=isinstance(data, datagen.Dense) or xd is not None)
+    roof["step_share"] = kern_s * 1e3 / (t_ms / args.steps)
     try:                                 # DRAM bytes per launch of this kernel from the committed ncu capture
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"{cfg.name}/{n}/{algo_used}")
         if tr:
@@ -408,6 +421,47 @@ def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
                            f"/ {i_draw:.0f} lane-instr per draw-test ({algo})",
             "frac_vs_paper_loop": achieved / (issue / I_DRAW["simple"] / 1e9),
             "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3, "t_kernel_ms": kern_s * 1e3}
+
+
+def index_epochs(T: int):
+    """The index kernel's nested epoch boundaries for horizon T (hash_index.cu index_epochs)."""
+    B, b = [], 32
+    while b < T and len(B) < 9:
+        B.append(b)
+        b *= 2 if b < 512 else 4
+    if B and 2 * T < 3 * B[-1]:
+        B.pop()
+    return B + [T]
+
+
+def index_plan(s: np.ndarray, k: int, cap: int, B, cf: float) -> np.ndarray:
+    """Per row the horizon T_x the index kernel picks (hash_index.cu ix_plan): the
+    epoch minimising k*T*s + k*(1-s)^T * max(32, min(1/s, cap-T)) * cf."""
+    s = np.clip(s.astype(np.float64), 1e-30, 1 - 1e-12)
+    costs = []
+    for T in B:
+        rest = 0.0 if T >= cap else np.maximum(32.0, np.minimum(1.0 / s, cap - T))
+        costs.append(T * s + np.exp(T * np.log1p(-s)) * rest * cf)
+    return np.asarray(B, np.float64)[np.argmin(np.stack(costs), axis=0)]
+
+
+def roofline_index(x_sum, nnz, M, cfg, T, kern_s, in_bytes, out_bytes, peaks, draws, n_sm, sm_mhz, dense):
+    """INDEX kernel: memory-bound.  Algorithmic bytes per launch = rows in +
+    signatures out + the filed draws the rows must visit (4 B each: k*T_x*s per
+    row, T_x the kernel's own per-row horizon) + two 4 B range bounds per nonzero."""
+    s = x_sum.astype(np.float64) / M
+    live = s > 0
+    Tx = index_plan(s[live], cfg.k, cfg.cap, index_epochs(int(T)), 2.0 if dense else 16.0)
+    entries = float(cfg.k * (Tx * s[live]).sum())
+    algo_bytes = in_bytes + out_bytes + 4.0 * entries + 8.0 * nnz
+    hbm = peaks.get("hbm_gbs", 6545.6)
+    gbs = algo_bytes / kern_s / 1e9
+    issue = n_sm * 4 * 32 * sm_mhz * 1e6
+    return {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
+            "kernel": "index", "peak_source": "MEASURED_PEAKS hbm_gbs (copy)",
+            "algo_bytes": algo_bytes, "entries_visited": entries, "horizon": int(T),
+            "frac_vs_paper_loop": draws / kern_s / 1e9 / (issue / I_DRAW["simple"] / 1e9),
+            "t_kernel_ms": kern_s * 1e3}
 
 
 def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd=None):

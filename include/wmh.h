@@ -150,9 +150,14 @@ typedef struct {
     uint32_t horizon;    /* INDEX: draws t < horizon of every hash are filed (0 = auto:
                             from the row-sum statistics wmh_prepare gathered, else cap);
                             clamped to [1, cap].  Performance only: results do not depend
-                            on it */
-    int32_t reserved[4]; /* must be zero */
+                            on it.  OUTPUT when the index kernel ran: the horizon it used */
+    uint32_t flags;      /* WMH_OPT_TIME_KERNEL: bracket the call's dominant (per-row)
+                            kernel with CUDA events on `stream`; read with
+                            wmh_last_kernel_ms */
+    int32_t reserved[3]; /* must be zero */
 } wmh_hash_opts;
+
+#define WMH_OPT_TIME_KERNEL 1u
 
 wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k,
                        uint32_t cap, int32_t sig_bytes, void *sig_out, uint64_t *n_saturated,
@@ -176,6 +181,11 @@ wmh_status wmh_hash_host(const wmh_layout *layout, const wmh_rows *rows_host, ui
  * Errors: EINVAL, ECUDA. */
 wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k, int64_t n_rows, const int64_t *pairs,
                        int64_t n_pairs, uint32_t *matches, float *jhat, int32_t check_pairs, void *stream);
+
+/* Device time (ms) of the dominant kernel of the last wmh_hash_ex call on this
+ * thread that set WMH_OPT_TIME_KERNEL (CUDA events on its stream).  Waits for
+ * that kernel to finish.  Errors: EINVAL (no such call), ECUDA. */
+wmh_status wmh_last_kernel_ms(float *ms);
 
 /* Thread-local description of the last failure ("" if none). */
 const char *wmh_last_error(void);

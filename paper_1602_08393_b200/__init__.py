@@ -187,11 +187,12 @@ def prepare(rows: Rows | None = None, bounds: torch.Tensor | None = None, group=
 
 
 last_algo = None     # name of the kernel the last hash() call ran ('simple' / 'tiled' / 'index')
+last_horizon = None  # the index horizon T of the last hash() call that ran the index kernel
 
 
 def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
          algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
-         chunk: int = 0, horizon: int = 0, stream=None) -> torch.Tensor:
+         chunk: int = 0, horizon: int = 0, time_kernel: bool = False, stream=None) -> torch.Tensor:
     """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16)."""
     if sig_bytes is None:
         sig_bytes = 1 if cap <= 255 else 2
@@ -203,11 +204,12 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
         raise ValueError("out has the wrong dtype or size")
     if n_saturated is not None and (n_saturated.dtype not in (torch.int64, torch.uint64) or not n_saturated.is_cuda):
         raise ValueError("n_saturated must be a CUDA int64 tensor")
-    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon)
+    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon, _lib.WMH_OPT_TIME_KERNEL if time_kernel else 0)
     _lib.check(_lib.load().wmh_hash_ex(layout.handle, ctypes.byref(rows._c()), seed & (2**64 - 1), k, cap, sig_bytes,
                                        _ptr(out), _ptr(n_saturated), ctypes.byref(opts), _stream(stream)))
-    global last_algo
+    global last_algo, last_horizon
     last_algo = {v: n for n, v in _lib.ALGOS.items()}.get(opts.algo_used, "?")
+    last_horizon = int(opts.horizon) if last_algo == "index" else None
     return out
 
 
@@ -245,6 +247,14 @@ def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, st
 
 def version() -> str:
     return _lib.load().wmh_version().decode()
+
+
+def last_kernel_ms() -> float:
+    """Device time of the dominant kernel of the last hash(..., time_kernel=True) call on
+    this thread (CUDA events on its stream; waits for it)."""
+    ms = ctypes.c_float()
+    _lib.check(_lib.load().wmh_last_kernel_ms(ctypes.byref(ms)))
+    return float(ms.value)
 
 
 def kernel_launches() -> int:

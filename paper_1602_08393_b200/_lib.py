@@ -10,6 +10,7 @@ SO_PATH = os.path.join(_HERE, "libwmh.so")
 
 WMH_OK, WMH_EINVAL, WMH_EBOUND, WMH_EEMPTY, WMH_EOVERFLOW, WMH_ECUDA, WMH_ENOMEM = range(7)
 WMH_DENSE, WMH_CSR = 0, 1
+WMH_OPT_TIME_KERNEL = 1
 ALGOS = {"auto": 0, "simple": 1, "tiled": 2, "index": 3}
 STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 4: "WMH_EOVERFLOW",
                 5: "WMH_ECUDA", 6: "WMH_ENOMEM"}
@@ -17,7 +18,7 @@ STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 
 # Every symbol include/wmh.h declares (tests check the .so exports all of them).
 EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_tables", "wmh_layout_free",
            "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version",
-           "wmh_kernel_launches"]
+           "wmh_kernel_launches", "wmh_last_kernel_ms"]
 
 
 class WmhRows(ctypes.Structure):
@@ -28,7 +29,7 @@ class WmhRows(ctypes.Structure):
 
 class WmhHashOpts(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("chunk", ctypes.c_int32), ("algo_used", ctypes.c_int32),
-                ("horizon", ctypes.c_uint32), ("reserved", ctypes.c_int32 * 4)]
+                ("horizon", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class WmhError(RuntimeError):
@@ -68,6 +69,7 @@ def load() -> ctypes.CDLL:
             "wmh_last_error": (ctypes.c_char_p, []),
             "wmh_version": (ctypes.c_char_p, []),
             "wmh_kernel_launches": (ctypes.c_uint64, []),
+            "wmh_last_kernel_ms": (st, [ctypes.POINTER(ctypes.c_float)]),
         }
         for name, (res, args) in proto.items():
             f = getattr(L, name)

@@ -28,6 +28,36 @@ wmh_status cuda_fail(cudaError_t e, const char *what) {
 }
 
 static std::atomic<unsigned long long> g_launches{0};
+
+// ---- optional event bracket around the dominant kernel of a hash call
+struct KernelTimer {
+    bool on = false;
+    int device = -1;
+    cudaEvent_t a = nullptr, b = nullptr;
+    bool recorded = false;
+};
+static thread_local KernelTimer g_ktimer;
+
+void kernel_timer_begin(cudaStream_t s) {
+    KernelTimer &t = g_ktimer;
+    if (!t.on) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (t.device != dev) {
+        if (t.a) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+        cudaEventCreate(&t.a);
+        cudaEventCreate(&t.b);
+        t.device = dev;
+    }
+    cudaEventRecord(t.a, s);
+}
+
+void kernel_timer_end(cudaStream_t s) {
+    KernelTimer &t = g_ktimer;
+    if (!t.on || !t.b) return;
+    cudaEventRecord(t.b, s);
+    t.recorded = true;
+}
 void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int num_sms() {
@@ -192,7 +222,8 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
     uint32_t horizon = 0;
     if (opts) {
         algo = opts->algo;
-        for (int i = 0; i < 4; i++)
+        if (opts->flags & ~(uint32_t)WMH_OPT_TIME_KERNEL) { set_error("wmh_hash_ex: unknown flags 0x%x", opts->flags); return WMH_EINVAL; }
+        for (int i = 0; i < 3; i++)
             if (opts->reserved[i]) { set_error("wmh_hash_ex: reserved option fields must be zero"); return WMH_EINVAL; }
         chunk = opts->chunk;
         horizon = opts->horizon;
@@ -200,9 +231,15 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
         if (algo < WMH_ALGO_AUTO || algo > WMH_ALGO_INDEX) { set_error("wmh_hash_ex: unknown algo %d", algo); return WMH_EINVAL; }
     }
     int used = 0;
+    g_ktimer.on = opts && (opts->flags & WMH_OPT_TIME_KERNEL);
+    if (g_ktimer.on) g_ktimer.recorded = false;
     st = hash_dispatch(L, rows, seed, k, cap, sig_bytes, sig_out, n_saturated, algo, chunk, horizon, (cudaStream_t)stream,
                        &used);
-    if (opts) opts->algo_used = used;
+    g_ktimer.on = false;
+    if (opts) {
+        opts->algo_used = used;
+        if (used == WMH_ALGO_INDEX) opts->horizon = index_horizon(L, k, cap, horizon);   // the T it filed
+    }
     return st;
 }
 
@@ -379,3 +416,12 @@ extern "C" const char *wmh_last_error(void) { return g_err; }
 extern "C" const char *wmh_version(void) { return "wmh 0.1 sm_100a"; }
 
 extern "C" uint64_t wmh_kernel_launches(void) { return wmh::g_launches.load(std::memory_order_relaxed); }
+
+extern "C" wmh_status wmh_last_kernel_ms(float *ms) {
+    if (!ms) { set_error("wmh_last_kernel_ms: ms is NULL"); return WMH_EINVAL; }
+    KernelTimer &t = g_ktimer;
+    if (!t.recorded) { set_error("wmh_last_kernel_ms: no timed hash call on this thread"); return WMH_EINVAL; }
+    WMH_CUDA_TRY(cudaEventSynchronize(t.b), "kernel timer sync");
+    WMH_CUDA_TRY(cudaEventElapsedTime(ms, t.a, t.b), "kernel timer elapsed");
+    return WMH_OK;
+}

@@ -43,6 +43,10 @@ void count_launch(unsigned n = 1);
     } while (0)
 
 wmh_status check_rows(const wmh_rows *rows, bool need_data);
+// Optional CUDA-event bracket around the dominant (per-row) kernel of a hash
+// call (wmh_hash_opts.flags & WMH_OPT_TIME_KERNEL); read with wmh_last_kernel_ms.
+void kernel_timer_begin(cudaStream_t s);
+void kernel_timer_end(cudaStream_t s);
 int num_sms();
 
 // ---------------------------------------------------------------- the RNG

@@ -599,7 +599,9 @@ static wmh_status ix_launch(IxParams p, cudaStream_t s) {
     WMH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem), "index occupancy");
     if (per_sm < 1) { set_error("wmh_hash: k=%u needs %zu B of shared memory per row", p.k, smem); return WMH_EINVAL; }
     const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, p.n_rows);
+    kernel_timer_begin(s);
     kern<<<(unsigned)grid, NW * 32, smem, s>>>(p);
+    kernel_timer_end(s);
     WMH_LAUNCH_CHECK("hash_index launch");
     if (getenv("WMH_INDEX_STATS")) {
         fprintf(stderr, "[wmh index] NW=%d per_sm=%d grid=%lld capn=%d E=%d B=", NW, per_sm, (long long)grid, p.capn,

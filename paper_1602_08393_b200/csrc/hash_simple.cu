@@ -72,8 +72,10 @@ wmh_status launch_hash_simple(const HashArgs &a) {
     hash_simple_kernel<SB, CS><<<(unsigned)blocks, threads, 0, a.stream>>>(                                      \
         a.rows.dense, a.rows.row_ptr, a.rows.col, a.rows.val, a.rows.n_rows, a.rows.dim, a.L->cell_pack, M, a.S, \
         a.k, a.cap, a.sig, a.n_sat)
+    kernel_timer_begin(a.stream);
     if (a.sig_bytes == 1) { if (csr) WMH_SIMPLE(1, true); else WMH_SIMPLE(1, false); }
     else { if (csr) WMH_SIMPLE(2, true); else WMH_SIMPLE(2, false); }
+    kernel_timer_end(a.stream);
 #undef WMH_SIMPLE
     WMH_LAUNCH_CHECK("hash_simple launch");
     return WMH_OK;

@@ -373,7 +373,9 @@ template <int SIGB, int NT>
 static wmh_status launch_tiled(const TiledParams &p, size_t smem, int grid, cudaStream_t s) {
     auto *fn = hash_tiled_dense_kernel<SIGB, NT>;
     WMH_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "tiled smem attr");
+    kernel_timer_begin(s);
     fn<<<grid, NT, smem, s>>>(p);
+    kernel_timer_end(s);
     WMH_LAUNCH_CHECK("hash_tiled_dense launch");
     return WMH_OK;
 }

@@ -433,7 +433,9 @@ static size_t cm_smem(int D, int R, int Rp) {
 template <int SIGB, int P>
 static void cm_launch(const CmParams &p, size_t smem, int grid, cudaStream_t s) {
     cudaFuncSetAttribute(hash_tiled_cm_kernel<SIGB, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_timer_begin(s);
     hash_tiled_cm_kernel<SIGB, P><<<grid, CM_NT, smem, s>>>(p);
+    kernel_timer_end(s);
 }
 
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {

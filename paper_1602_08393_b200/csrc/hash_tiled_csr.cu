@@ -325,7 +325,9 @@ wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled) {
     static const int dpl = getenv("WMH_CSR_DPL") ? atoi(getenv("WMH_CSR_DPL")) : 4;
     auto go = [&](auto kern) -> wmh_status {
         WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "csr smem attr");
+        kernel_timer_begin(a.stream);
         kern<<<grid, CSR_NT, smem, a.stream>>>(p);
+        kernel_timer_end(a.stream);
         return WMH_OK;
     };
     wmh_status lst;
