@@ -414,7 +414,7 @@ def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
     i_draw = I_DRAW.get(algo, I_DRAW["simple"])
     peak = issue / i_draw / 1e9                     # Gdraw-tests / s
     achieved = draws / kern_s / 1e9
-    hbm = peaks.get("hbm_gbs", 6545.6)
+    hbm = peaks.get("hbm_gbs", 6650.0)
     return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gdraws/s", "frac": achieved / peak,
             "traffic": None, "kernel": algo,
             "peak_source": f"{n_sm} SMs x 128 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) "
@@ -454,7 +454,7 @@ def roofline_index(x_sum, nnz, M, cfg, T, kern_s, in_bytes, out_bytes, peaks, dr
     Tx = index_plan(s[live], cfg.k, cfg.cap, index_epochs(int(T)), 2.0 if dense else 16.0)
     entries = float(cfg.k * (Tx * s[live]).sum())
     algo_bytes = in_bytes + out_bytes + 4.0 * entries + 8.0 * nnz
-    hbm = peaks.get("hbm_gbs", 6545.6)
+    hbm = peaks.get("hbm_gbs", 6650.0)
     gbs = algo_bytes / kern_s / 1e9
     issue = n_sm * 4 * 32 * sm_mhz * 1e6
     return {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
@@ -523,7 +523,7 @@ def measure_collide(wmh, sig, n_pairs, cfg, dev, peaks):
     ms = a.elapsed_time(b) / reps
     sig_bytes = sig.shape[1] * sig.element_size()
     algo_bytes = n_pairs * (2 * sig_bytes + 8 + 16)
-    hbm = peaks.get("hbm_gbs", 6545.6)
+    hbm = peaks.get("hbm_gbs", 6650.0)
     gbs = algo_bytes / (ms / 1e3) / 1e9
     return {"pairs": n_pairs, "ms": ms, "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
             "frac": gbs / hbm, "note": f"signatures {sig.numel() * sig.element_size() / 2**30:.2f} GiB "
