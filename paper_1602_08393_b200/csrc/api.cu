@@ -327,6 +327,26 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     const size_t row_sig = (size_t)k * sig_bytes;
     WMH_CUDA_TRY(cudaEventRecord(E.ev_start, (cudaStream_t)stream), "e2e start event");
     WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_in, E.ev_start, 0), "e2e wait");
+    WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_comp, E.ev_start, 0), "e2e wait");
+    // the index kernel (AUTO's choice for CSR rows) files the draws once for the
+    // whole call; every chunk then only runs its rows kernel
+    const bool use_index = h.kind == WMH_CSR && k <= 65536 && (unsigned long long)h.n_rows * k > (1ull << 20);
+    IndexBuilt ix;
+    HashArgs ha;
+    if (use_index) {
+        ha.L = L;
+        ha.rows = h;
+        ha.S = splitmix64(seed);
+        ha.k = k;
+        ha.cap = cap;
+        ha.sig_bytes = sig_bytes;
+        ha.sig = nullptr;
+        ha.n_sat = nullptr;
+        ha.stream = E.s_comp;
+        ha.chunk = 0;
+        ha.horizon = 0;
+        if ((st = index_build(ha, 0, &ix)) != WMH_OK) return st;
+    }
     for (int64_t ci = 0; ci < n_chunks; ci++) {
         const int slot = (int)(ci % E2E_SLOTS);
         const int64_t a = ci * cr, b = std::min<int64_t>(h.n_rows, a + cr), nr = b - a;
@@ -366,14 +386,22 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
         WMH_CUDA_TRY(cudaEventRecord(E.ev_in[slot], E.s_in), "e2e event");
         WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_comp, E.ev_in[slot], 0), "e2e wait");
         void *dsig = base + in_bytes;
-        int used = 0;
-        st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, 0, E.s_comp, &used);
-        if (st != WMH_OK) return st;
+        if (use_index) {
+            HashArgs ca = ha;
+            ca.rows = d;
+            ca.sig = dsig;
+            st = index_rows(ca, ix);
+        } else {
+            int used = 0;
+            st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, 0, E.s_comp, &used);
+        }
+        if (st != WMH_OK) { if (use_index) index_free(ix, E.s_comp); return st; }
         WMH_CUDA_TRY(cudaEventRecord(E.ev_comp[slot], E.s_comp), "e2e event");
         WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_out, E.ev_comp[slot], 0), "e2e wait");
         WMH_CUDA_TRY(cudaMemcpyAsync((uint8_t *)sig_out_host + a * row_sig, dsig, nr * row_sig, cudaMemcpyDeviceToHost, E.s_out), "e2e D2H signatures");
         WMH_CUDA_TRY(cudaEventRecord(E.ev_out[slot], E.s_out), "e2e event");
     }
+    if (use_index) index_free(ix, E.s_comp);
     WMH_CUDA_TRY(cudaStreamSynchronize(E.s_out), "e2e synchronize");
     return WMH_OK;
 }

@@ -111,6 +111,24 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled);
 wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon);
+// The index of one call, reusable by several row batches of the same (layout,
+// seed, k, cap): built on a.stream, freed stream-ordered.
+constexpr int IX_MAXE = 10;
+struct IxEpochs {
+    int E;
+    uint32_t B[IX_MAXE + 1];                   // B[0] = 0, epoch e holds t < B[e + 1]
+};
+struct IndexBuilt {
+    uint8_t *scr = nullptr;
+    uint32_t *pos = nullptr, *vals = nullptr;
+    uint2 *table = nullptr;
+    unsigned long long *ctr = nullptr;
+    IxEpochs ep{};
+    uint32_t T = 0;
+};
+wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out);
+wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix);
+void index_free(IndexBuilt &ix, cudaStream_t s);
 uint32_t index_horizon(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t hint);
 wmh_status launch_draw_table(uint2 *table, uint32_t k, uint64_t S, uint32_t M, const uint32_t *pack, uint32_t uni_m,
                              uint32_t cmul, cudaStream_t s);

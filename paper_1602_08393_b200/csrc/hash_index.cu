@@ -47,17 +47,11 @@
 
 namespace wmh {
 
-constexpr int IX_MAXE = 10;
 constexpr uint32_t IX_NONE = 0xFFFFFFFFu;      // no green draw below the row's horizon yet
 constexpr uint32_t IX_SAT = 0xFFFFFFFEu;       // no green draw below the cap
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int IX_U = 8;                        // windows in flight per warp step
 constexpr int IX_FB = 4;                       // fallback hashes per warp at once
-
-struct IxEpochs {
-    int E;
-    uint32_t B[IX_MAXE + 1];                   // B[0] = 0, epoch e holds t < B[e + 1]
-};
 
 // first epoch that holds draw t (it is also in every later one)
 __device__ __forceinline__ int ix_first_epoch(uint32_t t, const IxEpochs &ep) {
@@ -650,7 +644,8 @@ static IxEpochs index_epochs(uint32_t T) {
     return ep;
 }
 
-wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
+wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
+    *out = IndexBuilt();
     if (a.k > 65536) { set_error("wmh_hash: the index kernel takes k <= 65536"); return WMH_EINVAL; }
     const wmh_layout *L = a.L;
     const uint32_t M = (uint32_t)L->M;
@@ -735,42 +730,79 @@ wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
         const uint32_t uni = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
         if ((st = launch_draw_table(table, a.k, a.S, M, L->cell_pack, uni, 1u, a.stream)) != WMH_OK) break;
 
-        IxParams p;
-        const bool csr = a.rows.kind == WMH_CSR;
-        p.x = a.rows.dense;
-        p.row_ptr = a.rows.row_ptr;
-        p.col = a.rows.col;
-        p.val = a.rows.val;
-        p.n_rows = a.rows.n_rows;
-        p.D = a.rows.dim;
-        p.comp_to_m = L->comp_to_m;
-        p.pack = L->cell_pack;
-        p.uni_m = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
-        p.M = M;
-        p.pos = pos;
-        p.vals = vals;
-        p.table = table;
-        p.ep = ep;
-        p.S = a.S;
-        p.k = a.k;
-        p.cap = a.cap;
-        p.capn = 0;
-        static const float cfs = getenv("WMH_INDEX_CF") ? (float)atof(getenv("WMH_INDEX_CF")) : 0.f;
-        p.cf_dense = cfs > 0 ? cfs : 2.f;
-        p.cf_smem = cfs > 0 ? cfs : 3.f;
-        p.cf_global = cfs > 0 ? cfs : 16.f;
-        p.sig = a.sig;
-        p.n_sat = a.n_sat;
-        p.row_ctr = ctr;
-        // warps per row: >= 2; keep <= ~128 KiB of h[] per SM at 64 resident warps
-        static const int nw_env = getenv("WMH_INDEX_NW") ? atoi(getenv("WMH_INDEX_NW")) : 0;
-        int nw = 2;
-        while (nw < 8 && (uint64_t)(64 / nw) * a.k * 4 > (128u << 10)) nw *= 2;
-        if (nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
-        if (a.sig_bytes == 1) st = csr ? ix_launch_nw<1, true>(p, nw, a.stream) : ix_launch_nw<1, false>(p, nw, a.stream);
-        else st = csr ? ix_launch_nw<2, true>(p, nw, a.stream) : ix_launch_nw<2, false>(p, nw, a.stream);
     } while (0);
-    cudaFreeAsync(scr, a.stream);
+    if (st != WMH_OK) {
+        cudaFreeAsync(scr, a.stream);
+        return st;
+    }
+    out->scr = scr;
+    out->pos = pos;
+    out->vals = vals;
+    out->table = table;
+    out->ctr = ctr;
+    out->ep = ep;
+    out->T = T;
+    return WMH_OK;
+}
+
+void index_free(IndexBuilt &ix, cudaStream_t s) {
+    if (ix.scr) cudaFreeAsync(ix.scr, s);
+    ix = IndexBuilt();
+}
+
+wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
+    const wmh_layout *L = a.L;
+    const uint32_t M = (uint32_t)L->M;
+    if (a.rows.n_rows == 0) return WMH_OK;
+    WMH_CUDA_TRY(cudaMemsetAsync(ix.ctr, 0, 8, a.stream), "index row counter");
+    wmh_status st = WMH_OK;
+    unsigned long long *ctr = ix.ctr;
+    const uint32_t *pos = ix.pos, *vals = ix.vals;
+    const uint2 *table = ix.table;
+    const IxEpochs ep = ix.ep;
+    IxParams p;
+    const bool csr = a.rows.kind == WMH_CSR;
+    p.x = a.rows.dense;
+    p.row_ptr = a.rows.row_ptr;
+    p.col = a.rows.col;
+    p.val = a.rows.val;
+    p.n_rows = a.rows.n_rows;
+    p.D = a.rows.dim;
+    p.comp_to_m = L->comp_to_m;
+    p.pack = L->cell_pack;
+    p.uni_m = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
+    p.M = M;
+    p.pos = pos;
+    p.vals = vals;
+    p.table = table;
+    p.ep = ep;
+    p.S = a.S;
+    p.k = a.k;
+    p.cap = a.cap;
+    p.capn = 0;
+    static const float cfs = getenv("WMH_INDEX_CF") ? (float)atof(getenv("WMH_INDEX_CF")) : 0.f;
+    p.cf_dense = cfs > 0 ? cfs : 2.f;
+    p.cf_smem = cfs > 0 ? cfs : 3.f;
+    p.cf_global = cfs > 0 ? cfs : 16.f;
+    p.sig = a.sig;
+    p.n_sat = a.n_sat;
+    p.row_ctr = ctr;
+    // warps per row: >= 2; keep <= ~128 KiB of h[] per SM at 64 resident warps
+    static const int nw_env = getenv("WMH_INDEX_NW") ? atoi(getenv("WMH_INDEX_NW")) : 0;
+    int nw = 2;
+    while (nw < 8 && (uint64_t)(64 / nw) * a.k * 4 > (128u << 10)) nw *= 2;
+    if (nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
+    if (a.sig_bytes == 1) st = csr ? ix_launch_nw<1, true>(p, nw, a.stream) : ix_launch_nw<1, false>(p, nw, a.stream);
+    else st = csr ? ix_launch_nw<2, true>(p, nw, a.stream) : ix_launch_nw<2, false>(p, nw, a.stream);
+    return st;
+}
+
+wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon) {
+    IndexBuilt ix;
+    wmh_status st = index_build(a, horizon, &ix);
+    if (st != WMH_OK) return st;
+    st = index_rows(a, ix);
+    index_free(ix, a.stream);
     return st;
 }
 

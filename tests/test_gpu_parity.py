@@ -229,6 +229,26 @@ def test_hash_host_e2e_equals_device(wmh):
     assert torch.equal(dev, wmh.hash_host(layout, hr, 1, 20, 65535))
 
 
+def test_hash_host_e2e_index_chunks(wmh):
+    """wmh_hash_host with CSR rows large enough for AUTO's index kernel: the index
+    is built once per call and reused by every row chunk; signatures equal the
+    device path and the oracle."""
+    cfg, c = datagen.make("c4", n_rows=300)
+    rows = to_rows(c)
+    bounds = torch.full((c.dim,), 255, dtype=torch.uint32, device="cuda")
+    layout = wmh.prepare(rows, bounds=bounds)
+    k = 4000
+    dev = wmh.hash(layout, rows, 7, k, 65535).cpu()
+    assert wmh.last_algo == "index"
+    hr = wmh.Rows.from_csr(torch.from_numpy(c.row_ptr).pin_memory(), torch.from_numpy(c.col).pin_memory(),
+                           torch.from_numpy(c.val).pin_memory(), c.dim)
+    host = wmh.hash_host(layout, hr, 7, k, 65535)
+    assert torch.equal(dev, host)
+    L = oracle.Layout(np.full(c.dim, 255, np.uint32))
+    pick = [0, 1, 150, 299]
+    _assert_sig_equal(host[pick], oracle_hash(L, c, 7, k, 65535, rows=pick), "e2e index")
+
+
 # ------------------------------------------------------------------ collide
 @pytest.mark.parametrize("sb,k", [(2, 128), (1, 64), (2, 37), (1, 5)])
 def test_collide_matches_oracle(wmh, sb, k):
