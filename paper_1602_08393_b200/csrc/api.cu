@@ -195,10 +195,13 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     // tiny batches (<= 2^20 row-hash pairs, e.g. config c1) are launch-bound:
     // the single-launch SIMPLE kernel beats the table + tiled pair there
     const bool tiny = (unsigned long long)rows->n_rows * k <= (1ull << 20);
-    // sparse rows: the index kernel visits only the green draws (measured 6-40x
-    // faster than the tiled CSR kernel on c3/c4 slices); dense rows at s ~ 0.05
-    // stay on the shared-memory tile (the index reads ~45 KB of L2 per c2 row)
-    if (algo == WMH_ALGO_AUTO && !tiny && rows->kind == WMH_CSR && k <= 65536) {
+    // The index kernel visits only the green draws (k*T*s per row); the tile
+    // tests ~k/s draws per row, 4 rows per shared load.  Measured: CSR rows
+    // (c3, c4) 35-350x faster on the index; dense rows at mean s = 0.036 (c5)
+    // 1.17x faster on the index, at s = 0.050 (c2) 1.4x faster on the tile.
+    // Dense rows go to the index below mean s = 0.042 (prepare's statistics).
+    const bool sparse_dense = rows->kind == WMH_DENSE && L->mean_s >= 0.0 && L->mean_s < 0.042;
+    if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense) && k <= 65536) {
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
     }
@@ -330,7 +333,8 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_comp, E.ev_start, 0), "e2e wait");
     // the index kernel (AUTO's choice for CSR rows) files the draws once for the
     // whole call; every chunk then only runs its rows kernel
-    const bool use_index = h.kind == WMH_CSR && k <= 65536 && (unsigned long long)h.n_rows * k > (1ull << 20);
+    const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.042)) && k <= 65536 &&
+                           (unsigned long long)h.n_rows * k > (1ull << 20);
     IndexBuilt ix;
     HashArgs ha;
     if (use_index) {

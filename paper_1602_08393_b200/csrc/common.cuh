@@ -18,6 +18,7 @@ struct wmh_layout {
     uint32_t *int_to_comp = nullptr;  // [M]         IntToComp (Alg. 4)
     uint32_t *cell_pack = nullptr;    // [M]         (c << 8) | (t - CompToM[c]): Alg. 5 in one load
     uint64_t rowsum_q = 0;            // 0.1% quantile (power of two) of prepare's nonzero row sums; 0 = unknown
+    double mean_s = -1.0;             // mean effective sparsity |x|_1 / M of prepare's rows (Eq. 17); < 0 = unknown
     int device = 0;
 };
 

@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(256) rowsum_hist(const uint8_t *__restrict__ d
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long total = 0;                 // hist[65]: sum of all row sums
     for (int64_t r = w0; r < n_rows; r += nw) {
         unsigned long long s = 0;
         if (dense) {
@@ -270,7 +271,9 @@ __global__ void __launch_bounds__(256) rowsum_hist(const uint8_t *__restrict__ d
         }
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
         if (lane == 0) atomicAdd(hist + (s ? 63 - __clzll((long long)s) : 64), 1ull);
+        total += s;
     }
+    if (lane == 0 && total) atomicAdd(hist + 65, total);
 }
 
 extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *stream) {
@@ -362,7 +365,7 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
             check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, rows->val, rows->n_rows, dim, rows->nnz,
                                               L->bounds, bad);
     }
-    unsigned long long *hist = nullptr, hhist[65] = {0};
+    unsigned long long *hist = nullptr, hhist[66] = {0};
     const bool stats = rows && rows->n_rows > 0;
     if (stats) {
         if (cudaMallocAsync((void **)&hist, sizeof hhist, s) != cudaSuccess) { cudaFreeAsync(scr, s); set_error("wmh_prepare: scratch alloc failed"); return fail(WMH_ENOMEM); }
@@ -384,7 +387,8 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     cudaFreeAsync(scr, s);
     if (hist) cudaFreeAsync(hist, s);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(cuda_fail(e1 != cudaSuccess ? e1 : e2, "prepare readback"));
-    if (stats) {             // 0.1% quantile of the nonzero row sums, as the bin's lower end 2^b
+    if (stats) {             // 0.1% quantile of the nonzero row sums, as the bin's lower end 2^b; mean s
+        L->mean_s = host[0] ? (double)hhist[65] / ((double)rows->n_rows * (double)host[0]) : -1.0;
         unsigned long long nz = 0, run = 0;
         for (int b = 0; b < 64; b++) nz += hhist[b];
         for (int b = 0; b < 64 && nz; b++) {
