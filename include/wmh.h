@@ -18,9 +18,10 @@
  *    available from wmh_last_error() (thread-local, valid until the next
  *    call on the same thread).  Arguments are validated before any launch;
  *    an invalid call launches nothing and leaves outputs untouched.
- *  - Weights are integers x in {0..255} (uint8).  The paper quantises to
- *    integer bounds m_i = ceil(max) (Sec. 3.1); real-valued inputs
- *    must be scaled and quantised by the caller (Sec. 4).
+ *  - Weights are integers: uint8 (x in {0..255}) or uint16 (x in {0..65535},
+ *    wmh_rows.weight_bytes = 2).  The paper quantises to integer bounds
+ *    m_i = ceil(max) (Sec. 3.1); real-valued inputs are scaled and
+ *    quantised to uint16 fixed point by wmh_quantize (Sec. 4).
  *  - There is no CPU fallback: without a CUDA device every compute call
  *    fails with WMH_ECUDA.
  */
@@ -64,6 +65,10 @@ typedef struct {
     const int32_t *col;
     const uint8_t *val;
     int64_t nnz;
+    int32_t weight_bytes;  /* 1 (uint8 weights; 0 also means 1) or 2: `dense` / `val`
+                              then point to uint16 weights (cast), for fixed-point
+                              real-valued data (P:137 ceil bound, Sec. 4 scaling;
+                              see wmh_quantize).  Bounds may then reach 65535. */
 } wmh_rows;
 
 /* Opaque, immutable red-green layout (Eq. 4; Alg. 4).
@@ -81,24 +86,48 @@ typedef struct wmh_layout wmh_layout;
  * Errors: EINVAL (null pointers, dim < 1, n_rows < 0, bad kind), ECUDA. */
 wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *stream);
 
+/* ---- f1: real-valued weights in fixed point (Sec. 3.1, Sec. 4)
+ * out[i] = min(65535, floor(in[i] * scale)) for n float32 weights in >= 0
+ * (the product rounded to nearest in float32, then floored), so a row of reals
+ * becomes the uint16 integer vector the integer method hashes exactly.  With
+ * scale = alpha * 2^f the bounds are the column maxima of the quantised rows
+ * (wmh_colmax), and a weight loses at most 1/scale.  Dyadic weights x = w/scale
+ * with integer w <= 65535 are exact.  in/out: device, n elements.
+ * Errors: EINVAL (null, n < 0, scale not finite or <= 0, a weight < 0 or NaN:
+ * reported after one synchronisation of `stream`), ECUDA. */
+wmh_status wmh_quantize(const float *in, int64_t n, float scale, uint16_t *out, void *stream);
+
+/* Sec. 4's choice of the scale ("alpha = arg max sum alpha x_i /
+ * sum ceil(alpha m_i)"), evaluated for fixed-point quantisation: for each
+ * candidate scale s_a the numerator sum_n sum_c floor(x * s_a) and the
+ * denominator n_rows * sum_c max_n floor(x * s_a) of the mean effective
+ * sparsity (Eq. 17) of the quantised rows.  rows_f32 uses the wmh_rows layout
+ * with FLOAT weights (dense / val point to float32, weight_bytes ignored).
+ * scales: host array of n_scales; out: host uint64[2 * n_scales] (num, den).
+ * Synchronises `stream`.  Errors: EINVAL, ENOMEM, ECUDA. */
+wmh_status wmh_scale_objective(const wmh_rows *rows_f32, const float *scales, int32_t n_scales, uint64_t *out,
+                               void *stream);
+
 /* ---- a3 + a4: prefix sums and Alg. 4 ComputeHashMaps --------------------
  * Builds CompToM[c] = sum_{i<c} m_i (Eq. 3; exclusive prefix, interval
  * c = [CompToM[c], CompToM[c+1]), reading R3) and IntToComp[t] = c for every
  * integer cell t of interval c (Alg. 4; M cells, reading R4).
  * Components with m_c = 0 get no cells (reading R11).
- *   bounds: device uint32[dim], every m_c <= 255 (weights are uint8);
+ *   bounds: device uint32[dim], every m_c <= 65535 (bounds above 255 make a
+ *           "wide" layout, hashed by the INDEX and SIMPLE kernels);
  *           copied, so the caller may free it after the call returns.
  *   rows:   optional (may be NULL).  When given, every weight is checked
  *           against its bound (and CSR structure is validated); the first
  *           offender is reported as WMH_EBOUND / WMH_EINVAL.
  * Synchronises `stream` once to read back M (8 bytes) and the checks.
- * Errors: EINVAL (null, dim < 1, a bound > 255, malformed CSR), EBOUND,
+ * Errors: EINVAL (null, dim < 1, a bound > 65535, malformed CSR), EBOUND,
  *         EEMPTY (M = 0), EOVERFLOW (M >= 2^32), ENOMEM, ECUDA. */
 wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh_rows *rows, wmh_layout **out,
                        void *stream);
 
 /* Layout facts (host values): dim, M, flags (bit 0: every m_c equal, so
- * IntToComp is the division r / m), the uniform bound (0 if not uniform). */
+ * IntToComp is the division r / m; bit 1: "wide", some m_c > 255), the
+ * uniform bound (0 if not uniform). */
 wmh_status wmh_layout_info(const wmh_layout *layout, int64_t *dim, uint64_t *M, uint32_t *flags,
                            uint32_t *uniform_bound);
 

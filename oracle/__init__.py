@@ -45,6 +45,7 @@ def lib() -> ctypes.CDLL:
             build()
             L = ctypes.CDLL(_SO)
             u8p = ctypes.POINTER(ctypes.c_uint8)
+            u16p = ctypes.POINTER(ctypes.c_uint16)
             u32p = ctypes.POINTER(ctypes.c_uint32)
             i32p = ctypes.POINTER(ctypes.c_int32)
             i64p = ctypes.POINTER(ctypes.c_int64)
@@ -69,6 +70,12 @@ def lib() -> ctypes.CDLL:
                 "oracle_collide": (None, [u32p, u32, i64p, i64, u32p]),
                 "oracle_jaccard_dense": (None, [u8p, u8p, i64, u64p, u64p]),
                 "oracle_jaccard_csr": (None, [i64p, i32p, u8p, i64, i64, u64p, u64p]),
+                "oracle_colmax_dense16": (None, [u16p, i64, i64, u32p]),
+                "oracle_colmax_csr16": (None, [i64p, i32p, u16p, i64, i64, u32p]),
+                "oracle_hash_one16": (u32, [u32p, u32p, u32, u16p, u64, u32, u32]),
+                "oracle_hash_dense16": (c_int, [u16p, i64, i64, u32p, u32p, u32, u64, u32, u32, u32p, c_int]),
+                "oracle_hash_csr16": (c_int, [i64p, i32p, u16p, i64, i64, u32p, u32p, u32, u64, u32, u32,
+                                              u32p, c_int]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -84,7 +91,14 @@ def _p(a: np.ndarray, ct):
 
 
 def _u8(a):
+    a = np.asarray(a)
+    if a.dtype == np.uint16:
+        raise TypeError("uint16 weights go through the *16 oracle functions")
     return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+def _is16(a) -> bool:
+    return np.asarray(a).dtype == np.uint16
 
 
 def _u32(a):
@@ -103,6 +117,11 @@ def draw(seed: int, j: int, t: int, M: int) -> int:
 
 # ----------------------------------------------------------------- preprocessing
 def colmax_dense(x: np.ndarray) -> np.ndarray:
+    if _is16(x):
+        x = np.ascontiguousarray(x)
+        m = np.zeros(x.shape[1], np.uint32)
+        lib().oracle_colmax_dense16(_p(x, ctypes.c_uint16), x.shape[0], x.shape[1], _p(m, ctypes.c_uint32))
+        return m
     x = _u8(x)
     n, d = x.shape
     m = np.zeros(d, np.uint32)
@@ -113,8 +132,13 @@ def colmax_dense(x: np.ndarray) -> np.ndarray:
 def colmax_csr(row_ptr, col, val, dim) -> np.ndarray:
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col = np.ascontiguousarray(col, np.int32)
-    val = _u8(val)
     m = np.zeros(dim, np.uint32)
+    if _is16(val):
+        val = np.ascontiguousarray(val)
+        lib().oracle_colmax_csr16(_p(row_ptr, ctypes.c_int64), _p(col, ctypes.c_int32), _p(val, ctypes.c_uint16),
+                                  len(row_ptr) - 1, dim, _p(m, ctypes.c_uint32))
+        return m
+    val = _u8(val)
     lib().oracle_colmax_csr(_p(row_ptr, ctypes.c_int64), _p(col, ctypes.c_int32), _p(val, ctypes.c_uint8),
                             len(row_ptr) - 1, dim, _p(m, ctypes.c_uint32))
     return m
@@ -179,6 +203,20 @@ class Layout:
         return int(lib().oracle_hash_one(i2c, c2m, self.M, _p(x, ctypes.c_uint8), seed & (2**64 - 1), j, cap))
 
     def hash_dense(self, x, seed: int, k: int, cap: int, threads: int | None = None) -> np.ndarray:
+        """uint8 weights, or uint16 (f1: fixed-point real data) through the *16 functions."""
+        if _is16(x):
+            x = np.ascontiguousarray(x)
+            if x.ndim == 1:
+                x = x[None, :]
+            assert x.shape[1] == self.dim
+            sig = np.zeros((x.shape[0], k), np.uint32)
+            i2c, c2m = self._t()
+            rc = lib().oracle_hash_dense16(_p(x, ctypes.c_uint16), x.shape[0], self.dim, i2c, c2m, self.M,
+                                           seed & (2**64 - 1), k, cap, _p(sig, ctypes.c_uint32),
+                                           threads or os.cpu_count() or 1)
+            if rc != OK:
+                raise ValueError(f"oracle_hash_dense16 failed: {rc}")
+            return sig
         x = _u8(x)
         if x.ndim == 1:
             x = x[None, :]
@@ -195,10 +233,19 @@ class Layout:
     def hash_csr(self, row_ptr, col, val, seed: int, k: int, cap: int, threads: int | None = None) -> np.ndarray:
         row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         col = np.ascontiguousarray(col, np.int32)
-        val = _u8(val)
         n = len(row_ptr) - 1
         sig = np.zeros((n, k), np.uint32)
         i2c, c2m = self._t()
+        if _is16(val):
+            val = np.ascontiguousarray(val)
+            rc = lib().oracle_hash_csr16(_p(row_ptr, ctypes.c_int64), _p(col, ctypes.c_int32),
+                                         _p(val, ctypes.c_uint16), n, self.dim, i2c, c2m, self.M,
+                                         seed & (2**64 - 1), k, cap, _p(sig, ctypes.c_uint32),
+                                         threads or os.cpu_count() or 1)
+            if rc != OK:
+                raise ValueError(f"oracle_hash_csr16 failed: {rc}")
+            return sig
+        val = _u8(val)
         rc = lib().oracle_hash_csr(_p(row_ptr, ctypes.c_int64), _p(col, ctypes.c_int32), _p(val, ctypes.c_uint8),
                                    n, self.dim, i2c, c2m, self.M, seed & (2**64 - 1), k, cap,
                                    _p(sig, ctypes.c_uint32), threads or os.cpu_count() or 1)
@@ -234,3 +281,40 @@ def jaccard_csr(row_ptr, col, val, a: int, b: int) -> Fraction | None:
     lib().oracle_jaccard_csr(_p(row_ptr, ctypes.c_int64), _p(col, ctypes.c_int32), _p(val, ctypes.c_uint8),
                              a, b, ctypes.byref(num), ctypes.byref(den))
     return None if den.value == 0 else Fraction(num.value, den.value)
+
+
+# ----------------------------------------------- f1: real-valued weights (Sec. 4)
+def quantize(x, scale: float) -> np.ndarray:
+    """w = min(65535, floor(x * scale)) with the product rounded to nearest in
+    float32 (IEEE, numpy) -- the fixed-point reading of P:137's ceil bound and
+    Sec. 4's scaling (R18).  x >= 0."""
+    x = np.asarray(x, np.float32)
+    if np.any(~(x >= 0)):
+        raise ValueError("weights must be >= 0")
+    q = np.floor(x * np.float32(scale))
+    return np.minimum(q, 65535).astype(np.uint16)
+
+
+def scale_objective(x_rows, scales):
+    """Sec. 4 for fixed point: per scale s, (sum_n sum_c floor(x s),
+    n_rows * sum_c max_n floor(x s)) -- the numerator and denominator of the mean
+    effective sparsity (Eq. 17) of the quantised rows.  x_rows: dense float32
+    (n_rows, D)."""
+    x = np.asarray(x_rows, np.float32)
+    out = []
+    for s in scales:
+        q = quantize(x, s).astype(np.int64)
+        out.append((int(q.sum()), int(x.shape[0]) * int(q.max(axis=0).sum())))
+    return out
+
+
+def choose_scale(x_rows, scales) -> float:
+    """argmax of the mean effective sparsity; ties go to the smaller scale (SPEC
+    optimize_alpha, S:237-245)."""
+    best = None
+    for s, (num, den) in sorted(zip(scales, scale_objective(x_rows, scales)), key=lambda t: t[0]):
+        if den == 0:
+            continue
+        if best is None or Fraction(num, den) > best[1]:
+            best = (s, Fraction(num, den))
+    return None if best is None else float(best[0])

@@ -350,3 +350,141 @@ void oracle_jaccard_csr(const int64_t *row_ptr, const int32_t *col, const uint8_
     *num = mn;
     *den = mx;
 }
+
+/* ------------------------------------------------------------------------ */
+/* f1: uint16 weights (fixed-point real data, Sec. 3.1 P:137 and Sec. 4      */
+/* P:322-324).  The same definitions as above with x_c in {0..65535} and    */
+/* bounds m_c <= 65535; written out again (not shared with the uint8 code)   */
+/* so that each can be read against the paper on its own.                    */
+/* ------------------------------------------------------------------------ */
+
+void oracle_colmax_dense16(const uint16_t *x, int64_t n_rows, int64_t dim, uint32_t *m_out)
+{
+    for (int64_t c = 0; c < dim; c++) m_out[c] = 0;
+    for (int64_t n = 0; n < n_rows; n++)
+        for (int64_t c = 0; c < dim; c++)
+            if (x[n * dim + c] > m_out[c]) m_out[c] = x[n * dim + c];
+}
+
+void oracle_colmax_csr16(const int64_t *row_ptr, const int32_t *col, const uint16_t *val,
+                         int64_t n_rows, int64_t dim, uint32_t *m_out)
+{
+    for (int64_t c = 0; c < dim; c++) m_out[c] = 0;
+    for (int64_t n = 0; n < n_rows; n++)
+        for (int64_t e = row_ptr[n]; e < row_ptr[n + 1]; e++)
+            if (val[e] > m_out[col[e]]) m_out[col[e]] = val[e];
+}
+
+/* Alg. 5 with a uint16 weight: green iff r - CompToM[i] < x_i. */
+static int oracle_is_green_o1_16(const uint32_t *int_to_comp, const uint32_t *comp_to_m,
+                                 const uint16_t *x_dense, uint32_t r)
+{
+    uint32_t i = int_to_comp[r];
+    return (r - comp_to_m[i]) < (uint32_t)x_dense[i];
+}
+
+/* Alg. 3 for one (vector, hash j) with uint16 weights. */
+uint32_t oracle_hash_one16(const uint32_t *int_to_comp, const uint32_t *comp_to_m, uint32_t M,
+                           const uint16_t *x_dense, uint64_t seed, uint32_t j, uint32_t cap)
+{
+    for (uint32_t t = 0; t < cap; t++) {
+        uint32_t r = oracle_draw(seed, j, t, M);
+        if (oracle_is_green_o1_16(int_to_comp, comp_to_m, x_dense, r)) return t + 1;
+    }
+    return cap;
+}
+
+typedef struct {
+    int kind;
+    const uint16_t *x;
+    const int64_t *row_ptr;
+    const int32_t *col;
+    const uint16_t *val;
+    int64_t n_rows, dim;
+    const uint32_t *int_to_comp, *comp_to_m;
+    uint32_t M;
+    uint64_t seed;
+    uint32_t k, cap;
+    uint32_t *sig;
+    int64_t row_begin, row_end;
+    int status;
+} oracle_job16;
+
+static void *oracle_hash_worker16(void *arg)
+{
+    oracle_job16 *jb = (oracle_job16 *)arg;
+    uint16_t *scratch = NULL;
+    if (jb->kind == 1) {
+        scratch = (uint16_t *)calloc((size_t)jb->dim, sizeof(uint16_t));
+        if (!scratch) { jb->status = ORC_ENOMEM; return NULL; }
+    }
+    for (int64_t n = jb->row_begin; n < jb->row_end; n++) {
+        const uint16_t *xrow;
+        if (jb->kind == 0) {
+            xrow = jb->x + n * jb->dim;
+        } else {
+            for (int64_t e = jb->row_ptr[n]; e < jb->row_ptr[n + 1]; e++) scratch[jb->col[e]] = jb->val[e];
+            xrow = scratch;
+        }
+        for (uint32_t j = 0; j < jb->k; j++)
+            jb->sig[n * (int64_t)jb->k + j] =
+                oracle_hash_one16(jb->int_to_comp, jb->comp_to_m, jb->M, xrow, jb->seed, j, jb->cap);
+        if (jb->kind == 1)
+            for (int64_t e = jb->row_ptr[n]; e < jb->row_ptr[n + 1]; e++) scratch[jb->col[e]] = 0;
+    }
+    free(scratch);
+    jb->status = ORC_OK;
+    return NULL;
+}
+
+static int oracle_hash_rows16(oracle_job16 proto, int n_threads)
+{
+    if (proto.k == 0 || proto.cap == 0) return ORC_EINVAL;
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > proto.n_rows && proto.n_rows > 0) n_threads = (int)proto.n_rows;
+    if (proto.n_rows == 0) return ORC_OK;
+    oracle_job16 *jobs = (oracle_job16 *)calloc((size_t)n_threads, sizeof(oracle_job16));
+    pthread_t *th = (pthread_t *)calloc((size_t)n_threads, sizeof(pthread_t));
+    if (!jobs || !th) { free(jobs); free(th); return ORC_ENOMEM; }
+    int64_t per = (proto.n_rows + n_threads - 1) / n_threads;
+    for (int i = 0; i < n_threads; i++) {
+        jobs[i] = proto;
+        jobs[i].row_begin = i * per;
+        jobs[i].row_end = (i + 1) * per < proto.n_rows ? (i + 1) * per : proto.n_rows;
+        if (jobs[i].row_begin > jobs[i].row_end) jobs[i].row_begin = jobs[i].row_end;
+        pthread_create(&th[i], NULL, oracle_hash_worker16, &jobs[i]);
+    }
+    int rc = ORC_OK;
+    for (int i = 0; i < n_threads; i++) {
+        pthread_join(th[i], NULL);
+        if (jobs[i].status != ORC_OK) rc = jobs[i].status;
+    }
+    free(jobs);
+    free(th);
+    return rc;
+}
+
+int oracle_hash_dense16(const uint16_t *x, int64_t n_rows, int64_t dim,
+                        const uint32_t *int_to_comp, const uint32_t *comp_to_m, uint32_t M,
+                        uint64_t seed, uint32_t k, uint32_t cap, uint32_t *sig, int n_threads)
+{
+    oracle_job16 p;
+    memset(&p, 0, sizeof p);
+    p.kind = 0; p.x = x; p.n_rows = n_rows; p.dim = dim;
+    p.int_to_comp = int_to_comp; p.comp_to_m = comp_to_m; p.M = M;
+    p.seed = seed; p.k = k; p.cap = cap; p.sig = sig;
+    return oracle_hash_rows16(p, n_threads);
+}
+
+int oracle_hash_csr16(const int64_t *row_ptr, const int32_t *col, const uint16_t *val,
+                      int64_t n_rows, int64_t dim,
+                      const uint32_t *int_to_comp, const uint32_t *comp_to_m, uint32_t M,
+                      uint64_t seed, uint32_t k, uint32_t cap, uint32_t *sig, int n_threads)
+{
+    oracle_job16 p;
+    memset(&p, 0, sizeof p);
+    p.kind = 1; p.row_ptr = row_ptr; p.col = col; p.val = val; p.n_rows = n_rows; p.dim = dim;
+    p.int_to_comp = int_to_comp; p.comp_to_m = comp_to_m; p.M = M;
+    p.seed = seed; p.k = k; p.cap = cap; p.sig = sig;
+    return oracle_hash_rows16(p, n_threads);
+}

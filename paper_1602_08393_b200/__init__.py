@@ -23,7 +23,7 @@ from . import _lib
 from ._lib import WmhError  # noqa: F401
 
 __all__ = ["Rows", "Layout", "colmax", "reduce_bounds", "shard", "prepare", "hash", "hash_host", "collide", "WmhError",
-           "version"]
+           "version", "quantize", "scale_objective", "choose_scale"]
 
 
 def _stream(stream=None) -> int:
@@ -43,9 +43,14 @@ def _need_cuda(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be contiguous")
 
 
+_WEIGHT_BYTES = {torch.uint8: 1, torch.uint16: 2, torch.float32: 4}
+
+
 @dataclass
 class Rows:
-    """A batch of vectors x >= 0 with uint8 weights, dense or CSR."""
+    """A batch of vectors x >= 0, dense or CSR, with uint8 or uint16 integer
+    weights (uint16: fixed-point real data, see quantize), or float32 weights for
+    scale_objective only."""
     kind: int
     n_rows: int
     dim: int
@@ -54,19 +59,20 @@ class Rows:
     col: torch.Tensor | None = None
     val: torch.Tensor | None = None
     nnz: int = 0
+    weight_bytes: int = 1
 
     @staticmethod
     def from_dense(x: torch.Tensor) -> "Rows":
-        if x.dtype != torch.uint8 or x.dim() != 2:
-            raise ValueError("dense rows must be a 2-D uint8 tensor")
-        return Rows(_lib.WMH_DENSE, x.shape[0], x.shape[1], dense=x)
+        if x.dtype not in _WEIGHT_BYTES or x.dim() != 2:
+            raise ValueError("dense rows must be a 2-D uint8 / uint16 (or float32 for scale_objective) tensor")
+        return Rows(_lib.WMH_DENSE, x.shape[0], x.shape[1], dense=x, weight_bytes=_WEIGHT_BYTES[x.dtype])
 
     @staticmethod
     def from_csr(row_ptr: torch.Tensor, col: torch.Tensor, val: torch.Tensor, dim: int) -> "Rows":
-        if row_ptr.dtype != torch.int64 or col.dtype != torch.int32 or val.dtype != torch.uint8:
-            raise ValueError("CSR rows need row_ptr int64, col int32, val uint8")
+        if row_ptr.dtype != torch.int64 or col.dtype != torch.int32 or val.dtype not in _WEIGHT_BYTES:
+            raise ValueError("CSR rows need row_ptr int64, col int32, val uint8 / uint16 (or float32)")
         return Rows(_lib.WMH_CSR, row_ptr.numel() - 1, int(dim), row_ptr=row_ptr, col=col, val=val,
-                    nnz=col.numel())
+                    nnz=col.numel(), weight_bytes=_WEIGHT_BYTES[val.dtype])
 
     def _c(self, device: bool = True) -> _lib.WmhRows:
         for name in ("dense", "row_ptr", "col", "val"):
@@ -77,7 +83,8 @@ class Rows:
                             None if self.dense is None else self.dense.data_ptr(),
                             None if self.row_ptr is None else self.row_ptr.data_ptr(),
                             None if self.col is None else self.col.data_ptr(),
-                            None if self.val is None else self.val.data_ptr(), self.nnz)
+                            None if self.val is None else self.val.data_ptr(), self.nnz,
+                            self.weight_bytes if self.weight_bytes in (1, 2) else 1)
 
     def slice(self, begin: int, end: int) -> "Rows":
         """Rows [begin, end) as a view (dense) or a re-based copy of row_ptr (CSR)."""
@@ -135,6 +142,7 @@ class Layout:
 
 def colmax(rows: Rows, stream=None) -> torch.Tensor:
     """a1: per-column maxima of `rows` (uint32 [D] on the rows' device)."""
+    _no_float(rows, "colmax")
     dev = (rows.dense if rows.dense is not None else rows.col).device
     out = torch.empty(rows.dim, dtype=torch.uint32, device=dev)
     _lib.check(_lib.load().wmh_colmax(ctypes.byref(rows._c()), _ptr(out), _stream(stream)))
@@ -202,6 +210,7 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
         out = torch.empty((rows.n_rows, k), dtype=dtype, device=dev)
     elif out.dtype != dtype or out.numel() != rows.n_rows * k:
         raise ValueError("out has the wrong dtype or size")
+    _no_float(rows, "hash")
     if n_saturated is not None and (n_saturated.dtype not in (torch.int64, torch.uint64) or not n_saturated.is_cuda):
         raise ValueError("n_saturated must be a CUDA int64 tensor")
     opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon, _lib.WMH_OPT_TIME_KERNEL if time_kernel else 0)
@@ -227,6 +236,49 @@ def hash_host(layout: Layout, rows_host, seed: int, k: int, cap: int, sig_bytes:
     _lib.check(_lib.load().wmh_hash_host(layout.handle, ctypes.byref(c), seed & (2**64 - 1), k, cap, sig_bytes,
                                          ctypes.c_void_p(out.data_ptr()), _stream(stream)))
     return out
+
+
+def _no_float(rows: Rows, what: str):
+    if rows.weight_bytes == 4:
+        raise ValueError(f"{what} takes integer weights; quantize float32 rows first")
+
+
+def quantize(x: torch.Tensor, scale: float, stream=None) -> torch.Tensor:
+    """f1: uint16 fixed-point weights floor(x * scale) (float32 product, then floor;
+    clamped at 65535) of a float32 CUDA tensor of weights >= 0 (Sec. 3.1 / Sec. 4)."""
+    _need_cuda(x, "x")
+    if x.dtype != torch.float32:
+        raise ValueError("quantize takes float32 weights")
+    out = torch.empty(x.shape, dtype=torch.uint16, device=x.device)
+    _lib.check(_lib.load().wmh_quantize(_ptr(x), x.numel(), float(scale), _ptr(out), _stream(stream)))
+    return out
+
+
+def scale_objective(rows: Rows, scales, stream=None) -> list[tuple[int, int]]:
+    """Sec. 4: for each candidate scale, (numerator, denominator) of the mean
+    effective sparsity of the rows quantised at that scale: sum floor(x*s) and
+    n_rows * sum_c max_n floor(x*s).  `rows` holds float32 weights."""
+    if rows.weight_bytes != 4:
+        raise ValueError("scale_objective takes float32 rows")
+    sc = (ctypes.c_float * len(scales))(*[float(v) for v in scales])
+    out = (ctypes.c_uint64 * (2 * len(scales)))()
+    _lib.check(_lib.load().wmh_scale_objective(ctypes.byref(rows._c()), sc, len(scales), out, _stream(stream)))
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(len(scales))]
+
+
+def choose_scale(rows: Rows, scales, stream=None) -> float:
+    """The candidate with the largest mean effective sparsity (ties: the smaller scale,
+    i.e. the smaller M); Sec. 4's alpha = argmax sum alpha x / sum ceil(alpha m)."""
+    obj = scale_objective(rows, scales, stream)
+    best = None
+    for s, (num, den) in sorted(zip(scales, obj), key=lambda t: t[0]):
+        if den == 0:
+            continue
+        if best is None or num * best[2] > best[1] * den:
+            best = (s, num, den)
+    if best is None:
+        raise ValueError("every candidate scale quantises the rows to zero")
+    return float(best[0])
 
 
 def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, stream=None):

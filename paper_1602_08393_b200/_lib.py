@@ -18,13 +18,13 @@ STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 
 # Every symbol include/wmh.h declares (tests check the .so exports all of them).
 EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_tables", "wmh_layout_free",
            "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version",
-           "wmh_kernel_launches", "wmh_last_kernel_ms"]
+           "wmh_kernel_launches", "wmh_last_kernel_ms", "wmh_quantize", "wmh_scale_objective"]
 
 
 class WmhRows(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("n_rows", ctypes.c_int64), ("dim", ctypes.c_int64),
                 ("dense", ctypes.c_void_p), ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
-                ("val", ctypes.c_void_p), ("nnz", ctypes.c_int64)]
+                ("val", ctypes.c_void_p), ("nnz", ctypes.c_int64), ("weight_bytes", ctypes.c_int32)]
 
 
 class WmhHashOpts(ctypes.Structure):
@@ -70,6 +70,8 @@ def load() -> ctypes.CDLL:
             "wmh_version": (ctypes.c_char_p, []),
             "wmh_kernel_launches": (ctypes.c_uint64, []),
             "wmh_last_kernel_ms": (st, [ctypes.POINTER(ctypes.c_float)]),
+            "wmh_quantize": (st, [vp, i64, ctypes.c_float, vp, vp]),
+            "wmh_scale_objective": (st, [rows_p, ctypes.POINTER(ctypes.c_float), i32, ctypes.POINTER(u64), vp]),
         }
         for name, (res, args) in proto.items():
             f = getattr(L, name)

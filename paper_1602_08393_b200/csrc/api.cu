@@ -85,6 +85,7 @@ wmh_status check_rows(const wmh_rows *rows, bool need_data) {
     if (!rows) { set_error("rows is NULL"); return WMH_EINVAL; }
     if (rows->n_rows < 0) { set_error("n_rows=%lld < 0", (long long)rows->n_rows); return WMH_EINVAL; }
     if (rows->dim < 1) { set_error("dim=%lld < 1", (long long)rows->dim); return WMH_EINVAL; }
+    if (rows->weight_bytes < 0 || rows->weight_bytes > 2) { set_error("weight_bytes=%d not in {1, 2}", (int)rows->weight_bytes); return WMH_EINVAL; }
     if (rows->kind == WMH_DENSE) {
         if (need_data && rows->n_rows > 0 && !rows->dense) { set_error("dense rows pointer is NULL"); return WMH_EINVAL; }
     } else if (rows->kind == WMH_CSR) {
@@ -201,7 +202,9 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     // 1.17x faster on the index, at s = 0.050 (c2) 1.4x faster on the tile.
     // Dense rows go to the index below mean s = 0.042 (prepare's statistics).
     const bool sparse_dense = rows->kind == WMH_DENSE && L->mean_s >= 0.0 && L->mean_s < 0.042;
-    if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense) && k <= 65536) {
+    // uint16 weights / bounds above 255 (fixed-point real data): index or simple
+    const bool wide = (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(*rows) != 1;
+    if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense || wide) && k <= 65536) {
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
     }
@@ -333,7 +336,8 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_comp, E.ev_start, 0), "e2e wait");
     // the index kernel (AUTO's choice for CSR rows) files the draws once for the
     // whole call; every chunk then only runs its rows kernel
-    const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.042)) && k <= 65536 &&
+    const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.042) ||
+                            (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && k <= 65536 &&
                            (unsigned long long)h.n_rows * k > (1ull << 20);
     IndexBuilt ix;
     HashArgs ha;
@@ -356,14 +360,15 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
         const int64_t a = ci * cr, b = std::min<int64_t>(h.n_rows, a + cr), nr = b - a;
         size_t in_bytes, off_col = 0, off_val = 0;
         int64_t e0 = 0, e1 = 0;
+        const size_t wb = (size_t)weight_bytes(h);
         if (h.kind == WMH_DENSE) {
-            in_bytes = align256((size_t)nr * h.dim);
+            in_bytes = align256((size_t)nr * h.dim * wb);
         } else {
             e0 = h.row_ptr[a];
             e1 = h.row_ptr[b];
             off_col = align256(sizeof(int64_t) * (nr + 1));
             off_val = off_col + align256(sizeof(int32_t) * (e1 - e0));
-            in_bytes = off_val + align256((size_t)(e1 - e0));
+            in_bytes = off_val + align256((size_t)(e1 - e0) * wb);
         }
         // the slot's previous chunk must have finished its D2H before reuse
         WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_in, E.ev_out[slot], 0), "e2e wait");
@@ -372,13 +377,13 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
         wmh_rows d = h;
         d.n_rows = nr;
         if (h.kind == WMH_DENSE) {
-            WMH_CUDA_TRY(cudaMemcpyAsync(base, h.dense + a * h.dim, (size_t)nr * h.dim, cudaMemcpyHostToDevice, E.s_in), "e2e H2D rows");
+            WMH_CUDA_TRY(cudaMemcpyAsync(base, h.dense + a * h.dim * wb, (size_t)nr * h.dim * wb, cudaMemcpyHostToDevice, E.s_in), "e2e H2D rows");
             d.dense = base;
         } else {
             WMH_CUDA_TRY(cudaMemcpyAsync(base, h.row_ptr + a, sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, E.s_in), "e2e H2D row_ptr");
             if (e1 > e0) {
                 WMH_CUDA_TRY(cudaMemcpyAsync(base + off_col, h.col + e0, sizeof(int32_t) * (e1 - e0), cudaMemcpyHostToDevice, E.s_in), "e2e H2D col");
-                WMH_CUDA_TRY(cudaMemcpyAsync(base + off_val, h.val + e0, (size_t)(e1 - e0), cudaMemcpyHostToDevice, E.s_in), "e2e H2D val");
+                WMH_CUDA_TRY(cudaMemcpyAsync(base + off_val, h.val + e0 * wb, (size_t)(e1 - e0) * wb, cudaMemcpyHostToDevice, E.s_in), "e2e H2D val");
             }
             rebase_row_ptr<<<std::max<int64_t>(1, std::min<int64_t>(64, (nr + 256) / 256)), 256, 0, E.s_in>>>((int64_t *)base, nr + 1, e0);
             WMH_LAUNCH_CHECK("e2e rebase");

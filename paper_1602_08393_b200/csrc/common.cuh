@@ -16,13 +16,14 @@ struct wmh_layout {
     uint32_t *bounds = nullptr;       // [dim]
     uint32_t *comp_to_m = nullptr;    // [dim + 1]   CompToM, exclusive prefix (Eq. 3)
     uint32_t *int_to_comp = nullptr;  // [M]         IntToComp (Alg. 4)
-    uint32_t *cell_pack = nullptr;    // [M]         (c << 8) | (t - CompToM[c]): Alg. 5 in one load
+    uint32_t *cell_pack = nullptr;    // [M]         (c << 8) | (t - CompToM[c]): Alg. 5 in one load (not wide)
     uint64_t rowsum_q = 0;            // 0.1% quantile (power of two) of prepare's nonzero row sums; 0 = unknown
     double mean_s = -1.0;             // mean effective sparsity |x|_1 / M of prepare's rows (Eq. 17); < 0 = unknown
     int device = 0;
 };
 
 #define WMH_LAYOUT_UNIFORM 1u
+#define WMH_LAYOUT_WIDE 2u          // some bound > 255: no cell_pack, uint16 offsets
 
 namespace wmh {
 
@@ -93,6 +94,23 @@ __device__ __forceinline__ uint32_t cell_of(uint32_t r, const uint32_t *__restri
 
 __device__ __forceinline__ uint2 unpack_cell(uint32_t cell) { return make_uint2(cell >> 8, cell & 0xFFu); }
 
+// (c, r - CompToM[c]) of cell r for any layout: the division (uniform bounds),
+// the packed table (bounds <= 255), else Alg. 5's two lookups IntToComp[r],
+// CompToM[c] (wide layouts).
+__device__ __forceinline__ uint2 cell_lookup(uint32_t r, const uint32_t *__restrict__ pack, uint32_t uni_m,
+                                             const uint32_t *__restrict__ i2c, const uint32_t *__restrict__ c2m) {
+    if (uni_m) {
+        const uint32_t c = r / uni_m;
+        return make_uint2(c, r - c * uni_m);
+    }
+    if (pack) return unpack_cell(__ldg(pack + r));
+    const uint32_t c = __ldg(i2c + r);
+    return make_uint2(c, r - __ldg(c2m + c));
+}
+
+// weight width of a batch (wmh_rows.weight_bytes: 0 or 1 -> 1)
+inline int weight_bytes(const wmh_rows &r) { return r.weight_bytes == 2 ? 2 : 1; }
+
 // ------------------------------------------------------------ launchers
 struct HashArgs {
     const wmh_layout *L;
@@ -132,6 +150,6 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix);
 void index_free(IndexBuilt &ix, cudaStream_t s);
 uint32_t index_horizon(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t hint);
 wmh_status launch_draw_table(uint2 *table, uint32_t k, uint64_t S, uint32_t M, const uint32_t *pack, uint32_t uni_m,
-                             uint32_t cmul, cudaStream_t s);
+                             uint32_t cmul, cudaStream_t s, const uint32_t *i2c = nullptr, const uint32_t *c2m = nullptr);
 
 }  // namespace wmh

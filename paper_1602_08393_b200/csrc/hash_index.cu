@@ -236,12 +236,12 @@ static wmh_status scan_inplace(uint32_t *a, int64_t n, uint32_t *sums, cudaStrea
 
 // ------------------------------------------------------------- the rows
 struct IxParams {
-    const uint8_t *x;            // dense rows (n_rows x D) or null
+    const void *x;               // dense rows (n_rows x D, uint8 or uint16 weights) or null
     const int64_t *row_ptr;      // CSR
     const int32_t *col;
-    const uint8_t *val;
+    const void *val;             // CSR weights (uint8 or uint16)
     int64_t n_rows, D;
-    const uint32_t *comp_to_m, *pack;
+    const uint32_t *comp_to_m, *pack, *i2c;   // pack = null for wide layouts
     uint32_t uni_m, M;
     const uint32_t *pos, *vals;
     const uint2 *table;          // (c, r - CompToM[c]) of draws t < T0 of every hash
@@ -257,10 +257,11 @@ struct IxParams {
 
 // x_c of the current row: dense byte, or a lower_bound over the CSR slice
 // (its columns staged in shared memory when the row is short enough).
-template <bool CSR>
-__device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const uint8_t *xrow, const uint32_t *scol,
+template <bool CSR, typename W>
+__device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const W *xrow, const uint32_t *scol,
                                              int64_t e0, int n, uint32_t c) {
-    if (!CSR) return scol ? reinterpret_cast<const uint8_t *>(scol)[c] : __ldg(xrow + c);
+    const W *val = reinterpret_cast<const W *>(p.val);
+    if (!CSR) return scol ? (uint32_t)reinterpret_cast<const W *>(scol)[c] : (uint32_t)__ldg(xrow + c);
     int lo = 0, hi = n;
     if (scol) {
         while (lo < hi) {
@@ -268,14 +269,14 @@ __device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const uint8_t *x
             if (scol[mid] < c) lo = mid + 1;
             else hi = mid;
         }
-        return (lo < n && scol[lo] == c) ? (uint32_t)__ldg(p.val + e0 + lo) : 0u;
+        return (lo < n && scol[lo] == c) ? (uint32_t)__ldg(val + e0 + lo) : 0u;
     }
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if ((uint32_t)__ldg(p.col + e0 + mid) < c) lo = mid + 1;
         else hi = mid;
     }
-    return (lo < n && (uint32_t)__ldg(p.col + e0 + lo) == c) ? (uint32_t)__ldg(p.val + e0 + lo) : 0u;
+    return (lo < n && (uint32_t)__ldg(p.col + e0 + lo) == c) ? (uint32_t)__ldg(val + e0 + lo) : 0u;
 }
 
 template <int NW>
@@ -341,8 +342,9 @@ __device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long lo
 // flat index base + f, its range found from the boundaries that fall inside
 // the window (one shared load, one OR-reduction, one popc) -- and fold each
 // (j, t) into h[j] = min(h[j], t) with a shared-memory atomic.
-template <int SIGB, bool CSR, int NW>
+template <int SIGB, bool CSR, int NW, typename W>
 __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
+    const W *pval = reinterpret_cast<const W *>(p.val);
     constexpr int NT = NW * 32, ITEMS = 8, CAPR = NT * ITEMS;
     extern __shared__ uint32_t smem[];
     uint32_t *h = smem;                          // [k] first green t per hash
@@ -362,27 +364,28 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
         if (row >= p.n_rows) break;
         int64_t e0 = 0;
         int n;
-        const uint8_t *xrow = nullptr;
+        const W *xrow = nullptr;
         if (CSR) {
             e0 = p.row_ptr[row];
             n = (int)(p.row_ptr[row + 1] - e0);
         } else {
-            xrow = p.x + row * p.D;
+            xrow = reinterpret_cast<const W *>(p.x) + row * p.D;
             n = (int)p.D;
         }
-        const bool staged = CSR ? n <= p.capn : (p.D & 3) == 0 && (n >> 2) <= p.capn;
+        constexpr int PER_WORD = 4 / sizeof(W);          // weights per 32-bit word
+        const bool staged = CSR ? n <= p.capn : (p.D % PER_WORD) == 0 && (n / PER_WORD) <= p.capn;
         // ---- |x|_1 (and the columns of a short CSR row into shared memory)
         unsigned long long xs = 0;
         if (CSR) {
             for (int i = threadIdx.x; i < n; i += NT) {
-                xs += __ldg(p.val + e0 + i);
+                xs += __ldg(pval + e0 + i);
                 if (staged) scol_buf[i] = (uint32_t)__ldg(p.col + e0 + i);
             }
-        } else if ((p.D & 3) == 0) {
+        } else if ((p.D % PER_WORD) == 0) {
             const uint32_t *x4 = reinterpret_cast<const uint32_t *>(xrow);
-            for (int i = threadIdx.x; i < n / 4; i += NT) {
+            for (int i = threadIdx.x; i < n / PER_WORD; i += NT) {
                 const uint32_t w = __ldg(x4 + i);
-                xs += __dp4a(w, 0x01010101u, 0u);
+                xs += sizeof(W) == 1 ? __dp4a(w, 0x01010101u, 0u) : (w & 0xFFFFu) + (w >> 16);
                 if (staged) scol_buf[i] = w;             // the dense row, for the fallback lookups
             }
         } else {
@@ -400,14 +403,19 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
                 // ---- (1) ranges of this thread's 8 coordinates
                 const int i0 = b0 + threadIdx.x * ITEMS;
                 uint32_t xv[ITEMS], lo[ITEMS];
-                if (!CSR && ((p.D & 7) == 0) && i0 + ITEMS <= n) {
+                if (!CSR && sizeof(W) == 1 && ((p.D & 7) == 0) && i0 + ITEMS <= n) {
                     const uint2 w = __ldg(reinterpret_cast<const uint2 *>(xrow + i0));
 #pragma unroll
                     for (int q = 0; q < ITEMS; q++) xv[q] = ((q < 4 ? w.x : w.y) >> (8 * (q & 3))) & 0xFFu;
+                } else if (!CSR && sizeof(W) == 2 && ((p.D & 7) == 0) && i0 + ITEMS <= n) {
+                    const uint4 w = __ldg(reinterpret_cast<const uint4 *>(xrow + i0));
+                    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++) xv[q] = (ww[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
                 } else {
 #pragma unroll
                     for (int q = 0; q < ITEMS; q++)
-                        xv[q] = i0 + q < n ? (CSR ? (uint32_t)__ldg(p.val + e0 + i0 + q) : (uint32_t)__ldg(xrow + i0 + q)) : 0u;
+                        xv[q] = i0 + q < n ? (CSR ? (uint32_t)__ldg(pval + e0 + i0 + q) : (uint32_t)__ldg(xrow + i0 + q)) : 0u;
                 }
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++) {
@@ -525,17 +533,17 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
                                         c[q] = d.x;
                                         off[q] = d.y;
                                     } else if (t < p.cap) {
-                                        const uint32_t cell = cell_of(
+                                        const uint2 cell = cell_lookup(
                                             mulhi_range(splitmix64(p.S ^ ((uint64_t)jq[q] << 32) ^ (uint64_t)t), p.M),
-                                            p.pack, p.uni_m);
-                                        c[q] = cell >> 8;
-                                        off[q] = cell & 0xFFu;
+                                            p.pack, p.uni_m, p.i2c, p.comp_to_m);
+                                        c[q] = cell.x;
+                                        off[q] = cell.y;
                                     }
                                 }
                             }
 #pragma unroll
                             for (int q = 0; q < IX_FB; q++) {
-                                const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR>(p, xrow, scol, e0, n, c[q]);
+                                const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q]);
                                 const unsigned gm = __ballot_sync(FULL, g);
                                 if (gm) {
                                     if (lane == 0) h[jq[q]] = t0 + __ffs(gm) - 1;
@@ -570,9 +578,9 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
     }
 }
 
-template <int SIGB, bool CSR, int NW>
+template <int SIGB, bool CSR, int NW, typename W>
 static wmh_status ix_launch(IxParams p, cudaStream_t s) {
-    auto kern = hash_index_kernel<SIGB, CSR, NW>;
+    auto kern = hash_index_kernel<SIGB, CSR, NW, W>;
     int dev = 0, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
@@ -585,7 +593,7 @@ static wmh_status ix_launch(IxParams p, cudaStream_t s) {
         // the dense row staged as words for the fallback lookups, when short
         // (measured: 4 KiB rows cost more in occupancy than they save)
         static const int stage_max = getenv("WMH_INDEX_STAGE_MAX") ? atoi(getenv("WMH_INDEX_STAGE_MAX")) : 1024;
-        p.capn = p.D <= stage_max ? (int)((p.D + 3) / 4) : 0;
+        p.capn = p.D <= stage_max ? (int)((p.D * (int64_t)sizeof(W) + 3) / 4) : 0;
     }
     const size_t smem = (size_t)p.k * 4 + (size_t)(2 * NW * 32 * 8 + 33) * 4 + (size_t)p.capn * 4;
     WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "index smem attr");
@@ -605,13 +613,18 @@ static wmh_status ix_launch(IxParams p, cudaStream_t s) {
     return WMH_OK;
 }
 
-template <int SIGB, bool CSR>
+template <int SIGB, bool CSR, typename W>
 static wmh_status ix_launch_nw(const IxParams &p, int nw, cudaStream_t s) {
     switch (nw) {
-        case 2: return ix_launch<SIGB, CSR, 2>(p, s);
-        case 4: return ix_launch<SIGB, CSR, 4>(p, s);
-        default: return ix_launch<SIGB, CSR, 8>(p, s);
+        case 2: return ix_launch<SIGB, CSR, 2, W>(p, s);
+        case 4: return ix_launch<SIGB, CSR, 4, W>(p, s);
+        default: return ix_launch<SIGB, CSR, 8, W>(p, s);
     }
+}
+
+template <int SIGB, bool CSR>
+static wmh_status ix_launch_w(const IxParams &p, int nw, int wb, cudaStream_t s) {
+    return wb == 2 ? ix_launch_nw<SIGB, CSR, uint16_t>(p, nw, s) : ix_launch_nw<SIGB, CSR, uint8_t>(p, nw, s);
 }
 
 // Index horizon T: draws t < T are filed.  0 = automatic: from the layout's
@@ -728,7 +741,8 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
         if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index sort"); break; }
 
         const uint32_t uni = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
-        if ((st = launch_draw_table(table, a.k, a.S, M, L->cell_pack, uni, 1u, a.stream)) != WMH_OK) break;
+        const uint32_t *pk = (L->flags & WMH_LAYOUT_WIDE) ? nullptr : L->cell_pack;
+        if ((st = launch_draw_table(table, a.k, a.S, M, pk, uni, 1u, a.stream, L->int_to_comp, L->comp_to_m)) != WMH_OK) break;
 
     } while (0);
     if (st != WMH_OK) {
@@ -769,7 +783,8 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     p.n_rows = a.rows.n_rows;
     p.D = a.rows.dim;
     p.comp_to_m = L->comp_to_m;
-    p.pack = L->cell_pack;
+    p.pack = (L->flags & WMH_LAYOUT_WIDE) ? nullptr : L->cell_pack;
+    p.i2c = L->int_to_comp;
     p.uni_m = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
     p.M = M;
     p.pos = pos;
@@ -792,8 +807,9 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     int nw = 2;
     while (nw < 8 && (uint64_t)(64 / nw) * a.k * 4 > (128u << 10)) nw *= 2;
     if (nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
-    if (a.sig_bytes == 1) st = csr ? ix_launch_nw<1, true>(p, nw, a.stream) : ix_launch_nw<1, false>(p, nw, a.stream);
-    else st = csr ? ix_launch_nw<2, true>(p, nw, a.stream) : ix_launch_nw<2, false>(p, nw, a.stream);
+    const int wb = weight_bytes(a.rows);
+    if (a.sig_bytes == 1) st = csr ? ix_launch_w<1, true>(p, nw, wb, a.stream) : ix_launch_w<1, false>(p, nw, wb, a.stream);
+    else st = csr ? ix_launch_w<2, true>(p, nw, wb, a.stream) : ix_launch_w<2, false>(p, nw, wb, a.stream);
     return st;
 }
 

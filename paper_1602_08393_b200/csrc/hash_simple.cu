@@ -6,14 +6,16 @@
 // Per thread: Alg. 3's while loop over the counter stream
 // r_t (common.cuh), Alg. 5's ISGREEN with IntToComp/CompToM fused
 // into one packed load cell_pack[r] = (c << 8) | (r - CompToM[c]) (exact since
-// every bound <= 255), and the saturating cap (reading R9).
+// every bound <= 255; wide layouts use the two lookups), and the saturating cap
+// (reading R9).  Weights uint8 or uint16 (fixed-point real data).
 #include "common.cuh"
 
 namespace wmh {
 
 // x_c of a CSR row by binary search over its ascending columns (Sec. 3.3's
 // O(log d) search, applied to the row's support).
-__device__ __forceinline__ uint32_t csr_value(const int32_t *__restrict__ col, const uint8_t *__restrict__ val,
+template <typename W>
+__device__ __forceinline__ uint32_t csr_value(const int32_t *__restrict__ col, const W *__restrict__ val,
                                               int64_t a, int64_t b, uint32_t c) {
     int64_t lo = a, hi = b;                       // first index with col >= c
     while (lo < hi) {
@@ -24,10 +26,11 @@ __device__ __forceinline__ uint32_t csr_value(const int32_t *__restrict__ col, c
     return (lo < b && (uint32_t)__ldg(col + lo) == c) ? (uint32_t)__ldg(val + lo) : 0u;
 }
 
-template <int SIGB, bool CSR>
+template <int SIGB, bool CSR, typename W>
 __global__ void __launch_bounds__(256) hash_simple_kernel(
-    const uint8_t *__restrict__ dense, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-    const uint8_t *__restrict__ val, int64_t n_rows, int64_t dim, const uint32_t *__restrict__ pack, uint32_t M,
+    const W *__restrict__ dense, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+    const W *__restrict__ val, int64_t n_rows, int64_t dim, const uint32_t *__restrict__ pack, uint32_t uni_m,
+    const uint32_t *__restrict__ i2c, const uint32_t *__restrict__ c2m, uint32_t M,
     uint64_t S, uint32_t k, uint32_t cap, void *__restrict__ sig, unsigned long long *__restrict__ n_sat) {
     const int64_t total = n_rows * (int64_t)k;
     unsigned int sat = 0;
@@ -43,8 +46,8 @@ __global__ void __launch_bounds__(256) hash_simple_kernel(
         if (!CSR || a < b) {
             for (uint32_t t = 0; t < cap; t++) {
                 const uint32_t r = mulhi_range(splitmix64(keyj ^ (uint64_t)t), M);
-                const uint32_t p = __ldg(pack + r);
-                const uint32_t c = p >> 8, off = p & 0xFFu;
+                const uint2 cell = cell_lookup(r, pack, uni_m, i2c, c2m);
+                const uint32_t c = cell.x, off = cell.y;
                 uint32_t xv;
                 if (CSR) xv = csr_value(col, val, a, b, c);
                 else xv = __ldg(dense + n * dim + c);
@@ -68,13 +71,20 @@ wmh_status launch_hash_simple(const HashArgs &a) {
     int64_t blocks = min((int64_t)num_sms() * 32, (total + threads - 1) / threads);
     const uint32_t M = (uint32_t)a.L->M;
     const bool csr = a.rows.kind == WMH_CSR;
-#define WMH_SIMPLE(SB, CS)                                                                                     \
-    hash_simple_kernel<SB, CS><<<(unsigned)blocks, threads, 0, a.stream>>>(                                      \
-        a.rows.dense, a.rows.row_ptr, a.rows.col, a.rows.val, a.rows.n_rows, a.rows.dim, a.L->cell_pack, M, a.S, \
-        a.k, a.cap, a.sig, a.n_sat)
+    const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
+    const uint32_t *pack = (a.L->flags & WMH_LAYOUT_WIDE) ? nullptr : a.L->cell_pack;
+#define WMH_SIMPLE(SB, CS, W)                                                                                    \
+    hash_simple_kernel<SB, CS, W><<<(unsigned)blocks, threads, 0, a.stream>>>(                                   \
+        reinterpret_cast<const W *>(a.rows.dense), a.rows.row_ptr, a.rows.col, reinterpret_cast<const W *>(a.rows.val), \
+        a.rows.n_rows, a.rows.dim, pack, uni_m, a.L->int_to_comp, a.L->comp_to_m, M, a.S, a.k, a.cap, a.sig, a.n_sat)
     kernel_timer_begin(a.stream);
-    if (a.sig_bytes == 1) { if (csr) WMH_SIMPLE(1, true); else WMH_SIMPLE(1, false); }
-    else { if (csr) WMH_SIMPLE(2, true); else WMH_SIMPLE(2, false); }
+    if (weight_bytes(a.rows) == 2) {
+        if (a.sig_bytes == 1) { if (csr) WMH_SIMPLE(1, true, uint16_t); else WMH_SIMPLE(1, false, uint16_t); }
+        else { if (csr) WMH_SIMPLE(2, true, uint16_t); else WMH_SIMPLE(2, false, uint16_t); }
+    } else {
+        if (a.sig_bytes == 1) { if (csr) WMH_SIMPLE(1, true, uint8_t); else WMH_SIMPLE(1, false, uint8_t); }
+        else { if (csr) WMH_SIMPLE(2, true, uint8_t); else WMH_SIMPLE(2, false, uint8_t); }
+    }
     kernel_timer_end(a.stream);
 #undef WMH_SIMPLE
     WMH_LAUNCH_CHECK("hash_simple launch");

@@ -30,20 +30,21 @@ constexpr int STRAG_MAX = 4;            // max pending rows handled draw-paralle
 // table[j * T0 + t] = (c * cmul, r_t - CompToM[c]) of draw r_t of hash j, t < T0
 // (cmul = 1 for row-major tiles, the column stride for column-major ones).
 __global__ void draw_table_kernel(uint2 *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
-                                  const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t cmul) {
+                                  const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t cmul,
+                                  const uint32_t *__restrict__ i2c, const uint32_t *__restrict__ c2m) {
     const int64_t total = (int64_t)k * T0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
-        const uint2 d = unpack_cell(cell_of(draw_r(S, j, t, M), pack, uni_m));
+        const uint2 d = cell_lookup(draw_r(S, j, t, M), pack, uni_m, i2c, c2m);
         table[i] = make_uint2(d.x * cmul, d.y);
     }
 }
 
 wmh_status launch_draw_table(uint2 *table, uint32_t k, uint64_t S, uint32_t M, const uint32_t *pack, uint32_t uni_m,
-                             uint32_t cmul, cudaStream_t s) {
+                             uint32_t cmul, cudaStream_t s, const uint32_t *i2c, const uint32_t *c2m) {
     const int64_t total = (int64_t)k * T0;
     const int blocks = (int)min((int64_t)num_sms() * 8, (total + 255) / 256);
-    draw_table_kernel<<<blocks, 256, 0, s>>>(table, k, S, M, pack, uni_m, cmul);
+    draw_table_kernel<<<blocks, 256, 0, s>>>(table, k, S, M, pack, uni_m, cmul, i2c, c2m);
     WMH_LAUNCH_CHECK("draw table launch");
     return WMH_OK;
 }
@@ -382,6 +383,8 @@ static wmh_status launch_tiled(const TiledParams &p, size_t smem, int grid, cuda
 
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     *handled = false;
+    // the tiles test uint8 weights against 8-bit cell offsets: narrow layouts only
+    if ((a.L->flags & WMH_LAYOUT_WIDE) || weight_bytes(a.rows) != 1) return WMH_OK;
     if (a.rows.kind != WMH_DENSE) return launch_hash_tiled_csr(a, handled);
     // column-major tile with the SIMD first round (hash_tiled_cm.cu) unless
     // WMH_TILED_RM=1 selects this row-major kernel

@@ -137,17 +137,18 @@ __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint2 *buf, ui
     return npend;
 }
 
-template <int SIGB, int P>
+template <int SIGB, int P, int NR0>
 __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams p) {
-    constexpr int R = 128 / P, NWD = R / 4, PD = 32 / P;   // rows, 4-row words (NWD * P == 32), draws per part
+    // rows, 4-row words (NWD * P == 32), draws per part of the NR0 SWAR rounds
+    constexpr int R = 128 / P, NWD = R / 4, PD = 32 * NR0 / P;
     extern __shared__ __align__(16) uint32_t smem[];
     const int Rp = p.Rp;
     uint8_t *xs = reinterpret_cast<uint8_t *>(smem);                               // [D][Rp]
     const size_t xs_bytes = ((size_t)p.D * Rp + 15) & ~(size_t)15;
     uint2 *sbuf_all = reinterpret_cast<uint2 *>(xs + xs_bytes);                     // [NW][T0]
     uint2 *swin_all = sbuf_all + CM_NW * T0;                                        // [NW][32]
-    uint4 *sr0_all = reinterpret_cast<uint4 *>(swin_all + CM_NW * 32);              // [NW][32] round-0 consts
-    uint32_t *spart_all = reinterpret_cast<uint32_t *>(sr0_all + CM_NW * 32);       // [NW][32] partial h4
+    uint4 *sr0_all = reinterpret_cast<uint4 *>(swin_all + CM_NW * 32);              // [NW][64] SWAR-round consts
+    uint32_t *spart_all = reinterpret_cast<uint32_t *>(sr0_all + CM_NW * 64);       // [NW][32] partial h4
     uint16_t *hres_all = reinterpret_cast<uint16_t *>(spart_all + CM_NW * 32);      // [NW][HB][R] results
     uint16_t *spend_all = hres_all + CM_NW * CM_HB * R;                             // [NW][2][R]
     uint8_t *sflag4 = reinterpret_cast<uint8_t *>(spend_all + CM_NW * 2 * R);       // [NWD] live-row nibbles
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint2 *sbuf = sbuf_all + warp * T0;
     uint2 *swin = swin_all + warp * 32;
-    uint4 *sr0 = sr0_all + warp * 32;
+    uint4 *sr0 = sr0_all + warp * 64;
     uint32_t *spart = spart_all + warp * 32;
     uint16_t *hres_blk = hres_all + warp * CM_HB * R;                              // [HB][R]
     uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
@@ -269,11 +270,13 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             }
             const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
 
-            // ---- round 0 (draws 0..31): lane = (4-row word, 32/P-draw part) ---------
-            {
-                const uint2 d = sbuf[lane];
-                const uint32_t nb = (uint32_t)lane < p.cap ? 255u - d.y : 0u;   // t >= cap: never green
-                sr0[lane] = make_uint4(d.x, (nb & 0x7Fu) * 0x01010101u, nb * 0x01010101u, 0u);
+            // ---- SWAR rounds (draws 0..32*NR0-1): lane = (4-row word, part) ---------
+#pragma unroll
+            for (int r0 = 0; r0 < NR0; r0++) {
+                const uint32_t t = 32u * r0 + lane;
+                const uint2 d = sbuf[t];
+                const uint32_t nb = t < p.cap ? 255u - d.y : 0u;                // t >= cap: never green
+                sr0[t] = make_uint4(d.x, (nb & 0x7Fu) * 0x01010101u, nb * 0x01010101u, 0u);
             }
             __syncwarp();
             const int w = lane % NWD, part = lane / NWD;
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             {
                 const bool wl = lane < NWD;
                 const uint32_t live4 = wl ? (uint32_t)sflag4[w] : 0u;
-                // bytes: first green index (0..31) -> h = index + 1; 0xFF -> 0 (pending)
+                // bytes: first green index (0..32*NR0-1) -> h = index + 1; 0xFF -> 0 (pending)
                 const uint32_t v = ((h4 & 0x7F7F7F7Fu) + 0x01010101u) & 0x7F7F7F7Fu;
                 if (wl) {
                     const uint32_t lo = prmt(v, 0u, 0x4140), hi = prmt(v, 0u, 0x4342);
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             }
             __syncwarp();
             const uint16_t *cur = own1;
-            uint32_t q = 1;
+            uint32_t q = NR0;
             switch (C) {
                 case 8: npend = cm_rounds<8>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
                 case 16: npend = cm_rounds<16>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
@@ -426,15 +429,19 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 }
 
 static size_t cm_smem(int D, int R, int Rp) {
-    return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 8 + (size_t)CM_NW * 32 * 16 +
+    return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 8 + (size_t)CM_NW * 64 * 16 +
            (size_t)CM_NW * 32 * 4 + (size_t)CM_NW * CM_HB * R * 2 + (size_t)CM_NW * 2 * R * 2 + (size_t)(R / 4) + 16;
 }
 
 template <int SIGB, int P>
 static void cm_launch(const CmParams &p, size_t smem, int grid, cudaStream_t s) {
-    cudaFuncSetAttribute(hash_tiled_cm_kernel<SIGB, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // SWAR rounds before the pending-list rounds: 2 (draws 0..63, ~96% of the
+    // rows resolved at s = 0.05) unless WMH_CM_SWAR_ROUNDS=1
+    static const int nr0 = getenv("WMH_CM_SWAR_ROUNDS") && atoi(getenv("WMH_CM_SWAR_ROUNDS")) == 1 ? 1 : 2;
+    auto kern = nr0 == 1 ? hash_tiled_cm_kernel<SIGB, P, 1> : hash_tiled_cm_kernel<SIGB, P, 2>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel_timer_begin(s);
-    hash_tiled_cm_kernel<SIGB, P><<<grid, CM_NT, smem, s>>>(p);
+    kern<<<grid, CM_NT, smem, s>>>(p);
     kernel_timer_end(s);
 }
 
@@ -461,6 +468,8 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
     const int sms = num_sms();
     int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 8, ((int64_t)sms * 8 + n_tiles - 1) / n_tiles));
+    static const int hc_env = getenv("WMH_CM_HCHUNKS") ? atoi(getenv("WMH_CM_HCHUNKS")) : 0;
+    if (hc_env > 0) n_hchunks = (int)min((int64_t)hc_env, (int64_t)(a.k + CM_HB - 1) / CM_HB);
     const int hchunk = (int)(((a.k + n_hchunks - 1) / n_hchunks + CM_HB - 1) / CM_HB * CM_HB);   // blocks stay 4-aligned
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
 

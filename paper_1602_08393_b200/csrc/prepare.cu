@@ -62,8 +62,9 @@ __global__ void __launch_bounds__(256) colmax_dense_vec16(const uint8_t *__restr
     }
 }
 
-// Generic byte path (any dim / alignment).
-__global__ void colmax_dense_bytes(const uint8_t *__restrict__ x, int64_t n_rows, int64_t dim,
+// Generic path (any dim / alignment / weight width).
+template <typename W>
+__global__ void colmax_dense_bytes(const W *__restrict__ x, int64_t n_rows, int64_t dim,
                                    int64_t rows_per_slice, uint32_t *__restrict__ colmax) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= dim) return;
@@ -76,7 +77,8 @@ __global__ void colmax_dense_bytes(const uint8_t *__restrict__ x, int64_t n_rows
 
 // CSR: one thread per nonzero; read first, atomic only when it would raise the
 // max (hot Zipf columns otherwise serialise on one address).
-__global__ void colmax_csr(const int32_t *__restrict__ col, const uint8_t *__restrict__ val, int64_t nnz,
+template <typename W>
+__global__ void colmax_csr(const int32_t *__restrict__ col, const W *__restrict__ val, int64_t nnz,
                            uint32_t *__restrict__ colmax) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
         uint32_t v = val[e];
@@ -87,7 +89,8 @@ __global__ void colmax_csr(const int32_t *__restrict__ col, const uint8_t *__res
 
 // ---------------------------------------------------------- validation
 // First offending position, as a min-reduced 64-bit key.
-__global__ void check_dense_bounds(const uint8_t *__restrict__ x, int64_t n_rows, int64_t dim,
+template <typename W>
+__global__ void check_dense_bounds(const W *__restrict__ x, int64_t n_rows, int64_t dim,
                                    const uint32_t *__restrict__ bounds, unsigned long long *first_bad) {
     for (int64_t n = blockIdx.x; n < n_rows; n += gridDim.x)
         for (int64_t c = threadIdx.x; c < dim; c += blockDim.x)
@@ -103,8 +106,9 @@ __global__ void colmax_exceeds(const uint32_t *__restrict__ cm, const uint32_t *
 
 // One warp per row: row_ptr monotone, columns in range and strictly
 // ascending, values within bounds.  key = (nnz index << 3) | code.
+template <typename W>
 __global__ void check_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                          const uint8_t *__restrict__ val, int64_t n_rows, int64_t dim, int64_t nnz,
+                          const W *__restrict__ val, int64_t n_rows, int64_t dim, int64_t nnz,
                           const uint32_t *__restrict__ bounds, unsigned long long *first_bad) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -234,7 +238,7 @@ __global__ void fill_int_to_comp(const uint32_t *__restrict__ comp_to_m, int64_t
         uint32_t a = comp_to_m[c], b = comp_to_m[c + 1];
         for (uint32_t t = a + lane; t < b; t += 32) {
             i2c[t] = (uint32_t)c;
-            pack[t] = ((uint32_t)c << 8) | (t - a);
+            if (pack) pack[t] = ((uint32_t)c << 8) | (t - a);
         }
     }
 }
@@ -248,8 +252,9 @@ using namespace wmh;
 // hist[b] += 1 for a row with |x|_1 in [2^b, 2^(b+1)); hist[64] counts empty
 // rows.  Warp per row.  The index kernel sizes its draw horizon from the
 // 0.1% quantile (Theorem 2: a row needs ~1/s draws, s = |x|_1 / M, Eq. 17).
-__global__ void __launch_bounds__(256) rowsum_hist(const uint8_t *__restrict__ dense, const int64_t *__restrict__ row_ptr,
-                                                   const uint8_t *__restrict__ val, int64_t n_rows, int64_t dim,
+template <typename W>
+__global__ void __launch_bounds__(256) rowsum_hist(const W *__restrict__ dense, const int64_t *__restrict__ row_ptr,
+                                                   const W *__restrict__ val, int64_t n_rows, int64_t dim,
                                                    unsigned long long *__restrict__ hist) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -258,8 +263,8 @@ __global__ void __launch_bounds__(256) rowsum_hist(const uint8_t *__restrict__ d
     for (int64_t r = w0; r < n_rows; r += nw) {
         unsigned long long s = 0;
         if (dense) {
-            const uint8_t *x = dense + r * dim;
-            if ((dim & 3) == 0 && ((uintptr_t)dense & 3) == 0) {
+            const W *x = dense + r * dim;
+            if (sizeof(W) == 1 && (dim & 3) == 0 && ((uintptr_t)dense & 3) == 0) {
                 const uint32_t *x4 = reinterpret_cast<const uint32_t *>(x);
                 for (int64_t i = lane; i < dim / 4; i += 32) s += __dp4a(__ldg(x4 + i), 0x01010101u, 0u);
             } else {
@@ -283,9 +288,12 @@ extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *s
     cudaStream_t s = (cudaStream_t)stream;
     WMH_CUDA_TRY(cudaMemsetAsync(colmax, 0, sizeof(uint32_t) * rows->dim, s), "memset colmax");
     if (rows->n_rows == 0) return WMH_OK;
+    const bool w16 = weight_bytes(*rows) == 2;
+    const uint16_t *dense16 = reinterpret_cast<const uint16_t *>(rows->dense);
+    const uint16_t *val16 = reinterpret_cast<const uint16_t *>(rows->val);
     if (rows->kind == WMH_DENSE) {
         const int sms = num_sms();
-        const bool vec = (rows->dim % 16 == 0) && (rows->dim / 16 <= 256) && ((uintptr_t)rows->dense % 16 == 0);
+        const bool vec = !w16 && (rows->dim % 16 == 0) && (rows->dim / 16 <= 256) && ((uintptr_t)rows->dense % 16 == 0);
         if (vec) {
             const int64_t blocks = min(rows->n_rows, (int64_t)sms * 4);
             const int64_t per = (rows->n_rows + blocks - 1) / blocks;
@@ -298,13 +306,18 @@ extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *s
             gy = min(gy, (int64_t)65535);
             const int64_t per = (rows->n_rows + gy - 1) / gy;
             gy = (rows->n_rows + per - 1) / per;
-            colmax_dense_bytes<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, s>>>(rows->dense, rows->n_rows,
-                                                                                  rows->dim, per, colmax);
+            if (w16)
+                colmax_dense_bytes<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, s>>>(dense16, rows->n_rows,
+                                                                                      rows->dim, per, colmax);
+            else
+                colmax_dense_bytes<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, s>>>(rows->dense, rows->n_rows,
+                                                                                      rows->dim, per, colmax);
         }
     } else {
         if (rows->nnz > 0) {
             int64_t blocks = min((int64_t)num_sms() * 16, (rows->nnz + 255) / 256);
-            colmax_csr<<<(unsigned)blocks, 256, 0, s>>>(rows->col, rows->val, rows->nnz, colmax);
+            if (w16) colmax_csr<<<(unsigned)blocks, 256, 0, s>>>(rows->col, val16, rows->nnz, colmax);
+            else colmax_csr<<<(unsigned)blocks, 256, 0, s>>>(rows->col, rows->val, rows->nnz, colmax);
         }
     }
     WMH_LAUNCH_CHECK("colmax launch");
@@ -362,16 +375,26 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
             if (cst != WMH_OK) { cudaFreeAsync(scr, s); return fail(cst); }
             colmax_exceeds<<<(unsigned)((dim + 255) / 256), 256, 0, s>>>(cm, L->bounds, dim, bad);
         } else
-            check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, rows->val, rows->n_rows, dim, rows->nnz,
-                                              L->bounds, bad);
+        {
+            if (weight_bytes(*rows) == 2)
+                check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, reinterpret_cast<const uint16_t *>(rows->val),
+                                                  rows->n_rows, dim, rows->nnz, L->bounds, bad);
+            else
+                check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, rows->val, rows->n_rows, dim, rows->nnz,
+                                                  L->bounds, bad);
+        }
     }
     unsigned long long *hist = nullptr, hhist[66] = {0};
     const bool stats = rows && rows->n_rows > 0;
     if (stats) {
         if (cudaMallocAsync((void **)&hist, sizeof hhist, s) != cudaSuccess) { cudaFreeAsync(scr, s); set_error("wmh_prepare: scratch alloc failed"); return fail(WMH_ENOMEM); }
         cudaMemsetAsync(hist, 0, sizeof hhist, s);
-        rowsum_hist<<<sms * 8, 256, 0, s>>>(rows->kind == WMH_DENSE ? rows->dense : nullptr, rows->row_ptr, rows->val,
-                                            rows->n_rows, dim, hist);
+        if (weight_bytes(*rows) == 2)
+            rowsum_hist<<<sms * 8, 256, 0, s>>>(rows->kind == WMH_DENSE ? reinterpret_cast<const uint16_t *>(rows->dense) : nullptr,
+                                                rows->row_ptr, reinterpret_cast<const uint16_t *>(rows->val), rows->n_rows, dim, hist);
+        else
+            rowsum_hist<<<sms * 8, 256, 0, s>>>(rows->kind == WMH_DENSE ? rows->dense : nullptr, rows->row_ptr, rows->val,
+                                                rows->n_rows, dim, hist);
         count_launch();
         cudaMemcpyAsync(hhist, hist, sizeof hhist, cudaMemcpyDeviceToHost, s);
     }
@@ -399,14 +422,18 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     const unsigned long long M = host[0], first_bad = host[1];
     const unsigned int mn = (unsigned int)(host[2] & 0xFFFFFFFFu), mx = (unsigned int)(host[2] >> 32);
 
-    if (mx > 255) { set_error("wmh_prepare: a bound is %u > 255 (weights are uint8)", mx); return fail(WMH_EINVAL); }
+    if (mx > 65535) { set_error("wmh_prepare: a bound is %u > 65535 (weights are at most uint16)", mx); return fail(WMH_EINVAL); }
     if (first_bad != ~0ull) {
         if (rows->kind == WMH_DENSE) {
             // slow path: locate the first offending (row, col)
             unsigned long long *b2 = nullptr, fb = ~0ull;
             if (cudaMallocAsync((void **)&b2, sizeof fb, s) != cudaSuccess) return fail(WMH_ENOMEM);
             cudaMemcpyAsync(b2, &fb, sizeof fb, cudaMemcpyHostToDevice, s);
-            check_dense_bounds<<<sms * 8, 256, 0, s>>>(rows->dense, rows->n_rows, dim, L->bounds, b2);
+            if (weight_bytes(*rows) == 2)
+                check_dense_bounds<<<sms * 8, 256, 0, s>>>(reinterpret_cast<const uint16_t *>(rows->dense), rows->n_rows, dim,
+                                                           L->bounds, b2);
+            else
+                check_dense_bounds<<<sms * 8, 256, 0, s>>>(rows->dense, rows->n_rows, dim, L->bounds, b2);
             count_launch();
             cudaMemcpyAsync(&fb, b2, sizeof fb, cudaMemcpyDeviceToHost, s);
             cudaError_t e3 = cudaStreamSynchronize(s);
@@ -427,9 +454,10 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     if (M >= (1ull << 32)) { set_error("wmh_prepare: M = %llu >= 2^32", M); return fail(WMH_EOVERFLOW); }
     L->M = M;
     if (mn == mx) { L->flags |= WMH_LAYOUT_UNIFORM; L->uniform_m = mx; }
+    if (mx > 255) L->flags |= WMH_LAYOUT_WIDE;       // 8-bit cell offsets no longer fit: no cell_pack
 
     if (cudaMalloc(&L->int_to_comp, sizeof(uint32_t) * M) != cudaSuccess ||
-        cudaMalloc(&L->cell_pack, sizeof(uint32_t) * M) != cudaSuccess) {
+        (!(L->flags & WMH_LAYOUT_WIDE) && cudaMalloc(&L->cell_pack, sizeof(uint32_t) * M) != cudaSuccess)) {
         set_error("wmh_prepare: cudaMalloc of IntToComp (%llu cells) failed", M);
         return fail(WMH_ENOMEM);
     }
