@@ -87,7 +87,9 @@ def test_prepare_zero_width_and_errors(wmh):
     with pytest.raises(wmh.WmhError, match="WMH_EEMPTY"):
         wmh.prepare(bounds=torch.zeros(5, dtype=torch.uint32).cuda())
     with pytest.raises(wmh.WmhError, match="WMH_EINVAL"):
-        wmh.prepare(bounds=torch.full((5,), 300, dtype=torch.uint32).cuda())
+        wmh.prepare(bounds=torch.full((5,), 70000, dtype=torch.uint32).cuda())
+    wide = wmh.prepare(bounds=torch.full((5,), 300, dtype=torch.uint32).cuda())      # f1: bounds up to 65535
+    assert wide.M == 1500 and wide.flags == 3
     x = torch.tensor([[1, 2], [3, 9]], dtype=torch.uint8).cuda()
     with pytest.raises(wmh.WmhError, match=r"WMH_EBOUND.*x\[1\]\[1\]"):
         wmh.prepare(wmh.Rows.from_dense(x), bounds=torch.tensor([3, 5], dtype=torch.uint32).cuda())

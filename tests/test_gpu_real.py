@@ -87,9 +87,9 @@ def test_scale_invariance_across_kernels(wmh):
         r16 = _rows16(wmh, x16, False)
         l16 = wmh.prepare(r16)
         assert l16.M == l8.M << f
-        s16 = wmh.hash(l16, r16, 4, 128, 65535)
-        assert wmh.last_algo == "index"
-        assert torch.equal(s8, s16)
+        for algo in ("index", "simple", "auto"):
+            s16 = wmh.hash(l16, r16, 4, 128, 65535, algo=algo)
+            assert torch.equal(s8, s16), (f, algo)
 
 
 def test_tiled_rejects_wide(wmh):
