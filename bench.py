@@ -78,6 +78,8 @@ def _generate(cfg_name, cfg, lo, hi):
     import datagen
     if cfg_name == "c2":
         data = datagen.Dense(datagen.gen_c2_rows(cfg.data_seed, lo, hi, cfg.dim))
+    elif cfg_name == "c2r":
+        data = datagen.Dense(datagen.gen_c2_real_rows(cfg.data_seed, lo, hi, cfg.dim))
     elif cfg_name == "c1":
         data = datagen.Dense(datagen.gen_counter_c1_rows(cfg.data_seed, np.arange(lo, hi), cfg.dim))
     elif cfg_name == "c5":
@@ -89,7 +91,8 @@ def _generate(cfg_name, cfg, lo, hi):
 
 
 def desc(cfg, n):
-    return (f"{cfg.name}: N={n} rows/GPU, D={cfg.dim}, {cfg.kind} uint8, k={cfg.k}, cap={cfg.cap}, "
+    w = "real -> uint16 fixed point" if cfg.name == "c2r" else "uint8"
+    return (f"{cfg.name}: N={n} rows/GPU, D={cfg.dim}, {cfg.kind} {w}, k={cfg.k}, cap={cfg.cap}, "
             f"uint{8 * cfg.sig_bytes} signatures, seed={cfg.seed}")
 
 
@@ -266,10 +269,21 @@ def main():
         data = datagen.CounterRows(args.config, cfg.data_seed, rank * n, n, cfg.dim)
     else:
         cfg, n, data = workload(args.config, rank, args.rows)
+    # f1 (c2r): real-valued rows -> Sec. 4 scale choice -> uint16 fixed point, on the
+    # device and before the timed region (the paper's "one time pre-processing")
+    quant = None
+    if cfg.name == "c2r":
+        xf = torch.from_numpy(data.x).to(dev)
+        grid = [1.0, 2.0, 4.0, 8.0, 16.0, 32.0, 64.0]
+        scale = wmh.choose_scale(wmh.Rows.from_dense(xf), grid)
+        xd = wmh.quantize(xf, scale)
+        del xf
+        data = datagen.Dense(xd.cpu().numpy())
+        quant = {"scale": scale, "grid": grid, "weights": "uint16 fixed point floor(x*scale)"}
     # inputs resident in HBM before the timed region
     if xd is not None:
         rows = wmh.Rows.from_dense(xd)
-        in_bytes = xd.numel()
+        in_bytes = xd.numel() * xd.element_size()
     elif isinstance(data, datagen.Dense):
         rows = wmh.Rows.from_dense(torch.from_numpy(data.x).to(dev))
         in_bytes = data.x.nbytes
@@ -327,7 +341,8 @@ def main():
 
     # ---- roofline of the dominant (only) kernel of the step
     if xd is not None:                  # row sums on the device, in chunks (no full int64 copy)
-        x_sum = torch.cat([xd[a0:a0 + 65536].sum(1, dtype=torch.int64) for a0 in range(0, n, 65536)]).cpu().numpy()
+        x_sum = torch.cat([xd[a0:a0 + 65536].to(torch.int32).sum(1, dtype=torch.int64)
+                           for a0 in range(0, n, 65536)]).cpu().numpy()
     else:
         x_sum = row_sums(data)
     draws = expected_draws(x_sum, M, cfg.k, cfg.cap)      # this rank's algorithmic draw-tests per launch
@@ -343,7 +358,7 @@ def main():
     roof = roofline(algo_used, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
     if algo_used == "index":
         if xd is not None:
-            nnz = sum(int((xd[a0:a0 + 65536] != 0).sum().item()) for a0 in range(0, n, 65536))
+            nnz = sum(int((xd[a0:a0 + 65536].to(torch.int32) != 0).sum().item()) for a0 in range(0, n, 65536))
         elif isinstance(data, datagen.Dense):
             nnz = int(np.count_nonzero(data.x))
         else:
@@ -371,7 +386,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        bnds = xd.amax(0).to(torch.int32).cpu().numpy().astype(np.uint32) if xd is not None \
+        bnds = torch.stack([xd[a0:a0 + 65536].to(torch.int32).amax(0) for a0 in range(0, n, 65536)]).amax(0) \
+            .cpu().numpy().astype(np.uint32) if xd is not None \
             else layout_bounds(cfg, data)
         r, cores, sample = oracle_rate(cfg, data, bnds, args.cpu_seconds)
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
@@ -393,6 +409,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
+            "quantization": quant,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
@@ -471,7 +488,7 @@ def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd=None):
         n = min(n, 1 << 20)
         hx = xd[:n].cpu().pin_memory()
         hrows = wmh.Rows.from_dense(hx)
-        h2d = hx.numel()
+        h2d = hx.numel() * hx.element_size()
     elif isinstance(data, datagen.Dense):
         hx = torch.from_numpy(data.x).pin_memory()
         hrows = wmh.Rows.from_dense(hx)

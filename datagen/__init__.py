@@ -238,6 +238,8 @@ CONFIGS = {
     "c3": Config("c3", 1_000_000, 1 << 20, 1000, 65535, 2, data_seed=1003, kind="csr"),
     "c4": Config("c4", 200_000, 65536, 4000, 65535, 2, data_seed=1004, kind="csr", fixed_bound=255),
     "c5": Config("c5", 16_000_000, 4096, 1024, 65535, 2, data_seed=1005, kind="dense", n_pairs=10_000_000),
+    # f1: c2's histograms as real values, quantised to uint16 fixed point on the device
+    "c2r": Config("c2r", 100_000, 1024, 500, 65535, 2, data_seed=1002, kind="dense"),
 }
 
 
@@ -266,6 +268,27 @@ def gen_c2_rows(data_seed: int, row_begin: int, row_end: int, dim: int = 1024) -
         w = np.minimum(255.0, np.rint(64.0 * g)).astype(np.uint8)
         a, b = max(lo, row_begin), min(hi, row_end)
         out[a - row_begin:b - row_begin] = w[a - lo:b - lo]
+    return out
+
+
+def gen_c2_real_rows(data_seed: int, row_begin: int, row_end: int, dim: int = 1024) -> np.ndarray:
+    """c2r (f1): the c2 recipe's real histogram 64*g BEFORE rounding (float32):
+    the weights the fixed-point path quantises (reading R18)."""
+    out = np.empty((row_end - row_begin, dim), np.float32)
+    n_zero = int(round(0.6 * dim))
+    target = 0.5 * 0.4 * dim
+    c0, c1 = row_begin // CHUNK, (row_end - 1) // CHUNK
+    for ch in range(c0, c1 + 1):
+        rng = _chunk_rng(data_seed, ch)
+        lo, hi = ch * CHUNK, (ch + 1) * CHUNK
+        g = rng.gamma(0.5, 1.0, size=(CHUNK, dim))
+        zero_pos = np.argpartition(rng.random((CHUNK, dim)), n_zero, axis=1)[:, :n_zero]
+        np.put_along_axis(g, zero_pos, 0.0, axis=1)
+        s = g.sum(axis=1, keepdims=True)
+        s[s == 0] = 1.0
+        g *= target / s
+        a, b = max(lo, row_begin), min(hi, row_end)
+        out[a - row_begin:b - row_begin] = (64.0 * g[a - lo:b - lo]).astype(np.float32)
     return out
 
 

@@ -103,7 +103,9 @@ wmh_status wmh_quantize(const float *in, int64_t n, float scale, uint16_t *out, 
  * denominator n_rows * sum_c max_n floor(x * s_a) of the mean effective
  * sparsity (Eq. 17) of the quantised rows.  rows_f32 uses the wmh_rows layout
  * with FLOAT weights (dense / val point to float32, weight_bytes ignored).
- * scales: host array of n_scales; out: host uint64[2 * n_scales] (num, den).
+ * scales: host array of n_scales (<= 1024); out: host uint64[3 * n_scales]:
+ * (num, den, clipped) with clipped = #weights whose floor(x * s_a) >= 65536 (the
+ * uint16 quantiser would saturate them; such a scale changes the data).
  * Synchronises `stream`.  Errors: EINVAL, ENOMEM, ECUDA. */
 wmh_status wmh_scale_objective(const wmh_rows *rows_f32, const float *scales, int32_t n_scales, uint64_t *out,
                                void *stream);

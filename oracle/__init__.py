@@ -297,23 +297,25 @@ def quantize(x, scale: float) -> np.ndarray:
 
 def scale_objective(x_rows, scales):
     """Sec. 4 for fixed point: per scale s, (sum_n sum_c floor(x s),
-    n_rows * sum_c max_n floor(x s)) -- the numerator and denominator of the mean
-    effective sparsity (Eq. 17) of the quantised rows.  x_rows: dense float32
-    (n_rows, D)."""
+    n_rows * sum_c max_n floor(x s), #weights with floor(x s) >= 65536) -- the
+    numerator and denominator of the mean effective sparsity (Eq. 17) of the
+    quantised rows and the count the uint16 quantiser saturates.  x_rows: dense
+    float32 (n_rows, D)."""
     x = np.asarray(x_rows, np.float32)
     out = []
     for s in scales:
         q = quantize(x, s).astype(np.int64)
-        out.append((int(q.sum()), int(x.shape[0]) * int(q.max(axis=0).sum())))
+        clipped = int((np.floor(x * np.float32(s)) >= 65536).sum())
+        out.append((int(q.sum()), int(x.shape[0]) * int(q.max(axis=0).sum()), clipped))
     return out
 
 
 def choose_scale(x_rows, scales) -> float:
-    """argmax of the mean effective sparsity; ties go to the smaller scale (SPEC
-    optimize_alpha, S:237-245)."""
+    """argmax of the mean effective sparsity over the scales that saturate no
+    weight; ties go to the smaller scale (SPEC optimize_alpha)."""
     best = None
-    for s, (num, den) in sorted(zip(scales, scale_objective(x_rows, scales)), key=lambda t: t[0]):
-        if den == 0:
+    for s, (num, den, clipped) in sorted(zip(scales, scale_objective(x_rows, scales)), key=lambda t: t[0]):
+        if den == 0 or clipped:
             continue
         if best is None or Fraction(num, den) > best[1]:
             best = (s, Fraction(num, den))

@@ -254,25 +254,27 @@ def quantize(x: torch.Tensor, scale: float, stream=None) -> torch.Tensor:
     return out
 
 
-def scale_objective(rows: Rows, scales, stream=None) -> list[tuple[int, int]]:
-    """Sec. 4: for each candidate scale, (numerator, denominator) of the mean
-    effective sparsity of the rows quantised at that scale: sum floor(x*s) and
-    n_rows * sum_c max_n floor(x*s).  `rows` holds float32 weights."""
+def scale_objective(rows: Rows, scales, stream=None) -> list[tuple[int, int, int]]:
+    """Sec. 4: for each candidate scale, (numerator, denominator, clipped) of
+    the mean effective sparsity of the rows quantised at that scale: sum floor(x*s),
+    n_rows * sum_c max_n floor(x*s), and the number of weights the uint16 quantiser
+    would saturate.  `rows` holds float32 weights."""
     if rows.weight_bytes != 4:
         raise ValueError("scale_objective takes float32 rows")
     sc = (ctypes.c_float * len(scales))(*[float(v) for v in scales])
-    out = (ctypes.c_uint64 * (2 * len(scales)))()
+    out = (ctypes.c_uint64 * (3 * len(scales)))()
     _lib.check(_lib.load().wmh_scale_objective(ctypes.byref(rows._c()), sc, len(scales), out, _stream(stream)))
-    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(len(scales))]
+    return [(int(out[3 * i]), int(out[3 * i + 1]), int(out[3 * i + 2])) for i in range(len(scales))]
 
 
 def choose_scale(rows: Rows, scales, stream=None) -> float:
-    """The candidate with the largest mean effective sparsity (ties: the smaller scale,
-    i.e. the smaller M); Sec. 4's alpha = argmax sum alpha x / sum ceil(alpha m)."""
+    """The candidate with the largest mean effective sparsity among those that do
+    not saturate a weight (ties: the smaller scale, i.e. the smaller M); Sec. 4's
+    alpha = argmax sum alpha x / sum ceil(alpha m)."""
     obj = scale_objective(rows, scales, stream)
     best = None
-    for s, (num, den) in sorted(zip(scales, obj), key=lambda t: t[0]):
-        if den == 0:
+    for s, (num, den, clipped) in sorted(zip(scales, obj), key=lambda t: t[0]):
+        if den == 0 or clipped:
             continue
         if best is None or num * best[2] > best[1] * den:
             best = (s, num, den)

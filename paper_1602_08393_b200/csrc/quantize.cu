@@ -36,22 +36,29 @@ __global__ void quantize_kernel(const float *__restrict__ in, int64_t n, float s
 // For every scale a: num[a] += floor(x * s_a) and colmax[a][c] = max floor(x * s_a).
 __global__ void scale_objective_kernel(const float *__restrict__ x, const int32_t *__restrict__ col, int64_t n,
                                        int64_t dim, const float *__restrict__ scales, int n_scales,
-                                       uint32_t *__restrict__ colmax, unsigned long long *__restrict__ num) {
+                                       uint32_t *__restrict__ colmax, unsigned long long *__restrict__ num,
+                                       unsigned long long *__restrict__ clipped) {
     for (int a = 0; a < n_scales; a++) {
         const float sc = scales[a];
         unsigned long long acc = 0;
+        unsigned clip = 0;
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
             const float v = __ldg(x + i);
             if (!(v > 0.f)) continue;
             const float qf = floorf(__fmul_rn(v, sc));
             const uint32_t q = qf >= 65535.f ? 65535u : (uint32_t)qf;
+            clip += qf >= 65536.f;
             acc += q;
             const int64_t c = col ? (int64_t)__ldg(col + i) : i % dim;
             uint32_t *dst = colmax + (int64_t)a * dim + c;
             if (q > *((volatile uint32_t *)dst)) atomicMax(dst, q);
         }
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+        for (int o = 16; o; o >>= 1) {
+            acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+            clip += __shfl_xor_sync(0xFFFFFFFFu, clip, o);
+        }
         if ((threadIdx.x & 31) == 0 && acc) atomicAdd(num + a, acc);
+        if ((threadIdx.x & 31) == 0 && clip) atomicAdd(clipped + a, (unsigned long long)clip);
     }
 }
 
@@ -103,15 +110,16 @@ extern "C" wmh_status wmh_scale_objective(const wmh_rows *rows, const float *sca
     const int64_t n = rows->kind == WMH_DENSE ? rows->n_rows * dim : rows->nnz;
     const size_t cm_bytes = sizeof(uint32_t) * (size_t)dim * n_scales;
     uint8_t *scr = nullptr;
-    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, cm_bytes + 16 * (size_t)n_scales + 4 * (size_t)n_scales + 256, s),
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, cm_bytes + 24 * (size_t)n_scales + 4 * (size_t)n_scales + 256, s),
                  "scale objective scratch");
     uint32_t *colmax = reinterpret_cast<uint32_t *>(scr);
     unsigned long long *num = reinterpret_cast<unsigned long long *>(scr + ((cm_bytes + 15) & ~(size_t)15));
     unsigned long long *den = num + n_scales;
-    float *dsc = reinterpret_cast<float *>(den + n_scales);
+    unsigned long long *clipped = den + n_scales;
+    float *dsc = reinterpret_cast<float *>(clipped + n_scales);
     st = WMH_OK;
     do {
-        if (cudaMemsetAsync(scr, 0, ((cm_bytes + 15) & ~(size_t)15) + 16 * (size_t)n_scales, s) != cudaSuccess ||
+        if (cudaMemsetAsync(scr, 0, ((cm_bytes + 15) & ~(size_t)15) + 24 * (size_t)n_scales, s) != cudaSuccess ||
             cudaMemcpyAsync(dsc, scales, sizeof(float) * n_scales, cudaMemcpyHostToDevice, s) != cudaSuccess) {
             st = cuda_fail(cudaGetLastError(), "scale objective setup");
             break;
@@ -120,20 +128,21 @@ extern "C" wmh_status wmh_scale_objective(const wmh_rows *rows, const float *sca
             const int64_t blocks = std::min<int64_t>((int64_t)num_sms() * 8, (n + 255) / 256);
             scale_objective_kernel<<<(unsigned)blocks, 256, 0, s>>>(
                 reinterpret_cast<const float *>(rows->kind == WMH_DENSE ? rows->dense : rows->val),
-                rows->kind == WMH_DENSE ? nullptr : rows->col, n, dim, dsc, n_scales, colmax, num);
+                rows->kind == WMH_DENSE ? nullptr : rows->col, n, dim, dsc, n_scales, colmax, num, clipped);
             count_launch();
             const int64_t bx = std::min<int64_t>(64, (dim + 255) / 256);
             sum_rows_kernel<<<dim3((unsigned)bx, (unsigned)n_scales), 256, 0, s>>>(colmax, dim, den);
             count_launch();
             if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "scale objective launch"); break; }
         }
-        unsigned long long h[2048];
-        cudaError_t e1 = cudaMemcpyAsync(h, num, 16 * (size_t)n_scales, cudaMemcpyDeviceToHost, s);
+        unsigned long long h[3072];
+        cudaError_t e1 = cudaMemcpyAsync(h, num, 24 * (size_t)n_scales, cudaMemcpyDeviceToHost, s);
         cudaError_t e2 = cudaStreamSynchronize(s);
         if (e1 != cudaSuccess || e2 != cudaSuccess) { st = cuda_fail(e1 != cudaSuccess ? e1 : e2, "scale objective readback"); break; }
         for (int a = 0; a < n_scales; a++) {
-            out[2 * a] = h[a];
-            out[2 * a + 1] = h[n_scales + a] * (uint64_t)rows->n_rows;
+            out[3 * a] = h[a];
+            out[3 * a + 1] = h[n_scales + a] * (uint64_t)rows->n_rows;
+            out[3 * a + 2] = h[2 * n_scales + a];
         }
     } while (0);
     cudaFreeAsync(scr, s);

@@ -89,5 +89,9 @@ def test_choose_scale_spec_examples():
     assert oracle.choose_scale(np.array([[0.5, 1.0]], np.float32), [3.0]) == 3.0
     xi = np.array([[1, 4, 0], [2, 2, 3]], np.float32)
     o = oracle.scale_objective(xi, [1, 2, 4])
-    assert Fraction(*o[0]) == Fraction(*o[1]) == Fraction(*o[2])
+    assert Fraction(*o[0][:2]) == Fraction(*o[1][:2]) == Fraction(*o[2][:2])
     assert oracle.choose_scale(xi, [4, 2, 1]) == 1.0
+    # a scale that would saturate a uint16 weight is not a candidate
+    big = np.array([[300.0, 1.0]], np.float32)
+    assert oracle.scale_objective(big, [256.0])[0][2] == 1
+    assert oracle.choose_scale(big, [1.0, 256.0]) == 1.0
