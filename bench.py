@@ -274,7 +274,7 @@ def main():
     quant = None
     if cfg.name == "c2r":
         xf = torch.from_numpy(data.x).to(dev)
-        grid = [1.0, 2.0, 4.0, 8.0, 16.0, 32.0, 64.0]
+        grid = [1.0, 2.0, 4.0, 8.0, 16.0]           # M (and the index) grow linearly with the scale
         scale = wmh.choose_scale(wmh.Rows.from_dense(xf), grid)
         xd = wmh.quantize(xf, scale)
         del xf
