@@ -198,10 +198,10 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     const bool tiny = (unsigned long long)rows->n_rows * k <= (1ull << 20);
     // The index kernel visits only the green draws (k*T*s per row); the tile
     // tests ~k/s draws per row, 4 rows per shared load.  Measured: CSR rows
-    // (c3, c4) 35-350x faster on the index; dense rows at mean s = 0.036 (c5)
-    // 1.17x faster on the index, at s = 0.050 (c2) 1.4x faster on the tile.
-    // Dense rows go to the index below mean s = 0.042 (prepare's statistics).
-    const bool sparse_dense = rows->kind == WMH_DENSE && L->mean_s >= 0.0 && L->mean_s < 0.042;
+    // (c3, c4) 35-350x faster on the index; dense rows at s = 0.05 (c2) 1.4x
+    // and at s = 0.036 (c5) 1.2x faster on the tile.  Dense rows go to the index
+    // only below mean s = 0.01 (prepare's statistics), where k/s tests dominate.
+    const bool sparse_dense = rows->kind == WMH_DENSE && L->mean_s >= 0.0 && L->mean_s < 0.01;
     // uint16 weights / bounds above 255 (fixed-point real data): index or simple
     const bool wide = (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(*rows) != 1;
     if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense || wide) && k <= 65536) {
@@ -336,7 +336,7 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_comp, E.ev_start, 0), "e2e wait");
     // the index kernel (AUTO's choice for CSR rows) files the draws once for the
     // whole call; every chunk then only runs its rows kernel
-    const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.042) ||
+    const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.01) ||
                             (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && k <= 65536 &&
                            (unsigned long long)h.n_rows * k > (1ull << 20);
     IndexBuilt ix;

@@ -46,16 +46,33 @@ struct CmParams {
     uint64_t S;
     int chunk;                   // 0 = auto (from the tile's effective sparsity)
     int vec_flush;               // k % 4 == 0 and sig aligned: 4-hash row stores
-    const uint2 *table;          // [k][T0] (c * Rp, off)
+    const uint32_t *table;       // [k][T0] packed draws (c * Rp) << 8 | nb, nb = 255 - off (0 at t >= cap)
     const uint32_t *pack;
     void *sig;
     unsigned long long *n_sat;
     unsigned long long *item_ctr;
 };
 
-__device__ __forceinline__ uint2 cm_late(const CmParams &p, uint64_t keyj, uint32_t t) {
-    const uint2 d = unpack_cell(cell_of(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m));
-    return make_uint2(d.x * (uint32_t)p.Rp, d.y);
+// A draw packed for the tile: (c * Rp) << 8 | nb with nb = 255 - (r - CompToM[c]),
+// and nb = 0 (never green: x + nb < 256) for t >= cap.  green(x) <=> x + nb >= 256
+// <=> x > nb ^ 0xFF.
+__device__ __forceinline__ uint32_t cm_pack(uint32_t r, const uint32_t *pack, uint32_t uni_m, uint32_t Rp, uint32_t t,
+                                            uint32_t cap) {
+    const uint2 d = unpack_cell(cell_of(r, pack, uni_m));
+    return ((d.x * Rp) << 8) | (t < cap ? 255u - d.y : 0u);
+}
+
+__device__ __forceinline__ uint32_t cm_late(const CmParams &p, uint64_t keyj, uint32_t t) {
+    return cm_pack(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m, (uint32_t)p.Rp, t, p.cap);
+}
+
+__global__ void cm_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
+                                const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t Rp, uint32_t cap) {
+    const int64_t total = (int64_t)k * T0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
+        table[i] = cm_pack(draw_r(S, j, t, M), pack, uni_m, Rp, t, cap);
+    }
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -67,37 +84,36 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 // Rounds 1.. over the pending list: lane = row, C draws per re-queue;
 // results to the warp's shared row hres[].
 template <int C>
-__device__ __forceinline__ int cm_rounds(const CmParams &p, const uint2 *buf, uint2 *win, const uint8_t *xs,
+__device__ __forceinline__ int cm_rounds(const CmParams &p, const uint32_t *buf, uint32_t *win, const uint8_t *xs,
                                          uint64_t keyj, uint16_t *hres, const uint16_t *&cur, uint16_t *own0,
                                          uint16_t *own1, int npend, uint32_t *q_io) {
     const int lane = threadIdx.x & 31;
     uint32_t q = *q_io;
     int flip = 0;
     while (npend > CM_STRAG && q * 32 < p.cap) {
-        const uint2 *src;
+        const uint32_t *src;
         if (q * 32 < (uint32_t)T0) {
             src = buf + q * 32;
         } else {
-            const uint2 d = cm_late(p, keyj, q * 32 + lane);
+            const uint32_t d = cm_late(p, keyj, q * 32 + lane);
             __syncwarp();
             win[lane] = d;
             __syncwarp();
             src = win;
         }
-        const bool cap_round = q * 32 + 32 > p.cap;
 #pragma unroll
         for (int sub = 0; sub < 32 / C; sub++) {
             if (npend == 0) break;
             uint32_t dc[C], doff[C];
 #pragma unroll
-            for (int i = 0; i < C / 2; i++) {
+            for (int i = 0; i < C / 4; i++) {          // four packed draws per 16-byte load
                 const uint4 v = reinterpret_cast<const uint4 *>(src + sub * C)[i];
-                dc[2 * i] = v.x; doff[2 * i] = v.y; dc[2 * i + 1] = v.z; doff[2 * i + 1] = v.w;
-            }
-            if (cap_round) {
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int tt = 0; tt < C; tt++)
-                    if (q * 32 + sub * C + tt >= p.cap) doff[tt] = 0xFFFFFFFFu;
+                for (int u = 0; u < 4; u++) {
+                    dc[4 * i + u] = w4[u] >> 8;
+                    doff[4 * i + u] = (w4[u] & 0xFFu) ^ 0xFFu;   // off (255 at t >= cap: never green)
+                }
             }
             uint16_t *nxt = flip ? own1 : own0;
             flip ^= 1;
@@ -145,10 +161,9 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     const int Rp = p.Rp;
     uint8_t *xs = reinterpret_cast<uint8_t *>(smem);                               // [D][Rp]
     const size_t xs_bytes = ((size_t)p.D * Rp + 15) & ~(size_t)15;
-    uint2 *sbuf_all = reinterpret_cast<uint2 *>(xs + xs_bytes);                     // [NW][T0]
-    uint2 *swin_all = sbuf_all + CM_NW * T0;                                        // [NW][32]
-    uint4 *sr0_all = reinterpret_cast<uint4 *>(swin_all + CM_NW * 32);              // [NW][64] SWAR-round consts
-    uint32_t *spart_all = reinterpret_cast<uint32_t *>(sr0_all + CM_NW * 64);       // [NW][32] partial h4
+    uint32_t *sbuf_all = reinterpret_cast<uint32_t *>(xs + xs_bytes);               // [NW][T0] packed draws
+    uint32_t *swin_all = sbuf_all + CM_NW * T0;                                     // [NW][32]
+    uint32_t *spart_all = swin_all + CM_NW * 32;                                    // [NW][32] partial h4
     uint16_t *hres_all = reinterpret_cast<uint16_t *>(spart_all + CM_NW * 32);      // [NW][HB][R] results
     uint16_t *spend_all = hres_all + CM_NW * CM_HB * R;                             // [NW][2][R]
     uint8_t *sflag4 = reinterpret_cast<uint8_t *>(spend_all + CM_NW * 2 * R);       // [NWD] live-row nibbles
@@ -157,9 +172,8 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     __shared__ unsigned long long s_xsum;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint2 *sbuf = sbuf_all + warp * T0;
-    uint2 *swin = swin_all + warp * 32;
-    uint4 *sr0 = sr0_all + warp * 64;
+    uint32_t *sbuf = sbuf_all + warp * T0;
+    uint32_t *swin = swin_all + warp * 32;
     uint32_t *spart = spart_all + warp * 32;
     uint16_t *hres_blk = hres_all + warp * CM_HB * R;                              // [HB][R]
     uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
@@ -250,48 +264,47 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
         uint32_t je = min(j1, jb + CM_HB);
         uint32_t jb_next = jb < j1 ? grab() : j1;      // next block's first hash
         uint32_t j = jb;
-        uint4 pre[4];
+        uint4 pre[2];                                  // T0 packed draws = 2 x 16 B per lane
         if (j < j1) {
             const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0);
 #pragma unroll
-            for (int i = 0; i < 4; i++) pre[i] = __ldg(t4 + 32 * i + lane);
+            for (int i = 0; i < 2; i++) pre[i] = __ldg(t4 + 32 * i + lane);
         }
         while (j < j1) {
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 4; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
+            for (int i = 0; i < 2; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
             __syncwarp();
             const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
             uint16_t *hres = hres_blk + (j - jb) * R;
             if (jn < j1) {
                 const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0);
 #pragma unroll
-                for (int i = 0; i < 4; i++) pre[i] = __ldg(t4 + 32 * i + lane);
+                for (int i = 0; i < 2; i++) pre[i] = __ldg(t4 + 32 * i + lane);
             }
             const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
 
-            // ---- SWAR rounds (draws 0..32*NR0-1): lane = (4-row word, part) ---------
-#pragma unroll
-            for (int r0 = 0; r0 < NR0; r0++) {
-                const uint32_t t = 32u * r0 + lane;
-                const uint2 d = sbuf[t];
-                const uint32_t nb = t < p.cap ? 255u - d.y : 0u;                // t >= cap: never green
-                sr0[t] = make_uint4(d.x, (nb & 0x7Fu) * 0x01010101u, nb * 0x01010101u, 0u);
-            }
-            __syncwarp();
+            // ---- SWAR rounds (draws 0..32*NR0-1): lane = (4-row word, part); four
+            //      packed draws per 16-byte shared load, B = nb in every byte, K = B & 0x7F
             const int w = lane % NWD, part = lane / NWD;
             uint32_t h4 = 0xFFFFFFFFu;                 // per byte: first green draw within the part
             {
-                const uint4 *e = sr0 + part * PD;
+                const uint4 *e4 = reinterpret_cast<const uint4 *>(sbuf + part * PD);
                 const uint8_t *xw = xs + 4 * w;
 #pragma unroll
-                for (int i = PD - 1; i >= 0; i--) {
-                    const uint4 ei = e[i];
-                    const uint32_t a = *reinterpret_cast<const uint32_t *>(xw + ei.x);
-                    const uint32_t s = (a & 0x7F7F7F7Fu) + ei.y;
-                    const uint32_t g = (a & ei.z) | (a & s) | (ei.z & s);       // carry out of bit 7 (MAJ)
-                    const uint32_t m = prmt(g, 0u, 0xBA98);                    // msb -> whole byte
-                    h4 = (h4 & ~m) | ((uint32_t)(part * PD + i) * 0x01010101u & m);
+                for (int i4 = PD / 4 - 1; i4 >= 0; i4--) {
+                    const uint4 q4 = e4[i4];
+                    const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                    for (int u = 3; u >= 0; u--) {
+                        const uint32_t pw = w4[u];
+                        const uint32_t B = prmt(pw, 0u, 0x0000);                // nb in every byte
+                        const uint32_t a = *reinterpret_cast<const uint32_t *>(xw + (pw >> 8));
+                        const uint32_t s = (a & 0x7F7F7F7Fu) + (B & 0x7F7F7F7Fu);
+                        const uint32_t g = (a & B) | (a & s) | (B & s);          // carry out of bit 7 (MAJ)
+                        const uint32_t m = prmt(g, 0u, 0xBA98);                 // msb -> whole byte
+                        h4 = (h4 & ~m) | ((uint32_t)(part * PD + 4 * i4 + u) * 0x01010101u & m);
+                    }
                 }
             }
             if (P > 1) {                                // first part with a green wins, per byte
@@ -362,12 +375,12 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
                 }
                 for (; live && q * 32 < p.cap; q++) {
                     const uint32_t t = q * 32 + lane;
-                    const uint2 d = t < (uint32_t)T0 ? sbuf[t] : cm_late(p, keyj, t);
-                    const uint32_t off = t < p.cap ? d.y : 0xFFFFFFFFu;
+                    const uint32_t pw = t < (uint32_t)T0 ? sbuf[t] : cm_late(p, keyj, t);
+                    const uint32_t off = (pw & 0xFFu) ^ 0xFFu, dcol = pw >> 8;
 #pragma unroll
                     for (int i = 0; i < CM_STRAG; i++) {
                         if (live & (1u << i)) {
-                            const uint32_t xv = xs[d.x + rr[i]];
+                            const uint32_t xv = xs[dcol + rr[i]];
                             const unsigned gm = __ballot_sync(0xFFFFFFFFu, xv > off);
                             if (gm) {
                                 if (lane == 0) hres[rr[i]] = (uint16_t)(q * 32 + __ffs(gm));
@@ -429,15 +442,17 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
 }
 
 static size_t cm_smem(int D, int R, int Rp) {
-    return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 8 + (size_t)CM_NW * 64 * 16 +
+    return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 4 +
            (size_t)CM_NW * 32 * 4 + (size_t)CM_NW * CM_HB * R * 2 + (size_t)CM_NW * 2 * R * 2 + (size_t)(R / 4) + 16;
 }
 
 template <int SIGB, int P>
 static void cm_launch(const CmParams &p, size_t smem, int grid, cudaStream_t s) {
-    // SWAR rounds before the pending-list rounds: 2 (draws 0..63, ~96% of the
-    // rows resolved at s = 0.05) unless WMH_CM_SWAR_ROUNDS=1
-    static const int nr0 = getenv("WMH_CM_SWAR_ROUNDS") && atoi(getenv("WMH_CM_SWAR_ROUNDS")) == 1 ? 1 : 2;
+    // SWAR rounds before the pending-list rounds: measured best 1 for the
+    // 128-row tile (c2: 0.609 vs 0.630 ms) and 2 for the 32-row tile (c5:
+    // 5.39 vs 6.41 ms per 262,144 rows); WMH_CM_SWAR_ROUNDS overrides
+    static const int env_nr0 = getenv("WMH_CM_SWAR_ROUNDS") ? atoi(getenv("WMH_CM_SWAR_ROUNDS")) : 0;
+    const int nr0 = env_nr0 == 1 || env_nr0 == 2 ? env_nr0 : (P == 1 ? 1 : 2);
     auto kern = nr0 == 1 ? hash_tiled_cm_kernel<SIGB, P, 1> : hash_tiled_cm_kernel<SIGB, P, 2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel_timer_begin(s);
@@ -474,15 +489,20 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
 
     uint8_t *scratch = nullptr;
-    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint2);
+    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint32_t);
     WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "tiled scratch alloc");
-    uint2 *table = reinterpret_cast<uint2 *>(scratch);
+    uint32_t *table = reinterpret_cast<uint32_t *>(scratch);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "tiled counter memset");
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
     const uint32_t M = (uint32_t)a.L->M;
-    wmh_status st = launch_draw_table(table, a.k, a.S, M, a.L->cell_pack, uni_m, (uint32_t)Rp, a.stream);
-    if (st != WMH_OK) { cudaFreeAsync(scratch, a.stream); return st; }
+    {
+        const int64_t total = (int64_t)a.k * T0;
+        const int blocks = (int)min((int64_t)num_sms() * 8, (total + 255) / 256);
+        cm_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, M, a.L->cell_pack, uni_m, (uint32_t)Rp, a.cap);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(scratch, a.stream); return cuda_fail(cudaGetLastError(), "cm table launch"); }
+    }
 
     CmParams p;
     p.x = a.rows.dense;
