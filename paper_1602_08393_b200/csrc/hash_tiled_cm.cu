@@ -66,13 +66,34 @@ __device__ __forceinline__ uint32_t cm_late(const CmParams &p, uint64_t keyj, ui
     return cm_pack(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m, (uint32_t)p.Rp, t, p.cap);
 }
 
+// TW = 1: one packed word per draw; TW = 2: (c * Rp, nb in every byte) -- the
+// SWAR constant B ready, two fewer ALU ops per draw-word test for twice the
+// shared-load bytes (the 128-row tile is ALU-bound, the 32-row tile load-bound)
+template <int TW>
+__device__ __forceinline__ void cm_put(uint32_t *dst, uint32_t pw) {
+    if (TW == 1) dst[0] = pw;
+    else *reinterpret_cast<uint2 *>(dst) = make_uint2(pw >> 8, (pw & 0xFFu) * 0x01010101u);
+}
+
+template <int TW>
 __global__ void cm_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
                                 const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t Rp, uint32_t cap) {
     const int64_t total = (int64_t)k * T0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
-        table[i] = cm_pack(draw_r(S, j, t, M), pack, uni_m, Rp, t, cap);
+        cm_put<TW>(table + i * TW, cm_pack(draw_r(S, j, t, M), pack, uni_m, Rp, t, cap));
     }
+}
+
+// column offset and off of draw t from a TW-word table
+template <int TW>
+__device__ __forceinline__ uint2 cm_get(const uint32_t *buf, uint32_t t) {
+    if (TW == 1) {
+        const uint32_t pw = buf[t];
+        return make_uint2(pw >> 8, (pw & 0xFFu) ^ 0xFFu);
+    }
+    const uint2 d = *reinterpret_cast<const uint2 *>(buf + 2 * t);
+    return make_uint2(d.x, (d.y & 0xFFu) ^ 0xFFu);
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -83,7 +104,7 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 
 // Rounds 1.. over the pending list: lane = row, C draws per re-queue;
 // results to the warp's shared row hres[].
-template <int C>
+template <int C, int TW>
 __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint32_t *buf, uint32_t *win, const uint8_t *xs,
                                          uint64_t keyj, uint16_t *hres, const uint16_t *&cur, uint16_t *own0,
                                          uint16_t *own1, int npend, uint32_t *q_io) {
@@ -93,11 +114,11 @@ __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint32_t *buf,
     while (npend > CM_STRAG && q * 32 < p.cap) {
         const uint32_t *src;
         if (q * 32 < (uint32_t)T0) {
-            src = buf + q * 32;
+            src = buf + q * 32 * TW;
         } else {
             const uint32_t d = cm_late(p, keyj, q * 32 + lane);
             __syncwarp();
-            win[lane] = d;
+            cm_put<TW>(win + lane * TW, d);
             __syncwarp();
             src = win;
         }
@@ -106,13 +127,21 @@ __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint32_t *buf,
             if (npend == 0) break;
             uint32_t dc[C], doff[C];
 #pragma unroll
-            for (int i = 0; i < C / 4; i++) {          // four packed draws per 16-byte load
-                const uint4 v = reinterpret_cast<const uint4 *>(src + sub * C)[i];
+            for (int i = 0; i < C * TW / 4; i++) {     // 16-byte loads: four (TW = 1) or two draws
+                const uint4 v = reinterpret_cast<const uint4 *>(src + sub * C * TW)[i];
                 const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                if (TW == 1) {
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    dc[4 * i + u] = w4[u] >> 8;
-                    doff[4 * i + u] = (w4[u] & 0xFFu) ^ 0xFFu;   // off (255 at t >= cap: never green)
+                    for (int u = 0; u < 4; u++) {
+                        dc[4 * i + u] = w4[u] >> 8;
+                        doff[4 * i + u] = (w4[u] & 0xFFu) ^ 0xFFu;   // off (255 at t >= cap: never green)
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        dc[2 * i + u] = w4[2 * u];
+                        doff[2 * i + u] = (w4[2 * u + 1] & 0xFFu) ^ 0xFFu;
+                    }
                 }
             }
             uint16_t *nxt = flip ? own1 : own0;
@@ -153,7 +182,7 @@ __device__ __forceinline__ int cm_rounds(const CmParams &p, const uint32_t *buf,
     return npend;
 }
 
-template <int SIGB, int P, int NR0>
+template <int SIGB, int P, int NR0, int TW>
 __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams p) {
     // rows, 4-row words (NWD * P == 32), draws per part of the NR0 SWAR rounds
     constexpr int R = 128 / P, NWD = R / 4, PD = 32 * NR0 / P;
@@ -161,9 +190,9 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     const int Rp = p.Rp;
     uint8_t *xs = reinterpret_cast<uint8_t *>(smem);                               // [D][Rp]
     const size_t xs_bytes = ((size_t)p.D * Rp + 15) & ~(size_t)15;
-    uint32_t *sbuf_all = reinterpret_cast<uint32_t *>(xs + xs_bytes);               // [NW][T0] packed draws
-    uint32_t *swin_all = sbuf_all + CM_NW * T0;                                     // [NW][32]
-    uint32_t *spart_all = swin_all + CM_NW * 32;                                    // [NW][32] partial h4
+    uint32_t *sbuf_all = reinterpret_cast<uint32_t *>(xs + xs_bytes);               // [NW][T0][TW] draws
+    uint32_t *swin_all = sbuf_all + CM_NW * T0 * TW;                                // [NW][32][TW]
+    uint32_t *spart_all = swin_all + CM_NW * 32 * TW;                               // [NW][32] partial h4
     uint16_t *hres_all = reinterpret_cast<uint16_t *>(spart_all + CM_NW * 32);      // [NW][HB][R] results
     uint16_t *spend_all = hres_all + CM_NW * CM_HB * R;                             // [NW][2][R]
     uint8_t *sflag4 = reinterpret_cast<uint8_t *>(spend_all + CM_NW * 2 * R);       // [NWD] live-row nibbles
@@ -172,8 +201,8 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     __shared__ unsigned long long s_xsum;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t *sbuf = sbuf_all + warp * T0;
-    uint32_t *swin = swin_all + warp * 32;
+    uint32_t *sbuf = sbuf_all + warp * T0 * TW;
+    uint32_t *swin = swin_all + warp * 32 * TW;
     uint32_t *spart = spart_all + warp * 32;
     uint16_t *hres_blk = hres_all + warp * CM_HB * R;                              // [HB][R]
     uint16_t *own0 = spend_all + warp * 2 * R, *own1 = own0 + R;
@@ -264,23 +293,23 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
         uint32_t je = min(j1, jb + CM_HB);
         uint32_t jb_next = jb < j1 ? grab() : j1;      // next block's first hash
         uint32_t j = jb;
-        uint4 pre[2];                                  // T0 packed draws = 2 x 16 B per lane
+        uint4 pre[2 * TW];                             // T0 draws = 2 * TW x 16 B per lane
         if (j < j1) {
-            const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0);
+            const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)j * T0 * TW);
 #pragma unroll
-            for (int i = 0; i < 2; i++) pre[i] = __ldg(t4 + 32 * i + lane);
+            for (int i = 0; i < 2 * TW; i++) pre[i] = __ldg(t4 + 32 * i + lane);
         }
         while (j < j1) {
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 2; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
+            for (int i = 0; i < 2 * TW; i++) reinterpret_cast<uint4 *>(sbuf)[32 * i + lane] = pre[i];
             __syncwarp();
             const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
             uint16_t *hres = hres_blk + (j - jb) * R;
             if (jn < j1) {
-                const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0);
+                const uint4 *t4 = reinterpret_cast<const uint4 *>(p.table + (int64_t)jn * T0 * TW);
 #pragma unroll
-                for (int i = 0; i < 2; i++) pre[i] = __ldg(t4 + 32 * i + lane);
+                for (int i = 0; i < 2 * TW; i++) pre[i] = __ldg(t4 + 32 * i + lane);
             }
             const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
 
@@ -289,21 +318,28 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             const int w = lane % NWD, part = lane / NWD;
             uint32_t h4 = 0xFFFFFFFFu;                 // per byte: first green draw within the part
             {
-                const uint4 *e4 = reinterpret_cast<const uint4 *>(sbuf + part * PD);
+                const uint4 *e4 = reinterpret_cast<const uint4 *>(sbuf + part * PD * TW);
                 const uint8_t *xw = xs + 4 * w;
+                constexpr int PER = 4 / TW;            // draws per 16-byte load
 #pragma unroll
-                for (int i4 = PD / 4 - 1; i4 >= 0; i4--) {
+                for (int i4 = PD / PER - 1; i4 >= 0; i4--) {
                     const uint4 q4 = e4[i4];
                     const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-                    for (int u = 3; u >= 0; u--) {
-                        const uint32_t pw = w4[u];
-                        const uint32_t B = prmt(pw, 0u, 0x0000);                // nb in every byte
-                        const uint32_t a = *reinterpret_cast<const uint32_t *>(xw + (pw >> 8));
+                    for (int u = PER - 1; u >= 0; u--) {
+                        uint32_t col, B;
+                        if (TW == 1) {
+                            col = w4[u] >> 8;
+                            B = prmt(w4[u], 0u, 0x0000);                        // nb in every byte
+                        } else {
+                            col = w4[2 * u];
+                            B = w4[2 * u + 1];
+                        }
+                        const uint32_t a = *reinterpret_cast<const uint32_t *>(xw + col);
                         const uint32_t s = (a & 0x7F7F7F7Fu) + (B & 0x7F7F7F7Fu);
                         const uint32_t g = (a & B) | (a & s) | (B & s);          // carry out of bit 7 (MAJ)
                         const uint32_t m = prmt(g, 0u, 0xBA98);                 // msb -> whole byte
-                        h4 = (h4 & ~m) | ((uint32_t)(part * PD + 4 * i4 + u) * 0x01010101u & m);
+                        h4 = (h4 & ~m) | ((uint32_t)(part * PD + PER * i4 + u) * 0x01010101u & m);
                     }
                 }
             }
@@ -354,9 +390,9 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
             const uint16_t *cur = own1;
             uint32_t q = NR0;
             switch (C) {
-                case 8: npend = cm_rounds<8>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
-                case 16: npend = cm_rounds<16>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
-                default: npend = cm_rounds<32>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
+                case 8: npend = cm_rounds<8, TW>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
+                case 16: npend = cm_rounds<16, TW>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
+                default: npend = cm_rounds<32, TW>(p, sbuf, swin, xs, keyj, hres, cur, own0, own1, npend, &q); break;
             }
             if (npend > 0 && q * 32 >= p.cap) {        // a9: no green draw before the cap
                 for (int i = lane; i < npend; i += 32) {
@@ -375,8 +411,13 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
                 }
                 for (; live && q * 32 < p.cap; q++) {
                     const uint32_t t = q * 32 + lane;
-                    const uint32_t pw = t < (uint32_t)T0 ? sbuf[t] : cm_late(p, keyj, t);
-                    const uint32_t off = (pw & 0xFFu) ^ 0xFFu, dcol = pw >> 8;
+                    uint2 dd;
+                    if (t < (uint32_t)T0) dd = cm_get<TW>(sbuf, t);
+                    else {
+                        const uint32_t pw = cm_late(p, keyj, t);
+                        dd = make_uint2(pw >> 8, (pw & 0xFFu) ^ 0xFFu);
+                    }
+                    const uint32_t off = dd.y, dcol = dd.x;
 #pragma unroll
                     for (int i = 0; i < CM_STRAG; i++) {
                         if (live & (1u << i)) {
@@ -441,19 +482,19 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
     }
 }
 
-static size_t cm_smem(int D, int R, int Rp) {
-    return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 4 +
+static size_t cm_smem(int D, int R, int Rp, int TW) {
+    return (((size_t)D * Rp + 15) & ~(size_t)15) + (size_t)CM_NW * (T0 + 32) * 4 * TW +
            (size_t)CM_NW * 32 * 4 + (size_t)CM_NW * CM_HB * R * 2 + (size_t)CM_NW * 2 * R * 2 + (size_t)(R / 4) + 16;
 }
 
-template <int SIGB, int P>
+template <int SIGB, int P, int TW>
 static void cm_launch(const CmParams &p, size_t smem, int grid, cudaStream_t s) {
     // SWAR rounds before the pending-list rounds: measured best 1 for the
     // 128-row tile (c2: 0.609 vs 0.630 ms) and 2 for the 32-row tile (c5:
     // 5.39 vs 6.41 ms per 262,144 rows); WMH_CM_SWAR_ROUNDS overrides
     static const int env_nr0 = getenv("WMH_CM_SWAR_ROUNDS") ? atoi(getenv("WMH_CM_SWAR_ROUNDS")) : 0;
     const int nr0 = env_nr0 == 1 || env_nr0 == 2 ? env_nr0 : (P == 1 ? 1 : 2);
-    auto kern = nr0 == 1 ? hash_tiled_cm_kernel<SIGB, P, 1> : hash_tiled_cm_kernel<SIGB, P, 2>;
+    auto kern = nr0 == 1 ? hash_tiled_cm_kernel<SIGB, P, 1, TW> : hash_tiled_cm_kernel<SIGB, P, 2, TW>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel_timer_begin(s);
     kern<<<grid, CM_NT, smem, s>>>(p);
@@ -470,14 +511,18 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     // rows per tile R = 128 / P; column stride Rp = R + 4 (Rp/4 odd: draw-
     // parallel accesses to random columns spread over the banks)
-    int P = 1, R = 0, Rp = 0;
+    // draw-table words per draw: 1 (packed; measured: c2 0.612 vs 0.623 ms with
+    // 2 words, c5 slice 5.41 vs 5.82 ms); WMH_CM_TW=2 selects the (c*Rp, B) pairs
+    static const int tw_env = getenv("WMH_CM_TW") ? atoi(getenv("WMH_CM_TW")) : 0;
+    int P = 1, R = 0, Rp = 0, TW = 1;
     for (; P <= 4; P *= 2) {
         R = 128 / P;
         Rp = R + 4;
-        if (cm_smem(D, R, Rp) <= (size_t)smem_optin) break;
+        TW = tw_env == 2 ? 2 : 1;
+        if (cm_smem(D, R, Rp, TW) <= (size_t)smem_optin) break;
     }
     if (P > 4) return WMH_OK;
-    const size_t smem = cm_smem(D, R, Rp);
+    const size_t smem = cm_smem(D, R, Rp, TW);
     *handled = true;
 
     const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
@@ -489,7 +534,7 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
 
     uint8_t *scratch = nullptr;
-    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint32_t);
+    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint32_t) * TW;
     WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "tiled scratch alloc");
     uint32_t *table = reinterpret_cast<uint32_t *>(scratch);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
@@ -499,7 +544,8 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     {
         const int64_t total = (int64_t)a.k * T0;
         const int blocks = (int)min((int64_t)num_sms() * 8, (total + 255) / 256);
-        cm_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, M, a.L->cell_pack, uni_m, (uint32_t)Rp, a.cap);
+        if (TW == 2) cm_table_kernel<2><<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, M, a.L->cell_pack, uni_m, (uint32_t)Rp, a.cap);
+        else cm_table_kernel<1><<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, M, a.L->cell_pack, uni_m, (uint32_t)Rp, a.cap);
         count_launch();
         if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(scratch, a.stream); return cuda_fail(cudaGetLastError(), "cm table launch"); }
     }
@@ -531,19 +577,25 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     p.n_sat = a.n_sat;
     p.item_ctr = ctr;
     const int grid = (int)min((int64_t)sms, p.n_items);
-    if (a.sig_bytes == 1) {
-        if (P == 1) cm_launch<1, 1>(p, smem, grid, a.stream);
-        else if (P == 2) cm_launch<1, 2>(p, smem, grid, a.stream);
-        else cm_launch<1, 4>(p, smem, grid, a.stream);
-    } else {
-        if (P == 1) cm_launch<2, 1>(p, smem, grid, a.stream);
-        else if (P == 2) cm_launch<2, 2>(p, smem, grid, a.stream);
-        else cm_launch<2, 4>(p, smem, grid, a.stream);
-    }
+#define WMH_CM_GO(SB)                                                        \
+    do {                                                                     \
+        if (TW == 2) {                                                       \
+            if (P == 1) cm_launch<SB, 1, 2>(p, smem, grid, a.stream);        \
+            else if (P == 2) cm_launch<SB, 2, 2>(p, smem, grid, a.stream);   \
+            else cm_launch<SB, 4, 2>(p, smem, grid, a.stream);               \
+        } else {                                                             \
+            if (P == 1) cm_launch<SB, 1, 1>(p, smem, grid, a.stream);        \
+            else if (P == 2) cm_launch<SB, 2, 1>(p, smem, grid, a.stream);   \
+            else cm_launch<SB, 4, 1>(p, smem, grid, a.stream);               \
+        }                                                                    \
+    } while (0)
+    if (a.sig_bytes == 1) WMH_CM_GO(1);
+    else WMH_CM_GO(2);
+#undef WMH_CM_GO
     WMH_LAUNCH_CHECK("hash_tiled_cm launch");
     if (getenv("WMH_TILED_STATS"))
-        fprintf(stderr, "[wmh tiled cm] R=%d Rp=%d P=%d grid=%d items=%lld hchunk=%d smem=%zu\n", R, Rp, P, grid,
-                (long long)p.n_items, hchunk, smem);
+        fprintf(stderr, "[wmh tiled cm] R=%d Rp=%d P=%d TW=%d grid=%d items=%lld hchunk=%d smem=%zu\n", R, Rp, P, TW,
+                grid, (long long)p.n_items, hchunk, smem);
     cudaFreeAsync(scratch, a.stream);
     return WMH_OK;
 }
