@@ -471,10 +471,12 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
                         for (int u = 0; u < IX_U; u++) {
                             const uint32_t bu = base + 32u * u;
                             const uint32_t d = rp[o + 1 + lane] - bu;     // padded with FULL past nr
-                            const uint32_t m = __reduce_or_sync(FULL, d < 32 ? (1u << d) : 0u);
+                            uint32_t bit;                              // 1 << d, 0 for d >= 32 (PTX shl clamps)
+                            asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(d));
+                            const uint32_t m = __reduce_or_sync(FULL, bit);   // uniform
                             const uint32_t own = o + __popc(m & lanemask_le);
                             addr[u] = ra[own] + (bu + lane - rp[own]);
-                            o = __shfl_sync(FULL, own, 31);
+                            o += __popc(m);                            // the owner of the next window's base
                         }
                         uint32_t v[IX_U];
 #pragma unroll
