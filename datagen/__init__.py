@@ -391,6 +391,36 @@ def make(name: str, n_rows: int | None = None, dim: int | None = None):
     return cfg, data
 
 
+def fig2_pairs(dim: int = 64, seed: int = 2016):
+    """Nine pairs (x_j, y_j) with generalized Jaccard exactly j/10, j = 1..9 --
+    SPEC's stand-in for Figure 2's unnamed pairs: a shared
+    block with total 20j (x = y there), an x-only and a y-only block with total
+    10(10 - j) each, the totals split over 16 coordinates per block by a seeded
+    integer partition.  Returns (x [9, dim] uint8, y [9, dim] uint8, [j/10])."""
+    assert dim >= 48
+    rng = np.random.default_rng(seed)
+
+    def split(total, n):
+        cuts = np.sort(rng.choice(np.arange(1, total), size=min(n, total) - 1, replace=False))
+        parts = np.diff(np.concatenate([[0], cuts, [total]]))
+        out = np.zeros(n, np.int64)
+        out[:len(parts)] = parts
+        rng.shuffle(out)
+        return out
+
+    x = np.zeros((9, dim), np.uint8)
+    y = np.zeros((9, dim), np.uint8)
+    for j in range(1, 10):
+        perm = rng.permutation(dim)
+        sh, xo, yo = perm[:16], perm[16:32], perm[32:48]
+        w = split(20 * j, 16)
+        x[j - 1, sh] = w
+        y[j - 1, sh] = w
+        x[j - 1, xo] = split(10 * (10 - j), 16)
+        y[j - 1, yo] = split(10 * (10 - j), 16)
+    return x, y, [j / 10 for j in range(1, 10)]
+
+
 def random_pairs(seed: int, n_rows: int, n_pairs: int) -> np.ndarray:
     """Uniform random (a, b) row pairs, a != b, int64 [P, 2]."""
     rng = np.random.Generator(np.random.PCG64([seed, 0xC011]))
