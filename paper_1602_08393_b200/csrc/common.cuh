@@ -139,7 +139,7 @@ struct IxEpochs {
 };
 struct IndexBuilt {
     uint8_t *scr = nullptr;
-    uint32_t *pos = nullptr, *vals = nullptr;
+    uint32_t *pos = nullptr, *vals = nullptr, *colstart = nullptr;
     uint2 *table = nullptr;
     unsigned long long *ctr = nullptr;
     IxEpochs ep{};

@@ -178,6 +178,19 @@ __global__ void __launch_bounds__(SC_T) ix_chunk_sort(const IxBuild b, const uin
     }
 }
 
+// colstart[e * (D + 1) + c] = pos[e * M + CompToM[c]]: the first filed draw of
+// column c in epoch e, so a row reads one of its two range bounds from a
+// D-sized (L2-resident) array instead of the E*M-sized pos.
+__global__ void ix_colstart_kernel(const uint32_t *__restrict__ pos, const uint32_t *__restrict__ c2m, uint32_t uni_m,
+                                   int E, uint32_t M, int64_t D, uint32_t *__restrict__ colstart) {
+    const int64_t total = (int64_t)E * (D + 1);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = i / (D + 1), c = i - e * (D + 1);
+        const uint32_t lo = uni_m ? (uint32_t)c * uni_m : __ldg(c2m + c);
+        colstart[i] = pos[(uint64_t)e * M + lo];
+    }
+}
+
 // In-place inclusive scan of uint32 a[0..n): tile sums, a one-block scan of
 // the sums, per-tile scans with the carried offset.
 __global__ void __launch_bounds__(SC_T) scan_tile_sums(const uint32_t *__restrict__ a, int64_t n,
@@ -244,6 +257,7 @@ struct IxParams {
     const uint32_t *comp_to_m, *pack, *i2c;   // pack = null for wide layouts
     uint32_t uni_m, M;
     const uint32_t *pos, *vals;
+    const uint32_t *colstart;    // [E][D + 1]: pos[e*M + CompToM[c]]
     const uint2 *table;          // (c, r - CompToM[c]) of draws t < T0 of every hash
     IxEpochs ep;
     uint64_t S;
@@ -399,6 +413,7 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
             const int e = ix_plan(p, s, CSR ? (staged ? p.cf_smem : p.cf_global) : p.cf_dense);
             const uint32_t T = p.ep.B[e + 1];
             const uint32_t *pe = p.pos + (uint64_t)e * p.M;
+            const uint32_t *ce = p.colstart + (uint64_t)e * (p.D + 1);
             for (int b0 = 0; b0 < n; b0 += CAPR) {
                 // ---- (1) ranges of this thread's 8 coordinates
                 const int i0 = b0 + threadIdx.x * ITEMS;
@@ -426,7 +441,9 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
                 uint32_t a[ITEMS], len[ITEMS];
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++) {
-                    a[q] = xv[q] ? __ldg(pe + lo[q]) : 0u;
+                    // uniform bounds: the column start from the small colstart table
+                    // (c = lo / m), else pos at the cell itself
+                    a[q] = xv[q] ? __ldg(p.uni_m ? ce + lo[q] / p.uni_m : pe + lo[q]) : 0u;
                     len[q] = xv[q] ? __ldg(pe + lo[q] + xv[q]) : 0u;
                 }
                 uint32_t cnt = 0, sum = 0;
@@ -618,6 +635,7 @@ static wmh_status ix_launch(IxParams p, cudaStream_t s) {
 template <int SIGB, bool CSR, typename W>
 static wmh_status ix_launch_nw(const IxParams &p, int nw, cudaStream_t s) {
     switch (nw) {
+        case 1: return ix_launch<SIGB, CSR, 1, W>(p, s);
         case 2: return ix_launch<SIGB, CSR, 2, W>(p, s);
         case 4: return ix_launch<SIGB, CSR, 4, W>(p, s);
         default: return ix_launch<SIGB, CSR, 8, W>(p, s);
@@ -709,9 +727,10 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
     const int64_t nt = (int64_t)((n_h + SC_TILE - 1) / SC_TILE);
     auto al = [](uint64_t v) { return (v + 255) & ~(uint64_t)255; };
     const uint64_t pos_b = al((b.n_keys + 1) * 4), vals_b = al(n_inst * 4), tmp_b = al(n_inst * 4),
-                   h_b = al(n_h * 4), sums_b = al((uint64_t)nt * 4 + 4), tab_b = al((uint64_t)a.k * T0 * 8);
+                   h_b = al(n_h * 4), sums_b = al((uint64_t)nt * 4 + 4), tab_b = al((uint64_t)a.k * T0 * 8),
+                   cs_b = (L->flags & WMH_LAYOUT_UNIFORM) ? al((uint64_t)ep.E * (L->dim + 1) * 4) : 0;
     uint8_t *scr = nullptr;
-    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, pos_b + vals_b + tmp_b + h_b + sums_b + tab_b + 256, a.stream),
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, pos_b + vals_b + tmp_b + h_b + sums_b + tab_b + cs_b + 256, a.stream),
                  "index alloc");
     uint32_t *pos = reinterpret_cast<uint32_t *>(scr);
     uint32_t *vals = reinterpret_cast<uint32_t *>(scr + pos_b);
@@ -719,7 +738,8 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
     uint32_t *H = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b + tmp_b);
     uint32_t *sums = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b + tmp_b + h_b);
     uint2 *table = reinterpret_cast<uint2 *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b);
-    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b + tab_b);
+    uint32_t *colstart = reinterpret_cast<uint32_t *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b + tab_b);
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scr + pos_b + vals_b + tmp_b + h_b + sums_b + tab_b + cs_b);
     wmh_status st = WMH_OK;
     do {
         if (cudaMemsetAsync(H, 0, 4, a.stream) != cudaSuccess || cudaMemsetAsync(ctr, 0, 8, a.stream) != cudaSuccess) {
@@ -745,6 +765,13 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
         const uint32_t uni = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
         const uint32_t *pk = (L->flags & WMH_LAYOUT_WIDE) ? nullptr : L->cell_pack;
         if ((st = launch_draw_table(table, a.k, a.S, M, pk, uni, 1u, a.stream, L->int_to_comp, L->comp_to_m)) != WMH_OK) break;
+        if (uni) {                               // uniform bounds only (the row kernel's lookup)
+            const int64_t total = (int64_t)ep.E * (L->dim + 1);
+            const int blocks = (int)std::min<int64_t>((int64_t)sms * 8, (total + 255) / 256);
+            ix_colstart_kernel<<<blocks, 256, 0, a.stream>>>(pos, L->comp_to_m, uni, ep.E, M, L->dim, colstart);
+            count_launch();
+            if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index colstart"); break; }
+        }
 
     } while (0);
     if (st != WMH_OK) {
@@ -753,6 +780,7 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
     }
     out->scr = scr;
     out->pos = pos;
+    out->colstart = colstart;
     out->vals = vals;
     out->table = table;
     out->ctr = ctr;
@@ -790,6 +818,7 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     p.uni_m = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
     p.M = M;
     p.pos = pos;
+    p.colstart = ix.colstart;
     p.vals = vals;
     p.table = table;
     p.ep = ep;
@@ -808,7 +837,7 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     static const int nw_env = getenv("WMH_INDEX_NW") ? atoi(getenv("WMH_INDEX_NW")) : 0;
     int nw = 2;
     while (nw < 8 && (uint64_t)(64 / nw) * a.k * 4 > (128u << 10)) nw *= 2;
-    if (nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
+    if (nw_env == 1 || nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
     const int wb = weight_bytes(a.rows);
     if (a.sig_bytes == 1) st = csr ? ix_launch_w<1, true>(p, nw, wb, a.stream) : ix_launch_w<1, false>(p, nw, wb, a.stream);
     else st = csr ? ix_launch_w<2, true>(p, nw, wb, a.stream) : ix_launch_w<2, false>(p, nw, wb, a.stream);
