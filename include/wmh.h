@@ -218,6 +218,28 @@ wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k, int64_t n
  * that kernel to finish.  Errors: EINVAL (no such call), ECUDA. */
 wmh_status wmh_last_kernel_ms(float *ms);
 
+/* ---- f3: (K, L) banding LSH over the signatures ---------------------
+ * Band b of a signature row is its hashes [bK, (b+1)K); a row is a candidate of
+ * a query when they are equal in at least one band, which happens with
+ * probability 1 - (1 - J^K)^L for a pair of generalized Jaccard J (Theorem 1).
+ * wmh_lsh_build indexes the n_rows x k signatures `sig` (device, sig_bytes 1 or
+ * 2, K*L <= k): per band a key of the K values, a bucket table and the rows
+ * grouped by bucket (device memory owned by the index).  `sig` is NOT copied:
+ * it must stay alive and unchanged while the index is used.
+ * wmh_lsh_query: for each of the n_q query rows `qsig` (device, same k and
+ * sig_bytes) writes out_count[q] = the number of distinct candidate rows (each
+ * reported once, for its first colliding band; band values compared exactly,
+ * so bucket-key collisions never add a candidate) and up to max_out of them to
+ * out_rows[q][0..max_out) (device int64; which ones when there are more is
+ * unspecified; unused slots untouched).  Asynchronous on `stream`.
+ * Errors: EINVAL, ENOMEM, ECUDA. */
+typedef struct wmh_lsh wmh_lsh;
+wmh_status wmh_lsh_build(const void *sig, int32_t sig_bytes, uint32_t k, int64_t n_rows, uint32_t K, uint32_t L,
+                         wmh_lsh **out, void *stream);
+wmh_status wmh_lsh_query(const wmh_lsh *index, const void *qsig, int64_t n_q, uint32_t max_out, int64_t *out_rows,
+                         uint32_t *out_count, void *stream);
+void wmh_lsh_free(wmh_lsh *index);
+
 /* Thread-local description of the last failure ("" if none). */
 const char *wmh_last_error(void);
 

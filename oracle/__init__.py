@@ -320,3 +320,22 @@ def choose_scale(x_rows, scales) -> float:
         if best is None or Fraction(num, den) > best[1]:
             best = (s, Fraction(num, den))
     return None if best is None else float(best[0])
+
+
+# ------------------------------------------------ f3: (K, L) banding LSH
+def lsh_candidates(sig, K: int, L: int, qsig):
+    """For every query row, the sorted rows of `sig` equal to it in at least one
+    band b (hashes [bK, (b+1)K)).  Plain dictionaries of band tuples."""
+    sig = np.asarray(sig)
+    qsig = np.asarray(qsig)
+    index = [dict() for _ in range(L)]
+    for n in range(sig.shape[0]):
+        for b in range(L):
+            index[b].setdefault(sig[n, b * K:(b + 1) * K].tobytes(), []).append(n)
+    out = []
+    for q in qsig:
+        s = set()
+        for b in range(L):
+            s.update(index[b].get(q[b * K:(b + 1) * K].tobytes(), ()))
+        out.append(np.array(sorted(s), np.int64))
+    return out

@@ -23,7 +23,7 @@ from . import _lib
 from ._lib import WmhError  # noqa: F401
 
 __all__ = ["Rows", "Layout", "colmax", "reduce_bounds", "shard", "prepare", "hash", "hash_host", "collide", "WmhError",
-           "version", "quantize", "scale_objective", "choose_scale"]
+           "version", "quantize", "scale_objective", "choose_scale", "LSH"]
 
 
 def _stream(stream=None) -> int:
@@ -297,6 +297,42 @@ def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, st
     _lib.check(_lib.load().wmh_collide(_ptr(sig), sb, k, n_rows, _ptr(pairs), P, _ptr(matches), _ptr(jhat),
                                        1 if check_pairs else 0, _stream(stream)))
     return matches, jhat
+
+
+class LSH:
+    """f3: (K, L) banding LSH over a signature tensor: band b = hashes
+    [bK, (b+1)K); candidates of a query = rows equal to it in >= 1 band.  Keeps a
+    reference to `sig` (the index reads it at query time)."""
+
+    def __init__(self, sig: torch.Tensor, K: int, L: int, stream=None):
+        _need_cuda(sig, "sig")
+        if sig.dim() != 2 or sig.dtype not in (torch.uint8, torch.uint16):
+            raise ValueError("sig must be a 2-D uint8/uint16 CUDA tensor")
+        self.sig, self.K, self.L = sig, K, L
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().wmh_lsh_build(_ptr(sig), sig.element_size(), sig.shape[1], sig.shape[0], K, L,
+                                             ctypes.byref(h), _stream(stream)))
+        self._h = h
+
+    def query(self, qsig: torch.Tensor, max_out: int = 64, stream=None):
+        """(counts uint32 [n_q], rows int64 [n_q, max_out], -1 where unused)."""
+        _need_cuda(qsig, "qsig")
+        if qsig.dtype != self.sig.dtype or qsig.dim() != 2 or qsig.shape[1] != self.sig.shape[1]:
+            raise ValueError("query signatures must match the indexed ones (dtype, k)")
+        n_q = qsig.shape[0]
+        counts = torch.empty(n_q, dtype=torch.uint32, device=qsig.device)
+        rows = torch.full((n_q, max_out), -1, dtype=torch.int64, device=qsig.device)
+        _lib.check(_lib.load().wmh_lsh_query(self._h, _ptr(qsig), n_q, max_out, _ptr(rows), _ptr(counts),
+                                             _stream(stream)))
+        return counts, rows
+
+    def __del__(self):
+        try:
+            if self._h and self._h.value:
+                torch.cuda.synchronize()
+                _lib.load().wmh_lsh_free(self._h)
+        except Exception:
+            pass
 
 
 def version() -> str:

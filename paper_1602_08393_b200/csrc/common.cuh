@@ -146,6 +146,8 @@ struct IndexBuilt {
     uint32_t T = 0;
 };
 wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out);
+// In-place inclusive scan of uint32 a[0..n) (sums: ceil(n / 8192) + 1 words of scratch).
+wmh_status scan_u32_inplace(uint32_t *a, int64_t n, uint32_t *sums, cudaStream_t s);
 wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix);
 void index_free(IndexBuilt &ix, cudaStream_t s);
 uint32_t index_horizon(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t hint);

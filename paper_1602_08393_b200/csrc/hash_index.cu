@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(SC_T) scan_tile_apply(uint32_t *__restrict__ a
     }
 }
 
-static wmh_status scan_inplace(uint32_t *a, int64_t n, uint32_t *sums, cudaStream_t s) {
+wmh_status scan_u32_inplace(uint32_t *a, int64_t n, uint32_t *sums, cudaStream_t s) {
     const int64_t nt = (n + SC_TILE - 1) / SC_TILE;
     if (nt == 0) return WMH_OK;
     scan_tile_sums<<<(unsigned)nt, SC_T, 0, s>>>(a, n, sums);
@@ -752,7 +752,7 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
         ix_partition<false><<<b.n_cta, 512, psm, a.stream>>>(b, H, tmp);
         count_launch();
         if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index count"); break; }
-        if ((st = scan_inplace(H + 1, (int64_t)(n_h - 1), sums, a.stream)) != WMH_OK) break;
+        if ((st = scan_u32_inplace(H + 1, (int64_t)(n_h - 1), sums, a.stream)) != WMH_OK) break;
         ix_partition<true><<<b.n_cta, 512, psm, a.stream>>>(b, H, tmp);
         count_launch();
         if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index partition"); break; }
