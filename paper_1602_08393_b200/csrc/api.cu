@@ -340,6 +340,11 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
                             (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && k <= 65536 &&
                            (unsigned long long)h.n_rows * k > (1ull << 20);
     IndexBuilt ix;
+    struct IxGuard {                             // frees the index on every return path
+        IndexBuilt *ix;
+        cudaStream_t s;
+        ~IxGuard() { index_free(*ix, s); }
+    } guard{&ix, E.s_comp};
     HashArgs ha;
     if (use_index) {
         ha.L = L;
@@ -404,13 +409,13 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
             int used = 0;
             st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, 0, E.s_comp, &used);
         }
-        if (st != WMH_OK) { if (use_index) index_free(ix, E.s_comp); return st; }
+        if (st != WMH_OK) return st;
         WMH_CUDA_TRY(cudaEventRecord(E.ev_comp[slot], E.s_comp), "e2e event");
         WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_out, E.ev_comp[slot], 0), "e2e wait");
         WMH_CUDA_TRY(cudaMemcpyAsync((uint8_t *)sig_out_host + a * row_sig, dsig, nr * row_sig, cudaMemcpyDeviceToHost, E.s_out), "e2e D2H signatures");
         WMH_CUDA_TRY(cudaEventRecord(E.ev_out[slot], E.s_out), "e2e event");
     }
-    if (use_index) index_free(ix, E.s_comp);
+    index_free(ix, E.s_comp);                    // stream-ordered after the last chunk's kernel
     WMH_CUDA_TRY(cudaStreamSynchronize(E.s_out), "e2e synchronize");
     return WMH_OK;
 }
