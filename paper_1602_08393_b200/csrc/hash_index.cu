@@ -267,6 +267,7 @@ struct IxParams {
     void *sig;
     unsigned long long *n_sat;
     unsigned long long *row_ctr;
+    const uint32_t *perm;        // rows in processing order (deepest epoch first), or null
 };
 
 // x_c of the current row: dense byte, or a lower_bound over the CSR slice
@@ -323,6 +324,57 @@ __device__ __forceinline__ int ix_plan(const IxParams &p, float s, float cf) {
     return best_e;
 }
 
+// Processing order: rows grouped by the epoch their plan picks, deepest first,
+// so the CTAs resident at any time read the same epoch's pos[] / vals[] (one
+// epoch's tables fit L2 where all of them do not) and the heaviest rows start
+// first.  The order changes nothing but the schedule.
+template <bool CSR, typename W>
+__global__ void __launch_bounds__(256) ix_order_count(const IxParams p, uint8_t *__restrict__ row_epoch,
+                                                      unsigned int *__restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < p.n_rows; r += nw) {
+        unsigned long long xs = 0;
+        if (CSR) {
+            const int64_t a = p.row_ptr[r], b = p.row_ptr[r + 1];
+            for (int64_t i = a + lane; i < b; i += 32) xs += __ldg(reinterpret_cast<const W *>(p.val) + i);
+        } else {
+            const W *x = reinterpret_cast<const W *>(p.x) + r * p.D;
+            for (int64_t i = lane; i < p.D; i += 32) xs += __ldg(x + i);
+        }
+        for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xFFFFFFFFu, xs, o);
+        const int e = xs ? ix_plan(p, (float)((double)xs / (double)p.M), CSR ? p.cf_global : p.cf_dense) : 0;
+        if (lane == 0) {
+            row_epoch[r] = (uint8_t)e;
+            atomicAdd(cnt + e, 1u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) ix_order_scatter(int64_t n_rows, int E, const uint8_t *__restrict__ row_epoch,
+                                                        const unsigned int *__restrict__ cnt,
+                                                        unsigned int *__restrict__ cursor, uint32_t *__restrict__ perm) {
+    __shared__ unsigned int base[IX_MAXE];
+    if (threadIdx.x == 0) {                      // deepest epoch first
+        unsigned int run = 0;
+        for (int e = E - 1; e >= 0; e--) {
+            base[e] = run;
+            run += cnt[e];
+        }
+    }
+    __syncthreads();
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int e = row_epoch[r];
+        const unsigned peers = __match_any_sync(__activemask(), e);
+        const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+        unsigned int b0 = 0;
+        if (lane == leader) b0 = atomicAdd(cursor + e, (unsigned)__popc(peers));
+        b0 = __shfl_sync(peers, b0, leader);
+        perm[base[e] + b0 + __popc(peers & ((1u << lane) - 1))] = (uint32_t)r;
+    }
+}
+
 // Block-wide exclusive scan of a 64-bit value (NW warps); *total gets the sum.
 template <int NW>
 __device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long long v, unsigned long long *total) {
@@ -374,8 +426,8 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
         if (threadIdx.x == 0) s_row = (long long)atomicAdd(p.row_ctr, 1ull);
         for (uint32_t j = threadIdx.x; j < p.k; j += NT) h[j] = IX_NONE;
         __syncthreads();
-        const long long row = s_row;
-        if (row >= p.n_rows) break;
+        if (s_row >= p.n_rows) break;
+        const long long row = p.perm ? (long long)p.perm[s_row] : s_row;
         int64_t e0 = 0;
         int n;
         const W *xrow = nullptr;
@@ -833,6 +885,40 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     p.sig = a.sig;
     p.n_sat = a.n_sat;
     p.row_ctr = ctr;
+    p.perm = nullptr;
+    // processing order by planned epoch when the per-cell tables are far larger
+    // than L2 (measured: c4's 535 MB pos[] 22.8 -> 20.2 ms; c3's 194 MB and c2r
+    // gain nothing and pay the pre-pass); WMH_INDEX_ORDER=0/1 forces it off/on
+    static const int order_env = getenv("WMH_INDEX_ORDER") ? atoi(getenv("WMH_INDEX_ORDER")) : -1;
+    int l2 = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    const bool big_tables = (uint64_t)ep.E * M * 4 > 3ull * (uint64_t)l2;
+    uint8_t *oscr = nullptr;
+    if ((order_env == 1 || (order_env < 0 && big_tables)) && a.rows.n_rows >= 4096 && a.rows.n_rows < (1ll << 32)) {
+        const size_t pe_b = ((size_t)a.rows.n_rows + 255) & ~(size_t)255, pm_b = (size_t)a.rows.n_rows * 4;
+        WMH_CUDA_TRY(cudaMallocAsync((void **)&oscr, pe_b + pm_b + 2 * IX_MAXE * 4 + 256, a.stream), "index order alloc");
+        uint8_t *row_epoch = oscr;
+        uint32_t *perm = reinterpret_cast<uint32_t *>(oscr + pe_b);
+        unsigned int *cnt = reinterpret_cast<unsigned int *>(oscr + pe_b + ((pm_b + 255) & ~(size_t)255));
+        unsigned int *cursor = cnt + IX_MAXE;
+        WMH_CUDA_TRY(cudaMemsetAsync(cnt, 0, 2 * IX_MAXE * 4, a.stream), "index order memset");
+        const int blocks = (int)std::min<int64_t>((int64_t)num_sms() * 8, (a.rows.n_rows * 32 + 255) / 256);
+        const int wbo = weight_bytes(a.rows);
+        if (csr) {
+            if (wbo == 2) ix_order_count<true, uint16_t><<<blocks, 256, 0, a.stream>>>(p, row_epoch, cnt);
+            else ix_order_count<true, uint8_t><<<blocks, 256, 0, a.stream>>>(p, row_epoch, cnt);
+        } else {
+            if (wbo == 2) ix_order_count<false, uint16_t><<<blocks, 256, 0, a.stream>>>(p, row_epoch, cnt);
+            else ix_order_count<false, uint8_t><<<blocks, 256, 0, a.stream>>>(p, row_epoch, cnt);
+        }
+        count_launch();
+        const int sblocks = (int)std::min<int64_t>((int64_t)num_sms() * 8, (a.rows.n_rows + 255) / 256);
+        ix_order_scatter<<<sblocks, 256, 0, a.stream>>>(a.rows.n_rows, ep.E, row_epoch, cnt, cursor, perm);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(oscr, a.stream); return cuda_fail(cudaGetLastError(), "index order"); }
+        p.perm = perm;
+    }
     // warps per row: >= 2; keep <= ~128 KiB of h[] per SM at 64 resident warps
     static const int nw_env = getenv("WMH_INDEX_NW") ? atoi(getenv("WMH_INDEX_NW")) : 0;
     int nw = 2;
@@ -841,6 +927,7 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     const int wb = weight_bytes(a.rows);
     if (a.sig_bytes == 1) st = csr ? ix_launch_w<1, true>(p, nw, wb, a.stream) : ix_launch_w<1, false>(p, nw, wb, a.stream);
     else st = csr ? ix_launch_w<2, true>(p, nw, wb, a.stream) : ix_launch_w<2, false>(p, nw, wb, a.stream);
+    if (oscr) cudaFreeAsync(oscr, a.stream);
     return st;
 }
 
