@@ -172,6 +172,13 @@ static wmh_status validate_hash(const wmh_layout *L, const wmh_rows *rows, uint3
     return WMH_OK;
 }
 
+static bool tiny_batch(const wmh_layout *L, const wmh_rows *rows, uint32_t k, uint32_t cap) {
+    const double ed = L->mean_s > 0.0 ? std::min((double)cap, 1.0 / L->mean_s)
+                                      : (rows->kind == WMH_CSR ? (double)cap : 32.0);
+    return (unsigned long long)rows->n_rows * k <= (1ull << 20) &&
+           (double)rows->n_rows * (double)k * ed <= (double)(1ull << 24);
+}
+
 static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
                                 int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, int algo, int chunk,
                                 uint32_t horizon, cudaStream_t s, int *algo_used) {
@@ -193,9 +200,11 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
     }
-    // tiny batches (<= 2^20 row-hash pairs, e.g. config c1) are launch-bound:
-    // the single-launch SIMPLE kernel beats the table + tiled pair there
-    const bool tiny = (unsigned long long)rows->n_rows * k <= (1ull << 20);
+    // tiny batches are launch-bound: the single-launch SIMPLE kernel beats the
+    // table + tiled pair there (c1).  "Tiny" counts expected draws, not pairs
+    // (Theorem 2: ~1/s per hash, s from prepare's statistics): a few sparse rows
+    // at s ~ 1e-4 are 10^4 draws per hash, far cheaper on the index
+    const bool tiny = tiny_batch(L, rows, k, cap);
     // The index kernel visits only the green draws (k*T*s per row); the tile
     // tests ~k/s draws per row, 4 rows per shared load.  Measured: CSR rows
     // (c3, c4) 35-350x faster on the index; dense rows at s = 0.05 (c2) 1.4x
@@ -338,7 +347,7 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     // whole call; every chunk then only runs its rows kernel
     const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.01) ||
                             (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && k <= 65536 &&
-                           (unsigned long long)h.n_rows * k > (1ull << 20);
+                           !tiny_batch(L, &h, k, cap);
     IndexBuilt ix;
     struct IxGuard {                             // frees the index on every return path
         IndexBuilt *ix;
