@@ -194,6 +194,22 @@ wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t 
                        uint32_t cap, int32_t sig_bytes, void *sig_out, uint64_t *n_saturated,
                        wmh_hash_opts *opts, void *stream);
 
+/* A prepared hash family for streaming many row batches: wmh_hasher_create
+ * draws every (j, t < T) once and files it under its cell (the INDEX kernel's
+ * build, see WMH_ALGO_INDEX; horizon as in wmh_hash_opts, 0 = auto);
+ * wmh_hasher_run then hashes a batch with the index kernel's row pass only.
+ * Output is bit-identical to wmh_hash(layout, rows, seed, k, cap, ...).  The
+ * hasher keeps a pointer to `layout` (keep it alive) and its device index
+ * (freed by wmh_hasher_free, which synchronises the device).  Runs on one
+ * hasher must not overlap in time (they share a row counter): issue them on
+ * one stream.  Errors: as wmh_hash; k <= 65536. */
+typedef struct wmh_hasher wmh_hasher;
+wmh_status wmh_hasher_create(const wmh_layout *layout, uint64_t seed, uint32_t k, uint32_t cap, uint32_t horizon,
+                             wmh_hasher **out, void *stream);
+wmh_status wmh_hasher_run(const wmh_hasher *hasher, const wmh_rows *rows, int32_t sig_bytes, void *sig_out,
+                          uint64_t *n_saturated, void *stream);
+void wmh_hasher_free(wmh_hasher *hasher);
+
 /* End-to-end convenience (the e2e path): rows and signatures in HOST memory
  * (pinned or pageable).  Copies the rows host->device into library scratch
  * (kept across calls and grown on demand, one per thread), runs wmh_hash on

@@ -23,7 +23,7 @@ from . import _lib
 from ._lib import WmhError  # noqa: F401
 
 __all__ = ["Rows", "Layout", "colmax", "reduce_bounds", "shard", "prepare", "hash", "hash_host", "collide", "WmhError",
-           "version", "quantize", "scale_objective", "choose_scale", "LSH"]
+           "version", "quantize", "scale_objective", "choose_scale", "LSH", "Hasher"]
 
 
 def _stream(stream=None) -> int:
@@ -297,6 +297,41 @@ def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, st
     _lib.check(_lib.load().wmh_collide(_ptr(sig), sb, k, n_rows, _ptr(pairs), P, _ptr(matches), _ptr(jhat),
                                        1 if check_pairs else 0, _stream(stream)))
     return matches, jhat
+
+
+class Hasher:
+    """A prepared hash family (seed, k, cap) over `layout`: the draws are filed once
+    (the index build) and every .hash(rows) call runs only the row pass -- for
+    streaming many batches.  Signatures equal hash(layout, rows, seed, k, cap)."""
+
+    def __init__(self, layout: Layout, seed: int, k: int, cap: int, horizon: int = 0, stream=None):
+        self.layout, self.seed, self.k, self.cap = layout, seed, k, cap
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().wmh_hasher_create(layout.handle, seed & (2**64 - 1), k, cap, horizon, ctypes.byref(h),
+                                                 _stream(stream)))
+        self._h = h
+
+    def hash(self, rows: Rows, sig_bytes: int | None = None, out: torch.Tensor | None = None,
+             n_saturated: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        _no_float(rows, "Hasher.hash")
+        if sig_bytes is None:
+            sig_bytes = 1 if self.cap <= 255 else 2
+        dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
+        dev = (rows.dense if rows.dense is not None else rows.row_ptr).device
+        if out is None:
+            out = torch.empty((rows.n_rows, self.k), dtype=dtype, device=dev)
+        elif out.dtype != dtype or out.numel() != rows.n_rows * self.k:
+            raise ValueError("out has the wrong dtype or size")
+        _lib.check(_lib.load().wmh_hasher_run(self._h, ctypes.byref(rows._c()), sig_bytes, _ptr(out),
+                                              _ptr(n_saturated), _stream(stream)))
+        return out
+
+    def __del__(self):
+        try:
+            if self._h and self._h.value:
+                _lib.load().wmh_hasher_free(self._h)
+        except Exception:
+            pass
 
 
 class LSH:

@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 
 EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_tables", "wmh_layout_free",
            "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version",
            "wmh_kernel_launches", "wmh_last_kernel_ms", "wmh_quantize", "wmh_scale_objective", "wmh_lsh_build",
-           "wmh_lsh_query", "wmh_lsh_free"]
+           "wmh_lsh_query", "wmh_lsh_free", "wmh_hasher_create", "wmh_hasher_run", "wmh_hasher_free"]
 
 
 class WmhRows(ctypes.Structure):
@@ -75,6 +75,9 @@ def load() -> ctypes.CDLL:
             "wmh_lsh_build": (st, [vp, i32, u32, i64, u32, u32, ctypes.POINTER(vp), vp]),
             "wmh_lsh_query": (st, [vp, vp, i64, u32, vp, vp, vp]),
             "wmh_lsh_free": (None, [vp]),
+            "wmh_hasher_create": (st, [vp, u64, u32, u32, u32, ctypes.POINTER(vp), vp]),
+            "wmh_hasher_run": (st, [vp, rows_p, i32, vp, vp, vp]),
+            "wmh_hasher_free": (None, [vp]),
             "wmh_scale_objective": (st, [rows_p, ctypes.POINTER(ctypes.c_float), i32, ctypes.POINTER(u64), vp]),
         }
         for name, (res, args) in proto.items():

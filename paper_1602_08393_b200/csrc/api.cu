@@ -258,6 +258,63 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
     return st;
 }
 
+// ---- a prepared hash family: the index built once, many row batches
+struct wmh_hasher {
+    const wmh_layout *L = nullptr;
+    uint64_t seed = 0;
+    uint32_t k = 0, cap = 0;
+    IndexBuilt ix;
+};
+
+extern "C" wmh_status wmh_hasher_create(const wmh_layout *L, uint64_t seed, uint32_t k, uint32_t cap, uint32_t horizon,
+                                        wmh_hasher **out, void *stream) {
+    if (!out) { set_error("wmh_hasher_create: out is NULL"); return WMH_EINVAL; }
+    *out = nullptr;
+    if (!L) { set_error("wmh_hasher_create: layout is NULL"); return WMH_EINVAL; }
+    if (k < 1 || k > 65536) { set_error("wmh_hasher_create: k=%u not in [1, 65536]", k); return WMH_EINVAL; }
+    if (cap < 1 || cap > 65535) { set_error("wmh_hasher_create: cap=%u not in [1, 65535]", cap); return WMH_EINVAL; }
+    HashArgs a{};
+    a.L = L;
+    a.S = splitmix64(seed);
+    a.k = k;
+    a.cap = cap;
+    a.stream = (cudaStream_t)stream;
+    wmh_hasher *h = new wmh_hasher();
+    h->L = L;
+    h->seed = seed;
+    h->k = k;
+    h->cap = cap;
+    wmh_status st = index_build(a, horizon, &h->ix);
+    if (st != WMH_OK) { delete h; return st; }
+    *out = h;
+    return WMH_OK;
+}
+
+extern "C" wmh_status wmh_hasher_run(const wmh_hasher *h, const wmh_rows *rows, int32_t sig_bytes, void *sig_out,
+                                     uint64_t *n_saturated, void *stream) {
+    if (!h) { set_error("wmh_hasher_run: hasher is NULL"); return WMH_EINVAL; }
+    wmh_status st = validate_hash(h->L, rows, h->k, h->cap, sig_bytes, sig_out, false);
+    if (st != WMH_OK) return st;
+    if (rows->n_rows == 0) return WMH_OK;
+    HashArgs a{};
+    a.L = h->L;
+    a.rows = *rows;
+    a.S = splitmix64(h->seed);
+    a.k = h->k;
+    a.cap = h->cap;
+    a.sig_bytes = sig_bytes;
+    a.sig = sig_out;
+    a.n_sat = reinterpret_cast<unsigned long long *>(n_saturated);
+    a.stream = (cudaStream_t)stream;
+    return index_rows(a, h->ix);
+}
+
+extern "C" void wmh_hasher_free(wmh_hasher *h) {
+    if (!h) return;
+    if (h->ix.scr) cudaFree(h->ix.scr);          // (pool memory: cudaFree synchronises)
+    delete h;
+}
+
 extern "C" wmh_status wmh_hash(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
                                int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, void *stream) {
     return wmh_hash_ex(L, rows, seed, k, cap, sig_bytes, sig_out, n_saturated, nullptr, stream);

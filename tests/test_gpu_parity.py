@@ -295,3 +295,17 @@ def test_collide_estimates_jaccard_c5_recipe(wmh):
     assert np.sum(np.abs(z) > 3) <= 0.01 * P + 2
     assert abs(z.mean()) <= 1.0
     assert 0.75 <= z.var() <= 1.25
+
+
+def test_hasher_streams_batches(wmh):
+    """wmh_hasher: the draws filed once, several row batches hashed with the row
+    pass only -- identical to wmh_hash on the whole matrix and to the oracle."""
+    cfg, data = datagen.make("c3", n_rows=400)
+    rows = to_rows(data)
+    layout = wmh.prepare(rows)
+    whole = wmh.hash(layout, rows, 3, 200, 65535, algo="index").cpu()
+    hz = wmh.Hasher(layout, 3, 200, 65535)
+    parts = [hz.hash(rows.slice(a, b)).cpu() for a, b in ((0, 150), (150, 151), (151, 400))]
+    assert torch.equal(torch.cat(parts), whole)
+    L = oracle.Layout(oracle_bounds(data))
+    _assert_sig_equal(parts[1], oracle_hash(L, data, 3, 200, 65535, rows=[150]), "hasher")
