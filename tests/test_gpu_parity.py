@@ -303,9 +303,10 @@ def test_hasher_streams_batches(wmh):
     cfg, data = datagen.make("c3", n_rows=400)
     rows = to_rows(data)
     layout = wmh.prepare(rows)
-    whole = wmh.hash(layout, rows, 3, 200, 65535, algo="index").cpu()
+    whole = wmh.hash(layout, rows, 3, 200, 65535, algo="index").view(torch.int16).cpu()
     hz = wmh.Hasher(layout, 3, 200, 65535)
-    parts = [hz.hash(rows.slice(a, b)).cpu() for a, b in ((0, 150), (150, 151), (151, 400))]
+    parts = [hz.hash(rows.slice(a, b)).view(torch.int16).cpu() for a, b in ((0, 150), (150, 151), (151, 400))]
     assert torch.equal(torch.cat(parts), whole)
     L = oracle.Layout(oracle_bounds(data))
-    _assert_sig_equal(parts[1], oracle_hash(L, data, 3, 200, 65535, rows=[150]), "hasher")
+    got = parts[1].numpy().view(np.uint16).astype(np.uint32)
+    assert np.array_equal(got, oracle_hash(L, data, 3, 200, 65535, rows=[150]))
