@@ -310,3 +310,22 @@ def test_hasher_streams_batches(wmh):
     L = oracle.Layout(oracle_bounds(data))
     got = parts[1].numpy().view(np.uint16).astype(np.uint32)
     assert np.array_equal(got, oracle_hash(L, data, 3, 200, 65535, rows=[150]))
+
+
+@pytest.mark.parametrize("name,n,k", [("c2", 900, 128), ("c3", 300, 100), ("c5", 700, 64)])
+def test_sharding_invariance(wmh, name, n, k):
+    """SURVEY P10 on the CUDA path: G row shards, each with its local column max
+    reduced to the global one (the all-reduce(MAX) of prepare, here an elementwise
+    max), hashed separately, give byte-identical signatures for G = 1, 2, 4, 8 --
+    every draw depends on (seed, j, t, M) only."""
+    cfg, data = datagen.make(name, n_rows=n)
+    rows = to_rows(data)
+    ref = wmh.hash(wmh.prepare(rows), rows, cfg.seed, k, cfg.cap, cfg.sig_bytes).view(torch.int16).cpu()
+    for G in (2, 4, 8):
+        shards = [rows.slice(*wmh.shard(n, r, G)) for r in range(G)]
+        bounds = torch.stack([wmh.colmax(s).to(torch.int64) for s in shards]).amax(0).to(torch.int32)
+        parts = []
+        for s in shards:
+            layout = wmh.prepare(s, bounds=bounds.view(torch.int32))
+            parts.append(wmh.hash(layout, s, cfg.seed, k, cfg.cap, cfg.sig_bytes).view(torch.int16).cpu())
+        assert torch.equal(torch.cat(parts), ref), G
