@@ -382,7 +382,18 @@ def main():
 
     coll = None
     if args.collide_pairs > 0:
-        coll = measure_collide(wmh, sig, args.collide_pairs, cfg, dev, peaks)
+        gather_ms = None
+        sig_c = sig
+        if world > 1:                   # the optional NCCL signature exchange, then pairs over all rows
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            sig_c = wmh.gather_signatures(sig)
+            g1.record()
+            torch.cuda.synchronize()
+            gather_ms = g0.elapsed_time(g1)
+        coll = measure_collide(wmh, sig_c, args.collide_pairs, cfg, dev, peaks)
+        coll["gather_ms"] = gather_ms
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

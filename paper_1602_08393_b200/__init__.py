@@ -23,7 +23,7 @@ from . import _lib
 from ._lib import WmhError  # noqa: F401
 
 __all__ = ["Rows", "Layout", "colmax", "reduce_bounds", "shard", "prepare", "hash", "hash_host", "collide", "WmhError",
-           "version", "quantize", "scale_objective", "choose_scale", "LSH", "Hasher"]
+           "version", "quantize", "scale_objective", "choose_scale", "LSH", "Hasher", "gather_signatures"]
 
 
 def _stream(stream=None) -> int:
@@ -162,6 +162,28 @@ def reduce_bounds(bounds: torch.Tensor, group=None) -> torch.Tensor:
     if world:
         dist.all_reduce(bounds.view(torch.int32), op=dist.ReduceOp.MAX, group=group)
     return bounds
+
+
+def gather_signatures(sig: torch.Tensor, group=None) -> torch.Tensor:
+    """The optional signature exchange of the multi-GPU path (north star: "NCCL ...
+    optionally, the signatures"): every rank's [n_r, k] shard, concatenated in
+    rank order on every rank (torch.distributed all-gather; shards may differ in
+    size by the shard() split).  A single-process call returns `sig` itself."""
+    dist = torch.distributed
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return sig
+    world = dist.get_world_size(group)
+    n_local = torch.tensor([sig.shape[0]], dtype=torch.int64, device=sig.device)
+    sizes = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(sizes, n_local, group=group)
+    sizes = [int(t.item()) for t in sizes]
+    n_max = max(sizes)
+    row_bytes = sig.shape[1] * sig.element_size()                     # bytes travel (NCCL and gloo take uint8)
+    buf = torch.zeros((n_max, row_bytes), dtype=torch.uint8, device=sig.device)
+    buf[:sig.shape[0]] = sig.contiguous().view(torch.uint8).view(sig.shape[0], row_bytes)
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    return torch.cat([o[:n] for o, n in zip(out, sizes)]).view(sig.dtype).view(-1, sig.shape[1])
 
 
 def shard(n_rows: int, rank: int, world: int) -> tuple[int, int]:

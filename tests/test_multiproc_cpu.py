@@ -50,6 +50,9 @@ def _worker(rank, world, port, n_rows, dim):
         gathered = [None] * world
         dist.all_gather_object(gathered, sig_shard)
         assert np.array_equal(np.concatenate(gathered), sig_all)
+        # the binding's optional signature exchange (all-gather, unequal shards)
+        full = wmh.gather_signatures(torch.from_numpy(sig_shard.astype(np.int16)).view(torch.uint16))
+        assert np.array_equal(full.view(torch.int16).numpy().astype(np.uint16).astype(np.uint32), sig_all)
     finally:
         dist.destroy_process_group()
 
