@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
         const uint32_t j0 = (uint32_t)hc * p.hchunk, j1 = min(p.k, j0 + (uint32_t)p.hchunk);
 
         // ---- a5: stage transposed: 4 rows x 4 columns per lane, 8 PRMTs --------
+        unsigned long long wsum = 0;                   // this warp's row sums / live rows: one
+        int walive = 0;                                // shared atomic per warp, not per row
         for (int g = warp; g < NWD; g += CM_NW) {
             const uint32_t *rp[4];
             bool ok[4];
@@ -268,9 +270,14 @@ __global__ void __launch_bounds__(CM_NT, 1) hash_tiled_cm_kernel(const CmParams 
                 uint32_t a = acc[b];
                 for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
                 if (a) live4 |= 1u << b;
-                if (lane == 0 && a) { atomicAdd(&s_xsum, (unsigned long long)a); atomicAdd(&s_nalive, 1); }
+                wsum += a;
+                walive += a != 0;
             }
             if (lane == 0) sflag4[g] = (uint8_t)live4;
+        }
+        if (lane == 0 && walive) {
+            atomicAdd(&s_xsum, wsum);
+            atomicAdd(&s_nalive, walive);
         }
         __syncthreads();
         const int nalive = s_nalive;
