@@ -74,3 +74,36 @@ def test_binding_has_no_cpu_fallback():
     rows = wmh.Rows.from_dense(torch.zeros((2, 8), dtype=torch.uint8))
     with pytest.raises(ValueError):
         wmh.colmax(rows)
+
+
+def test_new_entry_points_validate_without_gpu(lib):
+    """f1 / f3 / hasher / timing entry points reject bad arguments before any
+    CUDA call (so these run on a CPU-only host)."""
+    from paper_1602_08393_b200 import _lib
+    E = _lib.WMH_EINVAL
+    out = ctypes.c_void_p()
+    # LSH: K*L > k, bad width, NULL signatures, NULL index
+    assert lib.wmh_lsh_build(ctypes.c_void_p(1), 2, 10, 5, 4, 3, ctypes.byref(out), None) == E
+    assert b"K*L" in lib.wmh_last_error()
+    assert lib.wmh_lsh_build(ctypes.c_void_p(1), 4, 10, 5, 2, 2, ctypes.byref(out), None) == E
+    assert lib.wmh_lsh_build(None, 2, 10, 5, 2, 2, ctypes.byref(out), None) == E
+    cnt = ctypes.c_void_p(1)
+    assert lib.wmh_lsh_query(None, None, 1, 1, None, cnt, None) == E
+    # hasher: NULL layout, k out of range
+    assert lib.wmh_hasher_create(None, 1, 8, 10, 0, ctypes.byref(out), None) == E
+    assert lib.wmh_hasher_create(ctypes.c_void_p(1), 1, 0, 10, 0, ctypes.byref(out), None) == E
+    assert lib.wmh_hasher_run(None, None, 2, None, None, None) == E
+    # quantiser and scale objective: bad scale, n < 0, empty grid
+    assert lib.wmh_quantize(None, 4, ctypes.c_float(0.0), None, None) == E
+    assert lib.wmh_quantize(None, -1, ctypes.c_float(2.0), None, None) == E
+    rows = _lib.WmhRows(0, 4, 8, None, None, None, None, 0, 0)
+    sc = (ctypes.c_float * 1)(1.0)
+    o3 = (ctypes.c_uint64 * 3)()
+    assert lib.wmh_scale_objective(ctypes.byref(rows), sc, 0, o3, None) == E
+    # a weight width other than 1 / 2
+    bad = _lib.WmhRows(0, 4, 8, None, None, None, None, 0, 3)
+    assert lib.wmh_colmax(ctypes.byref(bad), None, None) == E
+    assert b"weight_bytes" in lib.wmh_last_error()
+    # no timed hash call on this thread yet
+    ms = ctypes.c_float()
+    assert lib.wmh_last_kernel_ms(ctypes.byref(ms)) == E
