@@ -146,6 +146,9 @@ struct IndexBuilt {
     uint32_t T = 0;
 };
 wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out);
+// The coalesced build of pos (E*M + 1) and vals (sum_e k * B[e+1]) (index_build.cu).
+wmh_status index_build_sorted(uint64_t S, uint32_t k, uint32_t M, const IxEpochs &ep, uint32_t *pos, uint32_t *vals,
+                              cudaStream_t s);
 // In-place inclusive scan of uint32 a[0..n) (sums: ceil(n / 8192) + 1 words of scratch).
 wmh_status scan_u32_inplace(uint32_t *a, int64_t n, uint32_t *sums, cudaStream_t s);
 wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix);

@@ -798,6 +798,12 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
             st = cuda_fail(cudaGetLastError(), "index memset");
             break;
         }
+        static const int build_env = getenv("WMH_INDEX_BUILD") ? atoi(getenv("WMH_INDEX_BUILD")) : 2;
+        st = build_env != 1 ? index_build_sorted(a.S, a.k, M, ep, pos, vals, a.stream) : WMH_EINVAL;
+        if (st != WMH_OK && st != WMH_EINVAL) break;
+        if (st == WMH_OK) {                      // the coalesced build (index_build.cu)
+        } else {                                 // the direct partition (very wide key spaces)
+        st = WMH_OK;
         const size_t psm = (size_t)b.n_chunks * 4;
         cudaFuncSetAttribute(ix_partition<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
         cudaFuncSetAttribute(ix_partition<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
@@ -813,6 +819,7 @@ wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
         ix_chunk_sort<<<b.n_chunks, SC_T, csm, a.stream>>>(b, H, tmp, pos, vals);
         count_launch();
         if (cudaGetLastError() != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "index sort"); break; }
+        }
 
         const uint32_t uni = (L->flags & WMH_LAYOUT_UNIFORM) ? L->uniform_m : 0u;
         const uint32_t *pk = (L->flags & WMH_LAYOUT_WIDE) ? nullptr : L->cell_pack;
