@@ -184,11 +184,17 @@ typedef struct {
                             on it.  OUTPUT when the index kernel ran: the horizon it used */
     uint32_t flags;      /* WMH_OPT_TIME_KERNEL: bracket the call's dominant (per-row)
                             kernel with CUDA events on `stream`; read with
-                            wmh_last_kernel_ms */
+                            wmh_last_kernel_ms.  WMH_OPT_TILE_BYTES /
+                            WMH_OPT_TILE_BITPLANES (exclusive): for TILED on
+                            dense rows, the byte tile or the bit-plane tile
+                            (default: bit planes when the byte tile would hold
+                            fewer than 128 rows).  Performance only. */
     int32_t reserved[3]; /* must be zero */
 } wmh_hash_opts;
 
 #define WMH_OPT_TIME_KERNEL 1u
+#define WMH_OPT_TILE_BYTES 2u
+#define WMH_OPT_TILE_BITPLANES 4u
 
 wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k,
                        uint32_t cap, int32_t sig_bytes, void *sig_out, uint64_t *n_saturated,

@@ -222,8 +222,11 @@ last_horizon = None  # the index horizon T of the last hash() call that ran the 
 
 def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
          algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
-         chunk: int = 0, horizon: int = 0, time_kernel: bool = False, stream=None) -> torch.Tensor:
-    """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16)."""
+         chunk: int = 0, horizon: int = 0, time_kernel: bool = False, stream=None,
+         tile: str = "auto") -> torch.Tensor:
+    """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16).
+    `tile` ("auto", "bytes", "bitplanes") picks the TILED kernel's dense tile
+    (performance only)."""
     if sig_bytes is None:
         sig_bytes = 1 if cap <= 255 else 2
     dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
@@ -235,7 +238,11 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
     _no_float(rows, "hash")
     if n_saturated is not None and (n_saturated.dtype not in (torch.int64, torch.uint64) or not n_saturated.is_cuda):
         raise ValueError("n_saturated must be a CUDA int64 tensor")
-    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon, _lib.WMH_OPT_TIME_KERNEL if time_kernel else 0)
+    if tile not in ("auto", "bytes", "bitplanes"):
+        raise ValueError(f"tile must be auto, bytes or bitplanes, not {tile!r}")
+    flags = (_lib.WMH_OPT_TIME_KERNEL if time_kernel else 0) | \
+        {"auto": 0, "bytes": _lib.WMH_OPT_TILE_BYTES, "bitplanes": _lib.WMH_OPT_TILE_BITPLANES}[tile]
+    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon, flags)
     _lib.check(_lib.load().wmh_hash_ex(layout.handle, ctypes.byref(rows._c()), seed & (2**64 - 1), k, cap, sig_bytes,
                                        _ptr(out), _ptr(n_saturated), ctypes.byref(opts), _stream(stream)))
     global last_algo, last_horizon

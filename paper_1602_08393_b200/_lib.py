@@ -11,6 +11,8 @@ SO_PATH = os.path.join(_HERE, "libwmh.so")
 WMH_OK, WMH_EINVAL, WMH_EBOUND, WMH_EEMPTY, WMH_EOVERFLOW, WMH_ECUDA, WMH_ENOMEM = range(7)
 WMH_DENSE, WMH_CSR = 0, 1
 WMH_OPT_TIME_KERNEL = 1
+WMH_OPT_TILE_BYTES = 2
+WMH_OPT_TILE_BITPLANES = 4
 ALGOS = {"auto": 0, "simple": 1, "tiled": 2, "index": 3}
 STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 4: "WMH_EOVERFLOW",
                 5: "WMH_ECUDA", 6: "WMH_ENOMEM"}

@@ -181,7 +181,7 @@ static bool tiny_batch(const wmh_layout *L, const wmh_rows *rows, uint32_t k, ui
 
 static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
                                 int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, int algo, int chunk,
-                                uint32_t horizon, cudaStream_t s, int *algo_used) {
+                                uint32_t horizon, cudaStream_t s, int *algo_used, int tile = 0) {
     *algo_used = algo == WMH_ALGO_AUTO ? WMH_ALGO_SIMPLE : algo;
     if (rows->n_rows == 0) return WMH_OK;
     HashArgs a;
@@ -196,6 +196,7 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     a.stream = s;
     a.chunk = chunk;
     a.horizon = horizon;
+    a.tile = tile;
     if (algo == WMH_ALGO_INDEX) {
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
@@ -233,11 +234,13 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
                                   void *stream) {
     wmh_status st = validate_hash(L, rows, k, cap, sig_bytes, sig_out, false);
     if (st != WMH_OK) return st;
-    int algo = WMH_ALGO_AUTO, chunk = 0;
+    int algo = WMH_ALGO_AUTO, chunk = 0, tile = 0;
     uint32_t horizon = 0;
     if (opts) {
         algo = opts->algo;
-        if (opts->flags & ~(uint32_t)WMH_OPT_TIME_KERNEL) { set_error("wmh_hash_ex: unknown flags 0x%x", opts->flags); return WMH_EINVAL; }
+        if (opts->flags & ~(uint32_t)(WMH_OPT_TIME_KERNEL | WMH_OPT_TILE_BYTES | WMH_OPT_TILE_BITPLANES)) { set_error("wmh_hash_ex: unknown flags 0x%x", opts->flags); return WMH_EINVAL; }
+        if ((opts->flags & WMH_OPT_TILE_BYTES) && (opts->flags & WMH_OPT_TILE_BITPLANES)) { set_error("wmh_hash_ex: WMH_OPT_TILE_BYTES and WMH_OPT_TILE_BITPLANES are exclusive"); return WMH_EINVAL; }
+        tile = (opts->flags & WMH_OPT_TILE_BYTES) ? 1 : (opts->flags & WMH_OPT_TILE_BITPLANES) ? 2 : 0;
         for (int i = 0; i < 3; i++)
             if (opts->reserved[i]) { set_error("wmh_hash_ex: reserved option fields must be zero"); return WMH_EINVAL; }
         chunk = opts->chunk;
@@ -249,7 +252,7 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
     g_ktimer.on = opts && (opts->flags & WMH_OPT_TIME_KERNEL);
     if (g_ktimer.on) g_ktimer.recorded = false;
     st = hash_dispatch(L, rows, seed, k, cap, sig_bytes, sig_out, n_saturated, algo, chunk, horizon, (cudaStream_t)stream,
-                       &used);
+                       &used, tile);
     g_ktimer.on = false;
     if (opts) {
         opts->algo_used = used;

@@ -13,6 +13,7 @@ struct wmh_layout {
     uint64_t M = 0;
     uint32_t flags = 0;          // bit 0: uniform bounds
     uint32_t uniform_m = 0;      // the common bound when uniform, else 0
+    uint32_t max_bound = 0;      // max_c m_c
     uint32_t *bounds = nullptr;       // [dim]
     uint32_t *comp_to_m = nullptr;    // [dim + 1]   CompToM, exclusive prefix (Eq. 3)
     uint32_t *int_to_comp = nullptr;  // [M]         IntToComp (Alg. 4)
@@ -123,12 +124,15 @@ struct HashArgs {
     cudaStream_t stream;
     int chunk;           // TILED: 0 = auto, else 4/8/16/32
     uint32_t horizon;    // INDEX: draws filed per hash (0 = auto)
+    int tile = 0;        // TILED dense: 0 auto, 1 byte tile, 2 bit-plane tile
 };
 
 wmh_status launch_hash_simple(const HashArgs &a);
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled);
+wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled);
+bool tiled_cm_full_tile(const HashArgs &a);
 wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon);
 // The index of one call, reusable by several row batches of the same (layout,
 // seed, k, cap): built on a.stream, freed stream-ordered.

@@ -389,6 +389,17 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     // column-major tile with the SIMD first round (hash_tiled_cm.cu) unless
     // WMH_TILED_RM=1 selects this row-major kernel
     static const bool force_rm = getenv("WMH_TILED_RM") != nullptr;
+    // bit-plane tile (hash_tiled_bs.cu) for long rows -- where the byte tile
+    // would hold fewer than 128 rows and the planes of >= 2 groups fit
+    // (measured: c5's recipe, 10^6 rows, NB = 6: 18.1 vs 21.2 ms; on c2's
+    // 128-row tile the SWAR byte tile stays ahead, 0.58 vs 0.75 ms);
+    // WMH_TILED_BS=1 / 0 or the WMH_OPT_TILE_* flags force the choice
+    static const int bs_env = getenv("WMH_TILED_BS") ? atoi(getenv("WMH_TILED_BS")) : -1;
+    const bool want_bs = a.tile == 2 || (a.tile == 0 && (bs_env == 1 || (bs_env != 0 && !tiled_cm_full_tile(a))));
+    if (!force_rm && want_bs) {
+        const wmh_status bst = launch_hash_tiled_bs(a, handled);
+        if (bst != WMH_OK || *handled) return bst;
+    }
     if (!force_rm) {
         const wmh_status cst = launch_hash_tiled_cm(a, handled);
         if (cst != WMH_OK || *handled) return cst;

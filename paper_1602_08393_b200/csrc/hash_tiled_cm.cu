@@ -508,6 +508,15 @@ static void cm_launch(const CmParams &p, size_t smem, int grid, cudaStream_t s) 
     kernel_timer_end(s);
 }
 
+// does the column-major byte tile hold its full 128 rows for these rows?
+bool tiled_cm_full_tile(const HashArgs &a) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return cm_smem((int)a.rows.dim, 128, 132, 1) <= (size_t)smem_optin;
+}
+
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
     *handled = false;
     const int D = (int)a.rows.dim;

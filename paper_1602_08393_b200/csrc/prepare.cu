@@ -454,6 +454,7 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     if (M >= (1ull << 32)) { set_error("wmh_prepare: M = %llu >= 2^32", M); return fail(WMH_EOVERFLOW); }
     L->M = M;
     if (mn == mx) { L->flags |= WMH_LAYOUT_UNIFORM; L->uniform_m = mx; }
+    L->max_bound = (uint32_t)mx;
     if (mx > 255) L->flags |= WMH_LAYOUT_WIDE;       // 8-bit cell offsets no longer fit: no cell_pack
 
     if (cudaMalloc(&L->int_to_comp, sizeof(uint32_t) * M) != cudaSuccess ||

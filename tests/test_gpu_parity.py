@@ -35,7 +35,7 @@ def _assert_sig_equal(gpu, ref, what=""):
                              f"oracle {ref[r, j]}")
 
 
-def _run(wmh, data, cfg, k, cap, sig_bytes, algo, seed=None, fixed_bound=None, horizon=0):
+def _run(wmh, data, cfg, k, cap, sig_bytes, algo, seed=None, fixed_bound=None, horizon=0, tile="auto"):
     rows = to_rows(data)
     seed = cfg.seed if seed is None else seed
     m = oracle_bounds(data, fixed_bound)
@@ -46,7 +46,7 @@ def _run(wmh, data, cfg, k, cap, sig_bytes, algo, seed=None, fixed_bound=None, h
     L = oracle.Layout(m)
     assert layout.M == L.M
     try:
-        sig = wmh.hash(layout, rows, seed, k, cap, sig_bytes, algo=algo, horizon=horizon)
+        sig = wmh.hash(layout, rows, seed, k, cap, sig_bytes, algo=algo, horizon=horizon, tile=tile)
     except wmh.WmhError as e:
         if algo == "tiled" and "does not take" in str(e):
             pytest.skip("tiled kernel does not take this shape")
@@ -167,6 +167,29 @@ def test_hash_edge_cases_dense(wmh, algo):
     layout = wmh.prepare(bounds=torch.full((D,), 8, dtype=torch.uint32).cuda())
     out = wmh.hash(layout, wmh.Rows.from_dense(torch.zeros((0, D), dtype=torch.uint8).cuda()), 1, 8, 100, algo=algo)
     assert out.shape == (0, 8)
+
+
+@pytest.mark.parametrize("tile", ["bitplanes", "bytes"])
+@pytest.mark.parametrize("D,n", [(64, 333), (1024, 200), (2048, 100), (4096, 70)])
+@pytest.mark.parametrize("mx", [1, 2, 3, 7, 12, 16, 31, 50, 100, 255])
+def test_tiled_bitplanes(wmh, D, n, mx, tile):
+    """Both dense tiles; the bit-sliced one (hash_tiled_bs.cu) at every plane count NB = 1..8 (the
+    largest bound mx), 8/4/2/1 groups of 32 rows and padded or packed plane blocks (D), ragged last tile, all-zero
+    rows, rows at the bound, a small cap and the uint8 signature width."""
+    rng = np.random.default_rng(1000 * mx + D)
+    x = rng.integers(0, mx + 1, size=(n, D)).astype(np.uint8)
+    x[rng.random((n, D)) < 0.7] = 0
+    x[3] = 0
+    x[n - 1] = 0
+    x[4] = mx
+    x[0, 0] = mx                               # the largest bound is mx
+    data = datagen.Dense(x)
+    cfg = datagen.Config("bs", n, D, 1, 255, 1)
+    for k, cap, sb in [(40, 65535, 2), (24, 9, 1)]:
+        sig, L, _ = _run(wmh, data, cfg, k, cap, sb, "tiled", seed=mx + 7, tile=tile)
+        _assert_sig_equal(sig, oracle_hash(L, data, mx + 7, k, cap), f"{tile} D={D} mx={mx} k={k} cap={cap}")
+        s = sig.cpu().numpy()
+        assert np.all(s[[3, n - 1]] == cap) and np.all(s[4] == 1)
 
 
 @pytest.mark.parametrize("algo", ALGOS)
