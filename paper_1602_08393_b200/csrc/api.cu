@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -329,6 +330,7 @@ extern "C" wmh_status wmh_hash(const wmh_layout *L, const wmh_rows *rows, uint64
 // transfers of neighbouring chunks overlap each other and the kernels.
 namespace {
 constexpr int E2E_SLOTS = 3;
+constexpr int E2E_CHUNKS = 8;
 
 struct E2EState {
     int device = -1;
@@ -396,9 +398,43 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     if (h.n_rows == 0) return WMH_OK;
     E2EState &E = g_e2e;
     if ((st = E.init()) != WMH_OK) return st;
-    // chunks of >= 2048 rows, <= 8 of them
-    const int64_t cr = std::max<int64_t>(2048, (h.n_rows + 7) / 8);
-    const int64_t n_chunks = (h.n_rows + cr - 1) / cr;
+    // Chunk boundaries.  The copies of the first chunk in and the last chunk out
+    // are not overlapped by anything, so large batches ramp: chunk sizes in the
+    // proportions 1 2 4 4 4 4 4 4 2 1 (measured on c2: 2.85 ms with 8 equal
+    // chunks against a 2.2 ms PCIe bound); smaller batches use <= E2E_CHUNKS
+    // equal chunks of >= 2048 rows.  WMH_E2E_CHUNKS=n forces n equal chunks.
+    static const int env_chunks = getenv("WMH_E2E_CHUNKS") ? atoi(getenv("WMH_E2E_CHUNKS")) : 0;
+    std::vector<int64_t> cut{0};
+    {
+        static const int ramp[] = {1, 2, 4, 4, 4, 4, 4, 4, 2, 1};
+        constexpr int n_ramp = (int)(sizeof ramp / sizeof ramp[0]);
+        int wsum = 0;
+        for (int i = 0; i < n_ramp; i++) wsum += ramp[i];
+        if (env_chunks <= 0 && h.n_rows >= (int64_t)wsum * 2048) {
+            int acc = 0;
+            for (int i = 0; i < n_ramp; i++) {
+                acc += ramp[i];
+                cut.push_back(h.n_rows * acc / wsum);
+            }
+        } else {
+            const int64_t max_chunks = env_chunks > 0 ? env_chunks : E2E_CHUNKS;
+            const int64_t cr = std::max<int64_t>(2048, (h.n_rows + max_chunks - 1) / max_chunks);
+            for (int64_t b = cr; b < h.n_rows + cr; b += cr) cut.push_back(std::min<int64_t>(b, h.n_rows));
+        }
+    }
+    const int64_t n_chunks = (int64_t)cut.size() - 1;
+    // WMH_E2E_TRACE=1: per-chunk stage times on stderr (timing events; diagnostics only)
+    static const bool trace = getenv("WMH_E2E_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&](cudaStream_t st_) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st_);
+        tev.push_back(e);
+    };
+    const auto host_t0 = std::chrono::steady_clock::now();
+    tmark((cudaStream_t)stream);
     const size_t row_sig = (size_t)k * sig_bytes;
     WMH_CUDA_TRY(cudaEventRecord(E.ev_start, (cudaStream_t)stream), "e2e start event");
     WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_in, E.ev_start, 0), "e2e wait");
@@ -431,7 +467,7 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     }
     for (int64_t ci = 0; ci < n_chunks; ci++) {
         const int slot = (int)(ci % E2E_SLOTS);
-        const int64_t a = ci * cr, b = std::min<int64_t>(h.n_rows, a + cr), nr = b - a;
+        const int64_t a = cut[ci], b = cut[ci + 1], nr = b - a;
         size_t in_bytes, off_col = 0, off_val = 0;
         int64_t e0 = 0, e1 = 0;
         const size_t wb = (size_t)weight_bytes(h);
@@ -466,6 +502,7 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
             d.val = base + off_val;
             d.nnz = e1 - e0;
         }
+        tmark(E.s_in);
         WMH_CUDA_TRY(cudaEventRecord(E.ev_in[slot], E.s_in), "e2e event");
         WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_comp, E.ev_in[slot], 0), "e2e wait");
         void *dsig = base + in_bytes;
@@ -479,13 +516,28 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
             st = hash_dispatch(L, &d, seed, k, cap, sig_bytes, dsig, nullptr, WMH_ALGO_AUTO, 0, 0, E.s_comp, &used);
         }
         if (st != WMH_OK) return st;
+        tmark(E.s_comp);
         WMH_CUDA_TRY(cudaEventRecord(E.ev_comp[slot], E.s_comp), "e2e event");
         WMH_CUDA_TRY(cudaStreamWaitEvent(E.s_out, E.ev_comp[slot], 0), "e2e wait");
         WMH_CUDA_TRY(cudaMemcpyAsync((uint8_t *)sig_out_host + a * row_sig, dsig, nr * row_sig, cudaMemcpyDeviceToHost, E.s_out), "e2e D2H signatures");
+        tmark(E.s_out);
         WMH_CUDA_TRY(cudaEventRecord(E.ev_out[slot], E.s_out), "e2e event");
     }
+    const double host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count();
     index_free(ix, E.s_comp);                    // stream-ordered after the last chunk's kernel
     WMH_CUDA_TRY(cudaStreamSynchronize(E.s_out), "e2e synchronize");
+    if (trace && !tev.empty()) {
+        cudaDeviceSynchronize();
+        fprintf(stderr, "[wmh e2e] %lld chunks, host enqueue %.0f us; per chunk (in, comp, out) end ms:", (long long)n_chunks,
+                host_us);
+        for (size_t i = 1; i < tev.size(); i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tev[0], tev[i]);
+            fprintf(stderr, "%s%.3f", (i - 1) % 3 == 0 ? " | " : " ", ms);
+        }
+        fprintf(stderr, "\n");
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
     return WMH_OK;
 }
 

@@ -543,7 +543,11 @@ wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled) {
 
     const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
     const int sms = num_sms();
-    int n_hchunks = (int)max((int64_t)1, min((int64_t)a.k / 8, ((int64_t)sms * 8 + n_tiles - 1) / n_tiles));
+    // >= 8 items per SM for balance, but >= WMH_MIN_HCHUNK hashes per item: each
+    // item stages its whole tile, so small batches must not slice k too thin
+    // (a 3,300-row batch of c2 in 16-hash items ran 3x slower than its share)
+    static const int min_hc = getenv("WMH_MIN_HCHUNK") ? std::max(8, atoi(getenv("WMH_MIN_HCHUNK"))) : 128;
+    int n_hchunks = (int)max((int64_t)1, min((int64_t)(a.k + min_hc - 1) / min_hc, ((int64_t)sms * 8 + n_tiles - 1) / n_tiles));
     static const int hc_env = getenv("WMH_CM_HCHUNKS") ? atoi(getenv("WMH_CM_HCHUNKS")) : 0;
     if (hc_env > 0) n_hchunks = (int)min((int64_t)hc_env, (int64_t)(a.k + CM_HB - 1) / CM_HB);
     const int hchunk = (int)(((a.k + n_hchunks - 1) / n_hchunks + CM_HB - 1) / CM_HB * CM_HB);   // blocks stay 4-aligned

@@ -254,6 +254,27 @@ def test_hash_host_e2e_equals_device(wmh):
     assert torch.equal(dev, wmh.hash_host(layout, hr, 1, 20, 65535))
 
 
+def test_hash_host_e2e_ramped_chunks(wmh):
+    """Batches of >= 30 * 2048 rows go through wmh_hash_host in ramped chunks
+    (sizes 1 2 4 ... 4 2 1): every row's signatures equal the device path's,
+    dense (tile) and CSR (index built once)."""
+    rng = np.random.default_rng(21)
+    n, D = 70001, 64
+    x = (rng.integers(0, 16, size=(n, D)) * (rng.random((n, D)) < 0.5)).astype(np.uint8)
+    rows = wmh.Rows.from_dense(torch.from_numpy(x).cuda())
+    layout = wmh.prepare(rows)
+    dev = wmh.hash(layout, rows, 5, 24, 65535).cpu()
+    host = wmh.hash_host(layout, wmh.Rows.from_dense(torch.from_numpy(x).pin_memory()), 5, 24, 65535)
+    assert torch.equal(dev, host)
+    cfg, c = datagen.make("c3", n_rows=62000)
+    rows = to_rows(c)
+    layout = wmh.prepare(rows)
+    dev = wmh.hash(layout, rows, 3, 16, 65535).cpu()
+    hr = wmh.Rows.from_csr(torch.from_numpy(c.row_ptr).pin_memory(), torch.from_numpy(c.col).pin_memory(),
+                           torch.from_numpy(c.val).pin_memory(), c.dim)
+    assert torch.equal(dev, wmh.hash_host(layout, hr, 3, 16, 65535))
+
+
 def test_hash_host_e2e_index_chunks(wmh):
     """wmh_hash_host with CSR rows large enough for AUTO's index kernel: the index
     is built once per call and reused by every row chunk; signatures equal the
