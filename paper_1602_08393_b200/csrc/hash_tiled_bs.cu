@@ -24,6 +24,7 @@
 #include <stdlib.h>
 
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 
@@ -49,20 +50,27 @@ struct BsParams {
     unsigned long long *item_ctr;
 };
 
-template <int NB>
+// The draw word of cell r for NB stored planes.  CLAMP (planes of min(x, 2^NB - 1),
+// the largest bound < 2^(NB + 1)): a draw with off >= 2^NB - 1 cannot be tested
+// on the planes; it is flagged (bit 7) with off - (2^NB - 1) in bits 0..6 and
+// tested on the rows' bytes in global memory (rare: only the top cells of the
+// few columns whose bound exceeds 2^NB - 1).
+template <int NB, bool CLAMP = false>
 __device__ __forceinline__ uint32_t bs_word(uint32_t r, const uint32_t *pack, uint32_t uni_m, uint32_t GN, uint32_t t,
                                             uint32_t cap) {
     const uint2 d = unpack_cell(cell_of(r, pack, uni_m));
-    return ((d.x * GN) << 8) | (t < cap ? (uint32_t)((1 << NB) - 1) - d.y : 0u);
+    constexpr uint32_t TOP = (1u << NB) - 1u;
+    if (CLAMP && t < cap && d.y >= TOP) return ((d.x * GN) << 8) | 0x80u | (d.y - TOP);
+    return ((d.x * GN) << 8) | (t < cap ? TOP - d.y : 0u);
 }
 
-template <int NB>
+template <int NB, bool CLAMP>
 __global__ void bs_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
                                 const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t GN, uint32_t cap) {
     const int64_t total = (int64_t)k * T0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
-        table[i] = bs_word<NB>(draw_r(S, j, t, M), pack, uni_m, GN, t, cap);
+        table[i] = bs_word<NB, CLAMP>(draw_r(S, j, t, M), pack, uni_m, GN, t, cap);
     }
 }
 
@@ -134,12 +142,22 @@ __device__ __forceinline__ void bs_t8(uint32_t &lo, uint32_t &hi) {
     t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
 }
 
-template <int NB>
+template <int NB, bool CLAMP>
 __device__ __forceinline__ uint32_t bs_late(const BsParams &p, uint64_t keyj, uint32_t t, uint32_t GN) {
-    return bs_word<NB>(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m, GN, t, p.cap);
+    return bs_word<NB, CLAMP>(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m, GN, t, p.cap);
 }
 
-template <int NB, int NBS, int G>
+// a flagged draw (CLAMP): x[row][c] > off read from the rows themselves
+template <int NB>
+__device__ __noinline__ uint32_t bs_slow(const BsParams &p, int64_t grow0, int nrg, uint32_t w, uint32_t GN) {
+    const uint32_t c = (w >> 8) / GN, off = (1u << NB) - 1u + (w & 0x7Fu);
+    const uint8_t *xc = p.x + grow0 * (int64_t)p.D + c;
+    uint32_t m = 0;
+    for (int i = 0; i < nrg; i++) m |= (uint32_t)(__ldg(xc + (int64_t)i * p.D) > off) << i;
+    return m;
+}
+
+template <int NB, int NBS, int G, bool CLAMP = false>
 __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams p) {
     constexpr int R = 32 * G, LP = 32 / G, DPL = G;   // rows, lanes per group, draws per lane per round
     extern __shared__ __align__(16) uint32_t smem[];
@@ -195,6 +213,7 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 const bool ok = rb + i < nr;
                 w[i] = ok ? __ldg(reinterpret_cast<const uint32_t *>(p.x + (row0 + rb + i) * (int64_t)p.D) + cq) : 0u;
                 live |= (w[i] != 0u) << i;
+                if (CLAMP) w[i] = __vminu4(w[i], ((1u << NB) - 1u) * 0x01010101u);
             }
             if (live) atomicOr(&s_live[g], live << (8 * o));
             // 4x4 byte transposes: col[u4] = byte u4 of rows 0..3 (lo) and 4..7 (hi)
@@ -292,7 +311,7 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 } else {
 #pragma unroll
                     for (int i = 0; i < DPL; i++)
-                        wd[i] = t0 + i < (uint32_t)T0 ? sbuf[t0 + i] : bs_late<NB>(p, keyj, t0 + i, GN);
+                        wd[i] = t0 + i < (uint32_t)T0 ? sbuf[t0 + i] : bs_late<NB, CLAMP>(p, keyj, t0 + i, GN);
                 }
                 uint32_t xv[DPL][NB];
 #pragma unroll
@@ -300,7 +319,8 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 uint32_t F[DPL], any = 0;
 #pragma unroll
                 for (int i = 0; i < DPL; i++) {
-                    const uint32_t gm = bs_test<NB>(xv[i], wd[i]);
+                    uint32_t gm = bs_test<NB>(xv[i], wd[i]);
+                    if (CLAMP && (wd[i] & 0x80u)) gm = bs_slow<NB>(p, row0 + 32 * g, min(32, nr - 32 * g), wd[i], GN);
                     F[i] = gm & ~any;
                     any |= gm;
                 }
@@ -386,9 +406,9 @@ static size_t bs_smem(int D, int G, int NBS) {
     return (((size_t)D * G * NBS + 3) & ~(size_t)3) * 4 + (size_t)BS_NW * T0 * 4 + (size_t)BS_NW * BS_HB * 32 * G * 2;
 }
 
-template <int NB, int NBS, int G>
+template <int NB, int NBS, int G, bool CLAMP = false>
 static void bs_launch(const BsParams &p, size_t smem, int grid, cudaStream_t s) {
-    auto kern = hash_tiled_bs_kernel<NB, NBS, G>;
+    auto kern = hash_tiled_bs_kernel<NB, NBS, G, CLAMP>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel_timer_begin(s);
     kern<<<grid, BS_NT, smem, s>>>(p);
@@ -413,19 +433,22 @@ static void bs_launch_nb(int NBS, int G, const BsParams &p, size_t smem, int gri
             else if (G == 2) bs_launch<NB, 8, 2>(p, smem, grid, s);
             else bs_launch<NB, 8, 1>(p, smem, grid, s);
         }
-    } else {
+    } else if (NBS == NB) {
         if constexpr (NB > 4 && NB < 8) {
             if (G == 2) bs_launch<NB, NB, 2>(p, smem, grid, s);
             else bs_launch<NB, NB, 1>(p, smem, grid, s);
         }
+    } else {                                     // NBS = -NB: clamped planes, 2 groups
+        if constexpr (NB >= 4 && NB < 8) bs_launch<NB, NB, 2, true>(p, smem, grid, s);
     }
 }
 
 template <int NB>
-static void bs_table(uint32_t *table, const HashArgs &a, uint32_t uni_m, uint32_t GN, cudaStream_t s) {
+static void bs_table(uint32_t *table, const HashArgs &a, uint32_t uni_m, uint32_t GN, bool clamp, cudaStream_t s) {
     const int64_t total = (int64_t)a.k * T0;
     const int blocks = (int)min((int64_t)num_sms() * 8, (total + 255) / 256);
-    bs_table_kernel<NB><<<blocks, 256, 0, s>>>(table, a.k, a.S, (uint32_t)a.L->M, a.L->cell_pack, uni_m, GN, a.cap);
+    if (clamp) bs_table_kernel<NB, true><<<blocks, 256, 0, s>>>(table, a.k, a.S, (uint32_t)a.L->M, a.L->cell_pack, uni_m, GN, a.cap);
+    else bs_table_kernel<NB, false><<<blocks, 256, 0, s>>>(table, a.k, a.S, (uint32_t)a.L->M, a.L->cell_pack, uni_m, GN, a.cap);
 }
 
 #define WMH_BS_NB_SWITCH(NBV, CALL) \
@@ -456,13 +479,28 @@ wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled) {
     if (g_env > 0 && g_env <= G && (g_env & (g_env - 1)) == 0) G = g_env;
     while (G >= 1 && bs_smem(D, G, NBS) > (size_t)smem_optin) G /= 2;
     if (G < 2 && NB > 4 && NB < 8 && bs_smem(D, 2, NB) <= (size_t)smem_optin) { NBS = NB; G = 2; }
+    // still one group: NB - 1 planes of min(x, 2^(NB-1) - 1) when the draws they
+    // cannot decide (the top cells of the columns with m_c >= 2^(NB-1)) are rare
+    int NBP = NB;                                // planes stored and tested
+    bool clamp = false;
+    if (G < 2 && NB >= 5 && bs_smem(D, 2, NB - 1) <= (size_t)smem_optin) {
+        std::vector<uint32_t> hb((size_t)D);
+        WMH_CUDA_TRY(cudaMemcpyAsync(hb.data(), a.L->bounds, sizeof(uint32_t) * D, cudaMemcpyDeviceToHost, a.stream), "bounds D2H");
+        WMH_CUDA_TRY(cudaStreamSynchronize(a.stream), "bounds D2H sync");
+        const uint32_t top = (1u << (NB - 1)) - 1u;
+        uint64_t flagged = 0;
+        for (uint32_t m : hb) flagged += m > top ? m - top : 0u;
+        static const double max_frac = getenv("WMH_BS_CLAMP_FRAC") ? atof(getenv("WMH_BS_CLAMP_FRAC")) : 1e-3;
+        if ((double)flagged <= max_frac * (double)a.L->M) { NBP = NB - 1; NBS = -NBP; G = 2; clamp = true; }
+    }
     if (G < 1 && NB > 4 && NB < 8 && bs_smem(D, 1, NB) <= (size_t)smem_optin) { NBS = NB; G = 1; }
     if (G < 1) return WMH_OK;
     // auto choice: a one-group tile (32 rows, one draw per lane per round) loses
     // to the byte tile (c5 at full size, NB = 7: 498 vs 377 ms)
     if (a.tile != 2 && G < 2) return WMH_OK;
-    if ((uint64_t)D * G * NBS >= (1ull << 24)) return WMH_OK;
-    const size_t smem = bs_smem(D, G, NBS);
+    const int NBSW = NBS < 0 ? -NBS : NBS;        // words per (column, group) block
+    if ((uint64_t)D * G * NBSW >= (1ull << 23)) return WMH_OK;
+    const size_t smem = bs_smem(D, G, NBSW);
     const int R = 32 * G;
     *handled = true;
 
@@ -485,9 +523,9 @@ wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled) {
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "tiled counter memset");
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
-    const uint32_t GN = (uint32_t)(G * NBS);
-#define WMH_BS_TAB(V) bs_table<V>(table, a, uni_m, GN, a.stream)
-    WMH_BS_NB_SWITCH(NB, WMH_BS_TAB)
+    const uint32_t GN = (uint32_t)(G * NBSW);
+#define WMH_BS_TAB(V) bs_table<V>(table, a, uni_m, GN, clamp, a.stream)
+    WMH_BS_NB_SWITCH(NBP, WMH_BS_TAB)
 #undef WMH_BS_TAB
     count_launch();
     if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(scratch, a.stream); return cuda_fail(cudaGetLastError(), "bs table launch"); }
@@ -517,11 +555,11 @@ wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled) {
     p.item_ctr = ctr;
     const int grid = (int)min((int64_t)sms, p.n_items);
 #define WMH_BS_GO(V) bs_launch_nb<V>(NBS, G, p, smem, grid, a.stream)
-    WMH_BS_NB_SWITCH(NB, WMH_BS_GO)
+    WMH_BS_NB_SWITCH(NBP, WMH_BS_GO)
 #undef WMH_BS_GO
     WMH_LAUNCH_CHECK("hash_tiled_bs launch");
     if (getenv("WMH_TILED_STATS"))
-        fprintf(stderr, "[wmh tiled bs] NB=%d NBS=%d G=%d grid=%d items=%lld hchunk=%d smem=%zu\n", NB, NBS, G, grid,
+        fprintf(stderr, "[wmh tiled bs] NB=%d planes=%d NBS=%d G=%d grid=%d items=%lld hchunk=%d smem=%zu\n", NB, NBP, NBS, G, grid,
                 (long long)p.n_items, hchunk, smem);
     cudaFreeAsync(scratch, a.stream);
     return WMH_OK;

@@ -192,6 +192,32 @@ def test_tiled_bitplanes(wmh, D, n, mx, tile):
         assert np.all(s[[3, n - 1]] == cap) and np.all(s[4] == 1)
 
 
+@pytest.mark.parametrize("tile", ["bitplanes", "auto"])
+def test_tiled_bitplanes_clamped(wmh, tile, capfd, monkeypatch):
+    """Long rows whose largest bound needs one plane more than two groups can
+    hold (D = 4096, bounds <= 63 except two columns at 100): the planes store
+    min(x, 63) and the draws that land in the top cells of the two wide columns
+    (off >= 63) are tested on the rows themselves.  Bit-exact with the oracle,
+    with rows that are green only in those cells."""
+    monkeypatch.setenv("WMH_TILED_STATS", "1")
+    rng = np.random.default_rng(77)
+    n, D = 70, 4096
+    x = (rng.integers(1, 64, size=(n, D)) * (rng.random((n, D)) < 0.05)).astype(np.uint8)
+    x[:, 7] = np.where(np.arange(n) % 2 == 0, 100, 0)
+    x[:, 2000] = np.where(np.arange(n) % 3 == 0, 90, 5)
+    x[10] = 0
+    x[10, 7] = 100                               # green only in column 7, 37 of its cells above 63
+    x[11] = 0
+    x[11, 2000] = 90
+    data = datagen.Dense(x)
+    cfg = datagen.Config("bsc", n, D, 1, 255, 1)
+    for k, cap in [(64, 65535), (16, 300)]:
+        sig, L, _ = _run(wmh, data, cfg, k, cap, 2, "tiled", seed=31, tile=tile)
+        _assert_sig_equal(sig, oracle_hash(L, data, 31, k, cap), f"clamped {tile} k={k}")
+    err = capfd.readouterr().err
+    assert "planes=6" in err and "NB=7" in err, err[-300:]
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_hash_edge_cases_csr(wmh, algo):
     rng = np.random.default_rng(13)
