@@ -408,8 +408,10 @@ __device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long lo
 // flat index base + f, its range found from the boundaries that fall inside
 // the window (one shared load, one OR-reduction, one popc) -- and fold each
 // (j, t) into h[j] = min(h[j], t) with a shared-memory atomic.
+// register budget: 64 at 1 and 8 warps, 48 at 2 and 4 (ptxas' own choice
+// spilled the 8-warp variant at 48; 40 at 2 warps ran c3 19% slower)
 template <int SIGB, bool CSR, int NW, typename W>
-__global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
+__global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(const IxParams p) {
     const W *pval = reinterpret_cast<const W *>(p.val);
     constexpr int NT = NW * 32, ITEMS = 8, CAPR = NT * ITEMS;
     extern __shared__ uint32_t smem[];
@@ -418,7 +420,7 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
     uint32_t *rp = ra + CAPR;                    // [CAPR + 33] exclusive prefix of range lengths, FULL-padded
     uint32_t *scol_buf = rp + CAPR + 33;         // [capn] staged CSR columns
     __shared__ long long s_row;
-    __shared__ uint32_t s_nu;
+    __shared__ uint32_t s_nu, s_qhead;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lanemask_le = lane == 31 ? FULL : ((2u << lane) - 1u);
     unsigned long long sat = 0;
@@ -562,12 +564,12 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
             if (T < p.cap) {
                 // ---- Alg. 3's loop from t = T for the hashes still without a green
                 //      draw: their ids are gathered into a shared list (ra[] is free
-                //      now), and each warp runs IX_FB of them at once, lane = draw
-                //      (IX_FB independent lookups in flight per lane)
+                //      now); each warp keeps IX_FB of them in flight, lane = draw
+                //      (IX_FB independent lookups per lane), refilling from the list
                 const uint32_t *scol = staged ? scol_buf : nullptr;
                 uint32_t *list = ra;
                 for (;;) {
-                    if (threadIdx.x == 0) s_nu = 0;
+                    if (threadIdx.x == 0) { s_nu = 0; s_qhead = 0; }
                     __syncthreads();
                     for (uint32_t jb = warp * 32; jb < p.k; jb += NT) {
                         const uint32_t jl = jb + lane;
@@ -582,6 +584,76 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
                     __syncthreads();
                     const uint32_t U = min(s_nu, (uint32_t)CAPR);
                     if (U == 0) break;
+                    if constexpr (NW < 8) {
+                    // IX_FB slots per warp, each with its own hash and draw position;
+                    // a slot whose hash resolves (or reaches the cap) takes the next
+                    // hash from the shared queue at once, so no warp idles behind
+                    // another's geometric tail
+                    uint32_t jq[IX_FB], tq[IX_FB];
+                    unsigned live = 0;
+                    {
+                        uint32_t q0 = 0;
+                        if (lane == 0) q0 = atomicAdd(&s_qhead, (uint32_t)IX_FB);
+                        q0 = __shfl_sync(FULL, q0, 0);
+#pragma unroll
+                        for (int q = 0; q < IX_FB; q++) {
+                            jq[q] = q0 + q < U ? list[q0 + q] : 0u;
+                            tq[q] = T;
+                            if (q0 + q < U) live |= 1u << q;
+                        }
+                    }
+                    while (live) {
+                        uint32_t c[IX_FB], off[IX_FB];
+#pragma unroll
+                        for (int q = 0; q < IX_FB; q++) {
+                            c[q] = 0;
+                            off[q] = 0xFFFFFFFFu;
+                            const uint32_t t = tq[q] + lane;
+                            if ((live >> q) & 1u) {
+                                if (t < (uint32_t)T0) {                // the call's table of the first draws
+                                    const uint2 d = __ldg(p.table + (uint64_t)jq[q] * T0 + t);
+                                    c[q] = d.x;
+                                    off[q] = d.y;
+                                } else if (t < p.cap) {
+                                    const uint2 cell = cell_lookup(
+                                        mulhi_range(splitmix64(p.S ^ ((uint64_t)jq[q] << 32) ^ (uint64_t)t), p.M),
+                                        p.pack, p.uni_m, p.i2c, p.comp_to_m);
+                                    c[q] = cell.x;
+                                    off[q] = cell.y;
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < IX_FB; q++) {
+                            if (!((live >> q) & 1u)) continue;
+                            const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q]);
+                            const unsigned gm = __ballot_sync(FULL, g);
+                            bool done = false;
+                            if (gm) {
+                                if (lane == 0) h[jq[q]] = tq[q] + __ffs(gm) - 1;
+                                done = true;
+                            } else {
+                                tq[q] += 32;
+                                if (tq[q] >= p.cap) {                  // no green draw before the cap
+                                    if (lane == 0) h[jq[q]] = IX_SAT;
+                                    done = true;
+                                }
+                            }
+                            if (done) {                                // refill the slot
+                                uint32_t nx = 0;
+                                if (lane == 0) nx = atomicAdd(&s_qhead, 1u);
+                                nx = __shfl_sync(FULL, nx, 0);
+                                if (nx < U) {
+                                    jq[q] = list[nx];
+                                    tq[q] = T;
+                                } else {
+                                    live &= ~(1u << q);
+                                }
+                            }
+                        }
+                    }
+                    } else {
+                    // 8 warps: static batches of IX_FB hashes (measured: c4 20.3 vs 21.0 ms with the refill)
                     for (uint32_t ub = warp * IX_FB; ub < U; ub += NT / 32 * IX_FB) {
                         uint32_t jq[IX_FB];
                         unsigned live = 0;
@@ -625,6 +697,7 @@ __global__ void __launch_bounds__(NW * 32) hash_index_kernel(const IxParams p) {
 #pragma unroll
                         for (int q = 0; q < IX_FB; q++)
                             if (((live >> q) & 1u) && lane == 0) h[jq[q]] = IX_SAT;   // no green draw before the cap
+                    }
                     }
                     __syncthreads();
                     if (s_nu <= (uint32_t)CAPR) break;
