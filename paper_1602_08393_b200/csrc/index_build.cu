@@ -47,14 +47,12 @@ struct X3Inst {
     int e;
 };
 
-__device__ __forceinline__ X3Inst x3_inst(const X3Params &p, uint64_t i) {
-    int e = 0;
-#pragma unroll
-    for (int q = 1; q < IX_MAXE; q++)
-        if (q < p.E && i >= p.ibase[q]) e = q;
-    const uint64_t w = i - p.ibase[e];
+// instance i (a thread visits increasing i: e advances from the previous call's)
+__device__ __forceinline__ X3Inst x3_inst(const X3Params &p, uint64_t i, int &e) {
+    while (e + 1 < p.E && i >= p.ibase[e + 1]) e++;
+    const uint32_t w = (uint32_t)(i - p.ibase[e]);     // < k * B[e+1] <= 2^16 * 2^16
     const uint32_t Bn = p.B[e + 1];
-    const uint32_t j = (uint32_t)(w / Bn), t = (uint32_t)(w - (uint64_t)j * Bn);
+    const uint32_t j = w / Bn, t = w - j * Bn;
     X3Inst o;
     o.val = (j << 16) | t;
     o.r = mulhi_range(splitmix64(p.S ^ ((uint64_t)j << 32) ^ (uint64_t)t), p.M);
@@ -121,8 +119,9 @@ __global__ void __launch_bounds__(X3_T) x3_count(const X3Params p, uint32_t *__r
     for (uint32_t i = threadIdx.x; i < p.n_chunks + p.n_super; i += X3_T) sm[i] = 0;
     __syncthreads();
     const uint64_t i0 = (uint64_t)blockIdx.x * p.per_cta, i1 = min(p.n_inst, i0 + p.per_cta);
+    int ee = 0;
     for (uint64_t i = i0 + threadIdx.x; i < i1; i += X3_T) {
-        const X3Inst x = x3_inst(p, i);
+        const X3Inst x = x3_inst(p, i, ee);
         const uint32_t loc = x.r >> p.cb[x.e];
         atomicAdd(cc + p.cbase[x.e] + loc, 1u);
         atomicAdd(sc + p.sbase[x.e] + loc / X3_GS, 1u);
@@ -144,6 +143,7 @@ __global__ void __launch_bounds__(X3_T) x3_partition(const X3Params p, const uin
     uint32_t *ss = sv + X3_NB;                  // [X3_NB] their super-chunks
     for (uint32_t s = threadIdx.x; s < p.n_super; s += X3_T) cur[s] = Hs[(uint64_t)s * p.n_cta + blockIdx.x];
     const uint64_t i0 = (uint64_t)blockIdx.x * p.per_cta, i1 = min(p.n_inst, i0 + p.per_cta);
+    int ee = 0;
     for (uint64_t b0 = i0; b0 < i1; b0 += X3_NB) {
         const uint32_t nb = (uint32_t)min((uint64_t)X3_NB, i1 - b0);
         for (uint32_t s = threadIdx.x; s < p.n_super; s += X3_T) cnt[s] = 0;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(X3_T) x3_partition(const X3Params p, const uin
             const uint32_t li = threadIdx.x + q * X3_T;
             mys[q] = 0xFFFFFFFFu;
             if (li < nb) {
-                const X3Inst x = x3_inst(p, b0 + li);
+                const X3Inst x = x3_inst(p, b0 + li, ee);
                 myv[q] = x.val;
                 mys[q] = p.sbase[x.e] + (x.r >> p.cb[x.e]) / X3_GS;
                 atomicAdd(cnt + mys[q], 1u);
