@@ -15,7 +15,7 @@
 // against 32 rows -- against ~2 per row for the byte-SWAR tile.
 //
 // A warp takes one hash for the whole tile (G groups of 32 rows): lane =
-// (group, part), each lane draws DPL = G consecutive t of the round's 32, the
+// (group, part), each lane draws DPL consecutive t of the group's round, the
 // parts of a group combine their green masks with a segmented prefix OR, and
 // the first green t of each pending row is recorded (h = t + 1, Alg. 3 / Def.,
 // P:166-188).  Rows stay pending until green or the cap (h = cap, reading R9);
@@ -33,6 +33,12 @@ namespace wmh {
 constexpr int BS_NT = 512;
 constexpr int BS_NW = BS_NT / 32;
 constexpr int BS_HB = 8;                 // hashes per claimed block (results flushed 8 per row)
+// draws per lane per round by groups per tile (a round of a group = 32 / G
+// lanes x DPL draws): longer rounds amortise the per-round scan and test
+// setup against draws tested past a group's last first-green.  Measured on
+// c5 (G = 2): DPL 2 / 4 / 8 -> 334 / 313 / 329 ms; on c2 (G = 4): 4 beats 8
+// (0.75 vs 0.81 ms)
+__host__ __device__ constexpr int bs_dpl(int G) { return G == 1 ? 2 : G == 2 ? 4 : G == 4 ? 4 : 8; }
 
 struct BsParams {
     const uint8_t *x;
@@ -159,7 +165,9 @@ __device__ __noinline__ uint32_t bs_slow(const BsParams &p, int64_t grow0, int n
 
 template <int NB, int NBS, int G, bool CLAMP = false>
 __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams p) {
-    constexpr int R = 32 * G, LP = 32 / G, DPL = G;   // rows, lanes per group, draws per lane per round
+    // rows, lanes per group, draws per lane per round, draws per group per round
+    constexpr int R = 32 * G, LP = 32 / G, DPL = bs_dpl(G), RD = LP * DPL;
+    static_assert(DPL <= 16, "the record loop decodes 4 bits of draw index");
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *planes = smem;                                                       // [D][G][NBS]
     const size_t pl_words = ((size_t)p.D * G * NBS + 3) & ~(size_t)3;
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 sat += __popc(dead);
             }
             uint32_t pend = pend0;
-            for (uint32_t tb = 0;; tb += 32) {
+            for (uint32_t tb = 0;; tb += RD) {
                 if (!__any_sync(0xFFFFFFFFu, pend != 0u)) break;
                 if (tb >= p.cap) {                     // a9: no green draw before the cap
                     if (part == 0) {
@@ -305,7 +313,7 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 const uint32_t t0 = tb + (uint32_t)(part * DPL);
                 // all DPL draw words, then all plane loads, then the tests (loads in flight together)
                 uint32_t wd[DPL];
-                if (tb + 32 <= (uint32_t)T0) {
+                if (tb + RD <= (uint32_t)T0) {
 #pragma unroll
                     for (int i = 0; i < DPL; i++) wd[i] = sbuf[t0 + i];
                 } else {
@@ -336,16 +344,18 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 // rows first green in this lane's draws: one loop over all of them,
                 // the draw index i from its bits (the F[i] are disjoint)
                 uint32_t n = any & ~excl & pend;
-                uint32_t B0 = 0, B1 = 0, B2 = 0;
+                uint32_t B0 = 0, B1 = 0, B2 = 0, B3 = 0;
 #pragma unroll
                 for (int i = 1; i < DPL; i++) {
                     if (i & 1) B0 |= F[i];
                     if (i & 2) B1 |= F[i];
                     if (i & 4) B2 |= F[i];
+                    if (i & 8) B3 |= F[i];
                 }
                 while (n) {
                     const int b = __ffs(n) - 1;
-                    const uint32_t i = ((B0 >> b) & 1u) | (((B1 >> b) & 1u) << 1) | (((B2 >> b) & 1u) << 2);
+                    const uint32_t i = ((B0 >> b) & 1u) | (((B1 >> b) & 1u) << 1) | (((B2 >> b) & 1u) << 2) |
+                                       (((B3 >> b) & 1u) << 3);
                     hres[32 * g + b] = (uint16_t)(t0 + i + 1);
                     n &= n - 1;
                 }
@@ -355,7 +365,6 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
             if (j + 1 == je) {
                 // ---- a9: flush the block: row r's hashes jb..je-1 are contiguous in sig
                 const int64_t eoff = (row0 + lane) * (int64_t)p.k + jb;
-                const int64_t step = 32 * (int64_t)p.k;
                 const int nh = (int)(je - jb);
                 if (nh == BS_HB && p.vec_flush) {
                     for (int r = lane; r < nr; r += 32) {
