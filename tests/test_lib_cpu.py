@@ -107,3 +107,14 @@ def test_new_entry_points_validate_without_gpu(lib):
     # no timed hash call on this thread yet
     ms = ctypes.c_float()
     assert lib.wmh_last_kernel_ms(ctypes.byref(ms)) == E
+
+
+def test_tile_option_validated_before_any_call():
+    """hash(tile=...) accepts only auto / bytes / bitplanes (WMH_OPT_TILE_* flags)."""
+    import torch
+    import paper_1602_08393_b200 as wmh
+    from paper_1602_08393_b200 import _lib
+    assert (_lib.WMH_OPT_TILE_BYTES, _lib.WMH_OPT_TILE_BITPLANES) == (2, 4)
+    rows = wmh.Rows.from_dense(torch.zeros((2, 8), dtype=torch.uint8))
+    with pytest.raises(ValueError, match="tile"):
+        wmh.hash(None, rows, 1, 4, 10, tile="diagonal")
