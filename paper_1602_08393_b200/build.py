@@ -38,6 +38,20 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
+    # one builder at a time (torchrun starts one process per GPU): the others
+    # wait on the lock and then find the library up to date
+    import fcntl
+    with open(os.path.join(PKG, ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and not needs_build():
+                return SO
+            return _build(verbose)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _build(verbose: bool) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
