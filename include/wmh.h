@@ -169,7 +169,9 @@ typedef enum {
     WMH_ALGO_TILED = 2,  /* rows staged in shared memory, draws shared by a tile  */
     WMH_ALGO_INDEX = 3   /* draws (j, t < T) filed once per call under their cell; a
                             row visits only its green draws, then Alg. 3's loop from
-                            t = T for hashes still unresolved (k <= 65536)           */
+                            t = T for hashes still unresolved; k up to ~54,000 on
+                            B200: h[k] lives in shared memory -- AUTO then picks
+                            another kernel, an explicit request gets WMH_EINVAL) */
 } wmh_algo;
 
 typedef struct {
@@ -208,7 +210,8 @@ wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t 
  * hasher keeps a pointer to `layout` (keep it alive) and its device index
  * (freed by wmh_hasher_free, which synchronises the device).  Runs on one
  * hasher must not overlap in time (they share a row counter): issue them on
- * one stream.  Errors: as wmh_hash; k <= 65536. */
+ * one stream.  Errors: as wmh_hash; k within the index kernel's limit
+ * (WMH_ALGO_INDEX). */
 typedef struct wmh_hasher wmh_hasher;
 wmh_status wmh_hasher_create(const wmh_layout *layout, uint64_t seed, uint32_t k, uint32_t cap, uint32_t horizon,
                              wmh_hasher **out, void *stream);

@@ -25,6 +25,7 @@ void set_error(const char *fmt, ...) {
 
 wmh_status cuda_fail(cudaError_t e, const char *what) {
     set_error("%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
+    (void)cudaGetLastError();                    // a non-sticky error must not resurface in the next call's check
     return e == cudaErrorMemoryAllocation ? WMH_ENOMEM : WMH_ECUDA;
 }
 
@@ -215,7 +216,7 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     const bool sparse_dense = rows->kind == WMH_DENSE && L->mean_s >= 0.0 && L->mean_s < 0.01;
     // uint16 weights / bounds above 255 (fixed-point real data): index or simple
     const bool wide = (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(*rows) != 1;
-    if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense || wide) && k <= 65536) {
+    if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense || wide) && k <= index_k_max()) {
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
     }
@@ -442,7 +443,7 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     // the index kernel (AUTO's choice for CSR rows) files the draws once for the
     // whole call; every chunk then only runs its rows kernel
     const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.01) ||
-                            (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && k <= 65536 &&
+                            (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && k <= index_k_max() &&
                            !tiny_batch(L, &h, k, cap);
     IndexBuilt ix;
     struct IxGuard {                             // frees the index on every return path

@@ -740,6 +740,11 @@ static wmh_status ix_launch(IxParams p, cudaStream_t s) {
         p.capn = p.D <= stage_max ? (int)((p.D * (int64_t)sizeof(W) + 3) / 4) : 0;
     }
     const size_t smem = (size_t)p.k * 4 + (size_t)(2 * NW * 32 * 8 + 33) * 4 + (size_t)p.capn * 4;
+    {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (smem > (size_t)optin) { set_error("wmh_hash: k=%u needs %zu B of shared memory per row", p.k, smem); return WMH_EINVAL; }
+    }
     WMH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "index smem attr");
     int per_sm = 0;
     WMH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem), "index occupancy");
@@ -802,9 +807,26 @@ static IxEpochs index_epochs(uint32_t T) {
     return ep;
 }
 
+// The largest k the rows kernel takes: its shared memory holds h[k] (4 B per
+// hash) next to the 8-warp range buffers; also bounded by the 16-bit j of an entry.
+uint32_t index_k_max() {
+    static uint32_t kmax = 0;
+    if (!kmax) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int64_t fixed = (int64_t)(2 * 8 * 32 * 8 + 33) * 4 + 256;     // + the static shared variables
+        kmax = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(65536, ((int64_t)optin - fixed) / 4));
+    }
+    return kmax;
+}
+
 wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
     *out = IndexBuilt();
-    if (a.k > 65536) { set_error("wmh_hash: the index kernel takes k <= 65536"); return WMH_EINVAL; }
+    if (a.k > index_k_max()) {
+        set_error("wmh_hash: the index kernel takes k <= %u (h[k] in shared memory)", index_k_max());
+        return WMH_EINVAL;
+    }
     const wmh_layout *L = a.L;
     const uint32_t M = (uint32_t)L->M;
     const uint32_t T = index_horizon(L, a.k, a.cap, horizon);

@@ -219,6 +219,36 @@ def test_tiled_bitplanes_clamped(wmh, tile, capfd, monkeypatch):
 
 
 @pytest.mark.parametrize("algo", ALGOS)
+def test_hash_maximum_sizes(wmh, algo):
+    """Limits: k = 65536 on CSR rows (the INDEX kernel keeps h[k] in shared
+    memory, so it takes k = 50,000 here and rejects 65,536 with a clean
+    WMH_EINVAL that leaves no error behind; AUTO picks another kernel), and
+    dense rows too long for any shared-memory tile (D = 20000), each bit-exact
+    with the oracle."""
+    rng = np.random.default_rng(99)
+    D = 512
+    dense = ((rng.random((3, D)) < 0.5) * rng.integers(1, 16, (3, D))).astype(np.uint8)
+    rp = np.concatenate([[0], np.cumsum((dense > 0).sum(1))]).astype(np.int64)
+    col = np.concatenate([np.nonzero(r)[0] for r in dense]).astype(np.int32)
+    val = np.concatenate([r[r > 0] for r in dense]).astype(np.uint8)
+    data = datagen.CSR(rp, col, val, D)
+    cfg = datagen.Config("kmax", 3, D, 1, 255, 1)
+    kk = 50000 if algo == "index" else 65536
+    if algo == "index":
+        with pytest.raises(wmh.WmhError, match="index kernel takes k"):
+            _run(wmh, data, cfg, 65536, 65535, 2, algo, seed=4)
+    sig, L, _ = _run(wmh, data, cfg, kk, 65535, 2, algo, seed=4)
+    _assert_sig_equal(sig, oracle_hash(L, data, 4, kk, 65535), f"k={kk}/{algo}")
+    D = 20000
+    x = ((rng.random((40, D)) < 0.3) * rng.integers(1, 16, (40, D))).astype(np.uint8)
+    x[7] = 0
+    data = datagen.Dense(x)
+    cfg = datagen.Config("dlong", 40, D, 1, 255, 1)
+    sig, L, _ = _run(wmh, data, cfg, 24, 65535, 2, algo, seed=6)
+    _assert_sig_equal(sig, oracle_hash(L, data, 6, 24, 65535), f"D=20000/{algo}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
 def test_hash_edge_cases_csr(wmh, algo):
     rng = np.random.default_rng(13)
     D = 5000
