@@ -185,7 +185,7 @@ def test_tiled_bitplanes(wmh, D, n, mx, tile):
     x[0, 0] = mx                               # the largest bound is mx
     data = datagen.Dense(x)
     cfg = datagen.Config("bs", n, D, 1, 255, 1)
-    for k, cap, sb in [(40, 65535, 2), (24, 9, 1)]:
+    for k, cap, sb in [(40, 65535, 2), (24, 9, 1), (13, 65535, 2), (5, 200, 1)]:
         sig, L, _ = _run(wmh, data, cfg, k, cap, sb, "tiled", seed=mx + 7, tile=tile)
         _assert_sig_equal(sig, oracle_hash(L, data, mx + 7, k, cap), f"{tile} D={D} mx={mx} k={k} cap={cap}")
         s = sig.cpu().numpy()
