@@ -170,8 +170,10 @@ typedef enum {
     WMH_ALGO_INDEX = 3   /* draws (j, t < T) filed once per call under their cell; a
                             row visits only its green draws, then Alg. 3's loop from
                             t = T for hashes still unresolved; k up to ~54,000 on
-                            B200: h[k] lives in shared memory -- AUTO then picks
-                            another kernel, an explicit request gets WMH_EINVAL) */
+                            B200 (h[k] lives in shared memory) and a key space
+                            E*M <= 5.4e8 cells (E = 1..10 nested epochs): beyond
+                            either AUTO picks another kernel and an explicit
+                            request gets WMH_EINVAL */
 } wmh_algo;
 
 typedef struct {

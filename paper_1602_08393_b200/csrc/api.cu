@@ -216,7 +216,8 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     const bool sparse_dense = rows->kind == WMH_DENSE && L->mean_s >= 0.0 && L->mean_s < 0.01;
     // uint16 weights / bounds above 255 (fixed-point real data): index or simple
     const bool wide = (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(*rows) != 1;
-    if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense || wide) && k <= index_k_max()) {
+    if (algo == WMH_ALGO_AUTO && !tiny && (rows->kind == WMH_CSR || sparse_dense || wide) &&
+        index_feasible(L, k, cap, horizon)) {
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
     }
@@ -443,7 +444,7 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     // the index kernel (AUTO's choice for CSR rows) files the draws once for the
     // whole call; every chunk then only runs its rows kernel
     const bool use_index = (h.kind == WMH_CSR || (L->mean_s >= 0.0 && L->mean_s < 0.01) ||
-                            (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && k <= index_k_max() &&
+                            (L->flags & WMH_LAYOUT_WIDE) || weight_bytes(h) != 1) && index_feasible(L, k, cap, 0) &&
                            !tiny_batch(L, &h, k, cap);
     IndexBuilt ix;
     struct IxGuard {                             // frees the index on every return path

@@ -135,6 +135,7 @@ wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled);
 bool tiled_cm_full_tile(const HashArgs &a);
 wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon);
 uint32_t index_k_max();
+bool index_feasible(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t horizon);
 // The index of one call, reusable by several row batches of the same (layout,
 // seed, k, cap): built on a.stream, freed stream-ordered.
 constexpr int IX_MAXE = 10;

@@ -821,6 +821,17 @@ uint32_t index_k_max() {
     return kmax;
 }
 
+// Can the index be built for (layout, k, cap, horizon)?  k within index_k_max(),
+// fewer than 2^32 filed instances, and a key space E*M the direct partition
+// covers (<= 16383 chunks of <= 2^15 cells).  AUTO only picks the index when so.
+bool index_feasible(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t horizon) {
+    if (k > index_k_max()) return false;
+    const IxEpochs ep = index_epochs(index_horizon(L, k, cap, horizon));
+    uint64_t n_inst = 0;
+    for (int e = 0; e < ep.E; e++) n_inst += (uint64_t)k * ep.B[e + 1];
+    return n_inst < (1ull << 32) && (uint64_t)ep.E * L->M <= 16383ull * 32768ull;
+}
+
 wmh_status index_build(const HashArgs &a, uint32_t horizon, IndexBuilt *out) {
     *out = IndexBuilt();
     if (a.k > index_k_max()) {

@@ -248,6 +248,24 @@ def test_hash_maximum_sizes(wmh, algo):
     _assert_sig_equal(sig, oracle_hash(L, data, 6, 24, 65535), f"D=20000/{algo}")
 
 
+def test_index_key_space_limit(wmh):
+    """A key space beyond the index build (D = 2^20 columns at bound 255: M =
+    2.7e8 cells, E*M > 5.4e8): an explicit index request gets a clean
+    WMH_EINVAL, AUTO hashes with another kernel, bit-exact with the oracle."""
+    rng = np.random.default_rng(8)
+    D = 1 << 20
+    rp = np.arange(0, 7 * 3000, 3000, dtype=np.int64)
+    col = np.concatenate([np.sort(rng.choice(D, 3000, replace=False)) for _ in range(6)]).astype(np.int32)
+    val = rng.integers(1, 256, 6 * 3000).astype(np.uint8)
+    data = datagen.CSR(rp, col, val, D)
+    cfg = datagen.Config("widekeys", 6, D, 1, 255, 1)
+    with pytest.raises(wmh.WmhError, match="key space"):
+        _run(wmh, data, cfg, 64, 65535, 2, "index", seed=9, fixed_bound=255)
+    sig, L, _ = _run(wmh, data, cfg, 64, 65535, 2, "auto", seed=9, fixed_bound=255)
+    assert wmh.last_algo != "index"
+    _assert_sig_equal(sig, oracle_hash(L, data, 9, 64, 65535), "wide key space/auto")
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_hash_edge_cases_csr(wmh, algo):
     rng = np.random.default_rng(13)
