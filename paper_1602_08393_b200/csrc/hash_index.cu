@@ -416,7 +416,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
     constexpr int NT = NW * 32, ITEMS = 8, CAPR = NT * ITEMS;
     extern __shared__ uint32_t smem[];
     uint32_t *h = smem;                          // [k] first green t per hash
-    uint32_t *ra = h + p.k;                      // [CAPR] range start (index into vals)
+    uint32_t *ra = h + p.k;                      // [CAPR] range start in vals minus its flat offset (mod 2^32)
     uint32_t *rp = ra + CAPR;                    // [CAPR + 33] exclusive prefix of range lengths, FULL-padded
     uint32_t *scol_buf = rp + CAPR + 33;         // [capn] staged CSR columns
     __shared__ long long s_row;
@@ -513,7 +513,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++)
                     if (len[q]) {
-                        ra[slot] = a[q];
+                        ra[slot] = a[q] - f;
                         rp[slot] = f;
                         slot++;
                         f += len[q];
@@ -546,7 +546,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                             asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(d));
                             const uint32_t m = __reduce_or_sync(FULL, bit);   // uniform
                             const uint32_t own = o + __popc(m & lanemask_le);
-                            addr[u] = ra[own] + (bu + lane - rp[own]);
+                            addr[u] = ra[own] + (bu + lane);                   // = start + (flat - flat start)
                             o += __popc(m);                            // the owner of the next window's base
                         }
                         uint32_t v[IX_U];
