@@ -133,6 +133,14 @@ wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh_rows *rows
 wmh_status wmh_layout_info(const wmh_layout *layout, int64_t *dim, uint64_t *M, uint32_t *flags,
                            uint32_t *uniform_bound);
 
+/* A 64-bit digest of the layout: FNV-1a over dim and the bounds m_c (host
+ * value, computed once by wmh_prepare).  Signatures are comparable only when
+ * made with the same (seed, k, cap) over layouts with equal digests -- equal
+ * bounds give the same M, CompToM and draw stream (SPEC's
+ * same-layout rule).  The Python binding carries it with each
+ * Sketch and refuses to collide mismatched ones.  Errors: NULL arguments. */
+wmh_status wmh_layout_digest(const wmh_layout *layout, uint64_t *digest);
+
 /* Read-only DEVICE views of the layout's tables, for tests: comp_to_m
  * (uint32[dim+1]), int_to_comp (uint32[M]), bounds (uint32[dim]). */
 wmh_status wmh_layout_tables(const wmh_layout *layout, const uint32_t **comp_to_m,

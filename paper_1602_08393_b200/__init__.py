@@ -23,7 +23,8 @@ from . import _lib
 from ._lib import WmhError  # noqa: F401
 
 __all__ = ["Rows", "Layout", "colmax", "reduce_bounds", "shard", "prepare", "hash", "hash_host", "collide", "WmhError",
-           "version", "quantize", "scale_objective", "choose_scale", "LSH", "Hasher", "gather_signatures"]
+           "version", "quantize", "scale_objective", "choose_scale", "LSH", "Hasher", "gather_signatures", "Sketch",
+           "sketch", "collide_sketches"]
 
 
 def _stream(stream=None) -> int:
@@ -113,6 +114,9 @@ class Layout:
         _lib.check(_lib.load().wmh_layout_info(self._h, ctypes.byref(dim), ctypes.byref(M), ctypes.byref(flags),
                                                ctypes.byref(ub)))
         self.dim, self.M, self.flags, self.uniform_bound = dim.value, M.value, flags.value, ub.value
+        dg = ctypes.c_uint64()
+        _lib.check(_lib.load().wmh_layout_digest(self._h, ctypes.byref(dg)))
+        self.digest = dg.value              # FNV-1a over (dim, bounds): the "same layout" key
 
     @property
     def handle(self):
@@ -326,6 +330,40 @@ def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, st
     _lib.check(_lib.load().wmh_collide(_ptr(sig), sb, k, n_rows, _ptr(pairs), P, _ptr(matches), _ptr(jhat),
                                        1 if check_pairs else 0, _stream(stream)))
     return matches, jhat
+
+
+@dataclass
+class Sketch:
+    """Signatures with the metadata that decides whether two sets of them are
+    comparable: the same (seed, k, cap) over layouts with
+    the same digest (equal bounds, hence the same draw stream)."""
+    sig: torch.Tensor
+    seed: int
+    k: int
+    cap: int
+    digest: int
+
+    def key(self):
+        return (self.seed & (2**64 - 1), self.k, self.cap, self.digest)
+
+
+def sketch(layout: Layout, rows: Rows, seed: int, k: int, cap: int, **kw) -> Sketch:
+    """hash() wrapped with its metadata."""
+    return Sketch(hash(layout, rows, seed, k, cap, **kw), seed, k, cap, layout.digest)
+
+
+def collide_sketches(a: Sketch, b: Sketch, ia: torch.Tensor, ib: torch.Tensor, stream=None):
+    """a10 across two sketches: matches / J-hat of rows a.sig[ia[p]] and b.sig[ib[p]].
+    Refuses (ValueError) sketches of a different seed, k, cap or layout."""
+    if a.key() != b.key():
+        names = ("seed", "k", "cap", "layout digest")
+        diff = [n for n, x, y in zip(names, a.key(), b.key()) if x != y]
+        raise ValueError(f"sketches are not comparable: different {', '.join(diff)}")
+    if a.sig.dtype != b.sig.dtype:
+        raise ValueError("sketches have different signature widths")
+    both = torch.cat([a.sig, b.sig])
+    pairs = torch.stack([ia.to(torch.int64), ib.to(torch.int64) + a.sig.shape[0]], dim=1).contiguous()
+    return collide(both, pairs, stream=stream)
 
 
 class Hasher:

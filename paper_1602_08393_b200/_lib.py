@@ -18,7 +18,7 @@ STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 
                 5: "WMH_ECUDA", 6: "WMH_ENOMEM"}
 
 # Every symbol include/wmh.h declares (tests check the .so exports all of them).
-EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_tables", "wmh_layout_free",
+EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_digest", "wmh_layout_tables", "wmh_layout_free",
            "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version",
            "wmh_kernel_launches", "wmh_last_kernel_ms", "wmh_quantize", "wmh_scale_objective", "wmh_lsh_build",
            "wmh_lsh_query", "wmh_lsh_free", "wmh_hasher_create", "wmh_hasher_run", "wmh_hasher_free"]
@@ -64,6 +64,7 @@ def load() -> ctypes.CDLL:
             "wmh_layout_info": (st, [vp, ctypes.POINTER(i64), ctypes.POINTER(u64), ctypes.POINTER(u32),
                                      ctypes.POINTER(u32)]),
             "wmh_layout_tables": (st, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+            "wmh_layout_digest": (st, [vp, ctypes.POINTER(u64)]),
             "wmh_layout_free": (None, [vp]),
             "wmh_hash": (st, [vp, rows_p, u64, u32, u32, i32, vp, vp, vp]),
             "wmh_hash_ex": (st, [vp, rows_p, u64, u32, u32, i32, vp, vp, ctypes.POINTER(WmhHashOpts), vp]),

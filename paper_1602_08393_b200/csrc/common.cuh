@@ -14,6 +14,7 @@ struct wmh_layout {
     uint32_t flags = 0;          // bit 0: uniform bounds
     uint32_t uniform_m = 0;      // the common bound when uniform, else 0
     uint32_t max_bound = 0;      // max_c m_c
+    uint64_t digest = 0;         // FNV-1a over (dim, bounds): wmh_layout_digest
     uint32_t *bounds = nullptr;       // [dim]
     uint32_t *comp_to_m = nullptr;    // [dim + 1]   CompToM, exclusive prefix (Eq. 3)
     uint32_t *int_to_comp = nullptr;  // [M]         IntToComp (Alg. 4)

@@ -3,6 +3,8 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace wmh {
@@ -466,7 +468,26 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     fill_int_to_comp<<<(unsigned)blocks, 256, 0, s>>>(L->comp_to_m, dim, L->int_to_comp, L->cell_pack);
     count_launch();
     if (cudaGetLastError() != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "fill IntToComp launch"));
+    {   // layout digest: FNV-1a (64-bit) over dim and the bounds, for "same layout" checks
+        std::vector<uint32_t> hb((size_t)dim);
+        cudaError_t e1 = cudaMemcpyAsync(hb.data(), L->bounds, sizeof(uint32_t) * dim, cudaMemcpyDeviceToHost, s);
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(cuda_fail(e1 != cudaSuccess ? e1 : e2, "layout digest"));
+        uint64_t h = 0xcbf29ce484222325ull;
+        auto mix = [&](uint64_t v) {
+            for (int i = 0; i < 8; i++) { h ^= (v >> (8 * i)) & 0xFFu; h *= 0x100000001b3ull; }
+        };
+        mix((uint64_t)dim);
+        for (uint32_t b : hb) mix(b);
+        L->digest = h;
+    }
     *out = L;
+    return WMH_OK;
+}
+
+extern "C" wmh_status wmh_layout_digest(const wmh_layout *L, uint64_t *digest) {
+    if (!L || !digest) { set_error("wmh_layout_digest: NULL argument"); return WMH_EINVAL; }
+    *digest = L->digest;
     return WMH_OK;
 }
 

@@ -370,6 +370,34 @@ def test_hash_host_e2e_index_chunks(wmh):
 
 
 # ------------------------------------------------------------------ collide
+def test_sketches_and_layout_digest(wmh):
+    """The layout digest is a function of (dim, bounds): equal for two prepares
+    of the same rows, different when one bound changes.  collide_sketches over
+    two batches equals collide over their concatenation, and refuses a sketch
+    of another layout."""
+    cfg, data = datagen.make("c2", n_rows=300)
+    x = torch.from_numpy(data.x).cuda()
+    la, lb = wmh.prepare(wmh.Rows.from_dense(x[:150])), wmh.prepare(wmh.Rows.from_dense(x))
+    bounds = la.tables()[2].view(torch.int32).clone()
+    l1 = wmh.prepare(bounds=bounds.view(torch.uint32))
+    assert l1.digest == la.digest
+    b2 = bounds.clone()
+    b2[3] += 1
+    assert wmh.prepare(bounds=b2.view(torch.uint32)).digest != la.digest
+    full = wmh.prepare(bounds=lb.tables()[2].view(torch.int32).clone().view(torch.uint32))
+    sa = wmh.sketch(full, wmh.Rows.from_dense(x[:150]), 5, 64, 65535)
+    sb = wmh.sketch(full, wmh.Rows.from_dense(x[150:]), 5, 64, 65535)
+    ia = torch.arange(0, 150, device="cuda")
+    ib = torch.arange(149, -1, -1, device="cuda")
+    m1, j1 = wmh.collide_sketches(sa, sb, ia, ib)
+    allsig = wmh.hash(full, wmh.Rows.from_dense(x), 5, 64, 65535)
+    m2, j2 = wmh.collide(allsig, torch.stack([ia, ib + 150], 1).contiguous())
+    assert torch.equal(m1, m2) and torch.equal(j1, j2)
+    if la.digest != full.digest:
+        with pytest.raises(ValueError, match="layout digest"):
+            wmh.collide_sketches(wmh.sketch(la, wmh.Rows.from_dense(x[:150]), 5, 64, 65535), sb, ia, ib)
+
+
 @pytest.mark.parametrize("sb,k", [(2, 128), (1, 64), (2, 37), (1, 5)])
 def test_collide_matches_oracle(wmh, sb, k):
     """a10 (Eq. 14): match counts bit-exact; J-hat = matches/k IEEE-rounded."""

@@ -118,3 +118,16 @@ def test_tile_option_validated_before_any_call():
     rows = wmh.Rows.from_dense(torch.zeros((2, 8), dtype=torch.uint8))
     with pytest.raises(ValueError, match="tile"):
         wmh.hash(None, rows, 1, 4, 10, tile="diagonal")
+
+
+def test_sketches_refuse_mismatched_metadata():
+    """collide_sketches checks (seed, k, cap, layout digest) before any call."""
+    import torch
+    import paper_1602_08393_b200 as wmh
+    s = torch.zeros((2, 4), dtype=torch.uint16)
+    a = wmh.Sketch(s, 1, 4, 100, 7)
+    i = torch.zeros(1, dtype=torch.int64)
+    for b, what in [(wmh.Sketch(s, 2, 4, 100, 7), "seed"), (wmh.Sketch(s, 1, 4, 99, 7), "cap"),
+                    (wmh.Sketch(s, 1, 4, 100, 8), "layout digest")]:
+        with pytest.raises(ValueError, match=what):
+            wmh.collide_sketches(a, b, i, i)
