@@ -272,12 +272,29 @@ struct IxParams {
 
 // x_c of the current row: dense byte, or a lower_bound over the CSR slice
 // (its columns staged in shared memory when the row is short enough).
+// x_c of the row: dense -> direct; CSR -> binary search of c among the row's
+// columns, in shared memory when staged (scol), else first over the staged
+// sample samp[i] = col[i * sd] (ns entries) and then among the <= sd - 1
+// columns of one block in global memory (one or two cache lines)
 template <bool CSR, typename W>
 __device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const W *xrow, const uint32_t *scol,
-                                             int64_t e0, int n, uint32_t c) {
+                                             int64_t e0, int n, uint32_t c, const uint32_t *samp = nullptr,
+                                             int ns = 0, int sd = 1) {
     const W *val = reinterpret_cast<const W *>(p.val);
     if (!CSR) return scol ? (uint32_t)reinterpret_cast<const W *>(scol)[c] : (uint32_t)__ldg(xrow + c);
     int lo = 0, hi = n;
+    if (!scol && samp) {
+        int a = 0, b = ns;                       // first i with samp[i] >= c
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (samp[mid] < c) a = mid + 1;
+            else b = mid;
+        }
+        if (a < ns && samp[a] == c) return (uint32_t)__ldg(val + e0 + (int64_t)a * sd);
+        if (a == 0) return 0u;
+        lo = (a - 1) * sd + 1;                   // col[(a-1) * sd] < c < col[a * sd]
+        hi = min(n, a * sd);
+    }
     if (scol) {
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
@@ -568,6 +585,21 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                 //      (IX_FB independent lookups per lane), refilling from the list
                 const uint32_t *scol = staged ? scol_buf : nullptr;
                 uint32_t *list = ra;
+                // 8 warps (large k: many fallback hashes per row) on an unstaged CSR
+                // row: a sample of its columns in rp[] (free after phase 2) turns the
+                // ~11 dependent global loads of each lookup into shared-memory steps
+                // and one or two global ones (c4: 19.9 -> 18.9 ms; with fewer warps
+                // the extra code cost more than it saved, c3 10.0 -> 11.0 ms)
+                const uint32_t *samp = nullptr;
+                int ns = 0, sd = 1;
+                if constexpr (CSR && NW == 8) {
+                    if (!staged) {
+                        sd = (n + CAPR - 1) / CAPR;
+                        ns = (n + sd - 1) / sd;
+                        for (int i = threadIdx.x; i < ns; i += NT) rp[i] = (uint32_t)__ldg(p.col + e0 + (int64_t)i * sd);
+                        samp = rp;                // visible after the loop's first __syncthreads
+                    }
+                }
                 for (;;) {
                     if (threadIdx.x == 0) { s_nu = 0; s_qhead = 0; }
                     __syncthreads();
@@ -626,7 +658,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
 #pragma unroll
                         for (int q = 0; q < IX_FB; q++) {
                             if (!((live >> q) & 1u)) continue;
-                            const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q]);
+                            const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q], samp, ns, sd);
                             const unsigned gm = __ballot_sync(FULL, g);
                             bool done = false;
                             if (gm) {
@@ -686,7 +718,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                             }
 #pragma unroll
                             for (int q = 0; q < IX_FB; q++) {
-                                const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q]);
+                                const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q], samp, ns, sd);
                                 const unsigned gm = __ballot_sync(FULL, g);
                                 if (gm) {
                                     if (lane == 0) h[jq[q]] = t0 + __ffs(gm) - 1;
