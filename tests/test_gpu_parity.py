@@ -186,10 +186,15 @@ def test_tiled_bitplanes(wmh, D, n, mx, tile):
     data = datagen.Dense(x)
     cfg = datagen.Config("bs", n, D, 1, 255, 1)
     for k, cap, sb in [(40, 65535, 2), (24, 9, 1), (13, 65535, 2), (5, 200, 1)]:
-        sig, L, _ = _run(wmh, data, cfg, k, cap, sb, "tiled", seed=mx + 7, tile=tile)
+        sig, L, layout = _run(wmh, data, cfg, k, cap, sb, "tiled", seed=mx + 7, tile=tile)
         _assert_sig_equal(sig, oracle_hash(L, data, mx + 7, k, cap), f"{tile} D={D} mx={mx} k={k} cap={cap}")
         s = sig.cpu().numpy()
         assert np.all(s[[3, n - 1]] == cap) and np.all(s[4] == 1)
+        # saturation counter: every (row, j) of the all-zero rows, at most every h == cap
+        nsat = torch.zeros(1, dtype=torch.int64, device="cuda")
+        wmh.hash(layout, to_rows(data), mx + 7, k, cap, sb, algo="tiled", tile=tile, n_saturated=nsat)
+        dead = int((x.sum(1) == 0).sum())
+        assert dead * k <= int(nsat.item()) <= int((s == cap).sum())
 
 
 @pytest.mark.parametrize("tile", ["bitplanes", "auto"])
