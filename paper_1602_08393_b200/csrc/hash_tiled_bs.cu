@@ -324,13 +324,24 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 uint32_t xv[DPL][NB];
 #pragma unroll
                 for (int i = 0; i < DPL; i++) bs_load<NB, NBS>(plg, wd[i], (uint32_t)part & 1u, xv[i]);
+                uint32_t gms[DPL];
+#pragma unroll
+                for (int i = 0; i < DPL; i++) gms[i] = bs_test<NB>(xv[i], wd[i]);
+                if (CLAMP) {                         // one test for the lane's DPL draws, then the rare ones
+                    uint32_t fl = 0;
+#pragma unroll
+                    for (int i = 0; i < DPL; i++) fl |= wd[i];
+                    if (fl & 0x80u) {
+#pragma unroll
+                        for (int i = 0; i < DPL; i++)
+                            if (wd[i] & 0x80u) gms[i] = bs_slow<NB>(p, row0 + 32 * g, min(32, nr - 32 * g), wd[i], GN);
+                    }
+                }
                 uint32_t F[DPL], any = 0;
 #pragma unroll
                 for (int i = 0; i < DPL; i++) {
-                    uint32_t gm = bs_test<NB>(xv[i], wd[i]);
-                    if (CLAMP && (wd[i] & 0x80u)) gm = bs_slow<NB>(p, row0 + 32 * g, min(32, nr - 32 * g), wd[i], GN);
-                    F[i] = gm & ~any;
-                    any |= gm;
+                    F[i] = gms[i] & ~any;
+                    any |= gms[i];
                 }
                 // segmented prefix OR over the group's parts (lanes g, g + G, ...; draw order = part order)
                 uint32_t incl = any;
