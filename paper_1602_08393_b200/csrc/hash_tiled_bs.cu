@@ -169,8 +169,13 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
     constexpr int R = 32 * G, LP = 32 / G, DPL = bs_dpl(G), RD = LP * DPL;
     static_assert(DPL <= 16, "the record loop decodes 4 bits of draw index");
     extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *planes = smem;                                                       // [D][G][NBS]
+    // SPLIT (unpadded NB = 5..7): planes 0..3 of (column, group) as one 16-byte
+    // block [D][G][4], the other NB - 4 in a second array [D][G][NB - 4]: two
+    // shared loads per draw instead of three or more
+    constexpr bool SPLIT = NBS == NB && NB > 4 && NB < 8;
+    uint32_t *planes = smem;                                                       // [D][G][NBS] (or split)
     const size_t pl_words = ((size_t)p.D * G * NBS + 3) & ~(size_t)3;
+    uint32_t *planesB = planes + (size_t)p.D * G * 4;                              // SPLIT: [D][G][NB - 4]
     uint32_t *sbuf_all = planes + pl_words;                                        // [NW][T0]
     uint16_t *hres_all = reinterpret_cast<uint16_t *>(sbuf_all + BS_NW * T0);     // [NW][HB][R]
     __shared__ long long s_item, s_next;
@@ -240,9 +245,21 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
             for (int u4 = 0; u4 < 4; u4++) {
                 uint32_t a = lo[u4], b = hi[u4];
                 bs_t8(a, b);
-                uint8_t *dst = pbytes + ((size_t)((4 * cq + u4) * G + g) * NBS) * 4 + o;
+                const size_t blk = (size_t)(4 * cq + u4) * G + g;
+                if (SPLIT) {
+                    uint8_t *dA = pbytes + blk * 16 + o;
+                    uint8_t *dB = reinterpret_cast<uint8_t *>(planesB) + blk * (NB - 4) * 4 + o;
 #pragma unroll
-                for (int pb = 0; pb < NB; pb++) dst[4 * pb] = (uint8_t)((pb < 4 ? a : b) >> (8 * (pb & 3)));
+                    for (int pb = 0; pb < NB; pb++) {
+                        const uint8_t v = (uint8_t)((pb < 4 ? a : b) >> (8 * (pb & 3)));
+                        if (pb < 4) dA[4 * pb] = v;
+                        else dB[4 * (pb - 4)] = v;
+                    }
+                } else {
+                    uint8_t *dst = pbytes + blk * NBS * 4 + o;
+#pragma unroll
+                    for (int pb = 0; pb < NB; pb++) dst[4 * pb] = (uint8_t)((pb < 4 ? a : b) >> (8 * (pb & 3)));
+                }
             }
         }
         __syncthreads();
@@ -257,7 +274,7 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
         };
         const int g = lane % G, part = lane / G;          // groups fastest: the G lanes of a part share a column
         const uint32_t *plg = planes + g * NBS;
-        const uint32_t GN = (uint32_t)(G * NBS);
+        const uint32_t GN = (uint32_t)(SPLIT ? G : G * NBS);   // the table's column stride
         const uint32_t live0 = s_live[g];
         const uint32_t valid = 32 * g + 32 <= nr ? 0xFFFFFFFFu : (32 * g >= nr ? 0u : (1u << (nr - 32 * g)) - 1u);
         const uint32_t pend0 = live0 & valid;
@@ -323,7 +340,23 @@ __global__ void __launch_bounds__(BS_NT, 1) hash_tiled_bs_kernel(const BsParams 
                 }
                 uint32_t xv[DPL][NB];
 #pragma unroll
-                for (int i = 0; i < DPL; i++) bs_load<NB, NBS>(plg, wd[i], (uint32_t)part & 1u, xv[i]);
+                for (int i = 0; i < DPL; i++) {
+                    if constexpr (SPLIT) {
+                        const uint32_t blk = (wd[i] >> 8) + (uint32_t)g;              // (column, group) block
+                        const uint4 a4 = reinterpret_cast<const uint4 *>(planes)[blk];
+                        xv[i][0] = a4.x; xv[i][1] = a4.y; xv[i][2] = a4.z; xv[i][3] = a4.w;
+                        const uint32_t *pb = planesB + blk * (NB - 4);
+                        if (NB - 4 == 2) {
+                            const uint2 b2 = *reinterpret_cast<const uint2 *>(pb);
+                            xv[i][4 % NB] = b2.x; xv[i][5 % NB] = b2.y;
+                        } else {
+#pragma unroll
+                            for (int q = 4; q < NB; q++) xv[i][q] = pb[q - 4];
+                        }
+                    } else {
+                        bs_load<NB, NBS>(plg, wd[i], (uint32_t)part & 1u, xv[i]);
+                    }
+                }
                 uint32_t gms[DPL];
 #pragma unroll
                 for (int i = 0; i < DPL; i++) gms[i] = bs_test<NB>(xv[i], wd[i]);
@@ -543,7 +576,10 @@ wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled) {
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "tiled counter memset");
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
-    const uint32_t GN = (uint32_t)(G * NBSW);
+    // column stride of the draw words: (column, group) blocks for the split
+    // layout of unpadded 5..7 planes (the kernel's SPLIT), else words
+    const bool split = NBSW == NBP && NBP > 4 && NBP < 8;
+    const uint32_t GN = (uint32_t)(split ? G : G * NBSW);
 #define WMH_BS_TAB(V) bs_table<V>(table, a, uni_m, GN, clamp, a.stream)
     WMH_BS_NB_SWITCH(NBP, WMH_BS_TAB)
 #undef WMH_BS_TAB
