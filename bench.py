@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """bench.py -- weighted-minhash signatures/sec (row x hash) on 1..8 B200s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--algo auto]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--algo auto]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
     python bench.py --impl reference ...      # the CPU oracle, timed on the host cores
 
-A step is one wmh_hash launch over this rank's resident rows (all of §8(a)'s
-hot-path rows a5-a9; a1-a4 -- column max, the NCCL max exchange, prefix sums,
-IntToComp -- run once before timing, as the paper's "one time pre-processing",
-P:276).  Scaling is weak: every rank hashes its own N-row shard of one
-dataset (rows r*N .. (r+1)*N-1 of the chunk-seeded generator), so the work
-per GPU is fixed as N grows; the only collective is the max exchange in
-prepare.  Timing: CUDA events on the launching stream around each step, an
-L2 flush (256 MiB write) between steps outside the events, barrier +
-synchronize around the K steps, max over ranks.  Rank 0 prints one JSON line.
+The default workload is BASELINE.json configs[4] (c5: 16,000,000 dense rows x
+4096, k = 1024, uint16 signatures), the largest configuration that fits one
+B200 -- the metric names no config, so the line is quoted on it.  A step is
+one wmh_hash launch over this rank's resident rows (all of §8(a)'s hot-path
+rows a5-a9; a1-a4 -- column max, the NCCL max exchange, prefix sums,
+IntToComp -- run once before timing, as the paper's "one time
+pre-processing").  Scaling is strong: the N rows of ONE
+dataset are split into contiguous shards shard(N, r, G) (the same rows for
+every G, generated on the device for the counter-based configs c1/c5), so
+the total work is fixed as G grows; the only collective is the max exchange
+in prepare.  Timing: CUDA events on the launching stream around each step, an
+L2 flush (256 MiB write) between steps outside the events (the c5 rows, 65 GB,
+exceed L2 anyway), barrier + synchronize around the K steps, max over ranks.
+Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -40,9 +45,13 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c2", help="c1..c5 (default c2: the metric's workload, configs[1])")
-    p.add_argument("--rows", type=int, default=None, help="rows per GPU (default: the config's N)")
+    p.add_argument("--config", default="c5",
+                   help="c1..c5, c2r (default c5 = configs[4], the largest single-GPU configuration)")
+    p.add_argument("--rows", type=int, default=None,
+                   help="total rows N over all GPUs (default: the config's N); rank r hashes shard(N, r, G)")
     p.add_argument("--algo", default="auto", choices=["auto", "simple", "tiled", "index"])
+    p.add_argument("--tile", default="auto", choices=["auto", "bytes", "bitplanes", "bitslice"],
+                   help="tiled, dense rows: which tile (performance only)")
     p.add_argument("--chunk", type=int, default=0, help="tiled: draws per re-queue (0 = auto)")
     p.add_argument("--horizon", type=int, default=0, help="index: draws filed per hash (0 = auto)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -50,18 +59,31 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
     p.add_argument("--gpu-gen", action="store_true",
-                   help="c1/c5: generate the rows on the device (datagen/gen_kernels.cu) instead of the host")
-    p.add_argument("--collide-pairs", type=int, default=0,
-                   help="also time wmh_collide (a10) on this many random pairs of the step's signatures")
+                   help="(kept for old command lines: c1/c5 rows are always generated on the device)")
+    p.add_argument("--collide-pairs", type=int, default=-1,
+                   help="also time wmh_collide (a10) on this many random pairs of the step's signatures "
+                        "(-1 = the config's own: 10^7 for c5, else none)")
+    p.add_argument("--gather", action="store_true",
+                   help="under torchrun: all-gather the signatures (NCCL) before colliding pairs over all rows")
     return p.parse_args()
 
 
 # ----------------------------------------------------------------- workload
-def workload(cfg_name: str, rank: int, n_rows: int | None):
+def shard(n_rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous row block of rank r (the binding's shard(); restated here so the
+    reference arm does not import the CUDA package)."""
+    base, rem = divmod(n_rows, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def workload(cfg_name: str, rank: int, n_rows: int | None, world: int = 1):
+    """This rank's shard of the config's N rows (host-generated configs)."""
     import datagen
     cfg = datagen.CONFIGS[cfg_name]
-    n = cfg.n_rows if n_rows is None else n_rows
-    lo, hi = rank * n, (rank + 1) * n
+    N = cfg.n_rows if n_rows is None else n_rows
+    lo, hi = shard(N, rank, world)
+    n = hi - lo
     cache = os.environ.get("BENCH_CACHE_DIR")      # optional: reuse generated rows within one session
     if cache and cfg.kind == "dense":
         path = os.path.join(cache, f"{cfg_name}_{lo}_{hi}.npy")
@@ -90,10 +112,21 @@ def _generate(cfg_name, cfg, lo, hi):
     return data
 
 
-def desc(cfg, n):
+def desc(cfg, N):
     w = "real -> uint16 fixed point" if cfg.name == "c2r" else "uint8"
-    return (f"{cfg.name}: N={n} rows/GPU, D={cfg.dim}, {cfg.kind} {w}, k={cfg.k}, cap={cfg.cap}, "
+    return (f"{cfg.name}: N={N} rows, D={cfg.dim}, {cfg.kind} {w}, k={cfg.k}, cap={cfg.cap}, "
             f"uint{8 * cfg.sig_bytes} signatures, seed={cfg.seed}")
+
+
+def host_cores():
+    """(logical CPUs this process may use, physical cores) of the host."""
+    logical = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except Exception:                                  # noqa: BLE001
+        phys = None
+    return logical, phys
 
 
 def expected_draws(x_sum: np.ndarray, M: int, k: int, cap: int) -> float:
@@ -169,12 +202,14 @@ class ClockSampler:
 
 # ------------------------------------------------------------- CPU oracle leg
 def oracle_rate(cfg, data, M_bounds, seconds: float):
-    """Time the oracle (as it stands) on a bounded row sample of the same
-    workload, on all host cores; returns (hashes/s, cores, sample description)."""
+    """Time the oracle (as it stands) on a bounded, seeded row sample of the same
+    workload, on all host cores; returns (hashes/s, threads, sample description).
+    Counter-based rows (c1/c5) are regenerated on the host for the sampled rows
+    only, so the full 65 GB array never exists in host memory."""
     import datagen
     import oracle
     L = oracle.Layout(M_bounds)
-    cores = os.cpu_count() or 1
+    cores, _ = host_cores()
     n = data.n_rows
 
     def run(rows):
@@ -199,10 +234,24 @@ def oracle_rate(cfg, data, M_bounds, seconds: float):
     return rate, cores, f"{len(rows)} of {n} rows (seeded uniform sample), all k={cfg.k} hashes, {dt:.1f} s"
 
 
-def layout_bounds(cfg, data):
+def layout_bounds(cfg, data, N=None):
+    """The oracle-side column maxima m_c of the whole N-row dataset:
+    the fixed bound (c4), the host data's maxima, or -- for the counter-based
+    full-size c5 -- tests/golden/c5_colmax.txt (written by
+    scripts/make_golden_colmax.py through oracle.colmax_dense)."""
     import datagen
     if cfg.fixed_bound is not None:
         return np.full(data.dim, cfg.fixed_bound, np.uint32)
+    if isinstance(data, datagen.CounterRows):
+        N = data.n_rows if N is None else N
+        gold = os.path.join(ROOT, "tests", "golden", f"{cfg.name}_colmax.txt")
+        if N == cfg.n_rows and os.path.exists(gold):
+            return np.loadtxt(gold, dtype=np.int64, comments="#").reshape(-1).astype(np.uint32)
+        import oracle
+        m = np.zeros(data.dim, np.uint32)
+        for a0 in range(0, N, 65536):
+            m = np.maximum(m, oracle.colmax_dense(data.rows(np.arange(a0, min(N, a0 + 65536)))))
+        return m
     if isinstance(data, datagen.Dense):
         return data.x.max(axis=0).astype(np.uint32)
     m = np.zeros(data.dim, np.uint32)
@@ -210,11 +259,24 @@ def layout_bounds(cfg, data):
     return m
 
 
+def reference_data(cfg_name, N):
+    """The whole N-row dataset as the oracle sees it: lazy for c1/c5."""
+    import datagen
+    cfg = datagen.CONFIGS[cfg_name]
+    if cfg_name in ("c1", "c5"):
+        return cfg, datagen.CounterRows(cfg_name, cfg.data_seed, 0, N, cfg.dim)
+    cfg, _, data = workload(cfg_name, 0, N, 1)
+    return cfg, data
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cfg, n, data = workload(args.config, 0, args.rows)
+    import datagen
+    cfg = datagen.CONFIGS[args.config]
+    N = cfg.n_rows if args.rows is None else args.rows
+    cfg, data = reference_data(args.config, N)
     bounds = layout_bounds(cfg, data)
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     rates = []
@@ -223,12 +285,14 @@ def run_reference(args):
         if i >= args.warmup:
             rates.append(r)
     value = statistics.mean(rates)
+    _, phys = host_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": n * cfg.k / value * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": desc(cfg, n), "parallelism": "host threads (rank 0 only)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": N * cfg.k / value * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": desc(cfg, N), "parallelism": "host threads (rank 0 only)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "physical_cores": phys, "kind": "oracle",
+                         "sample": sample + f"; each of the {args.steps} timed steps a fresh ~{per_step:.0f} s sample"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -257,18 +321,20 @@ def main():
     import paper_1602_08393_b200 as wmh
 
     import datagen
-    gpu_gen = args.gpu_gen and args.config in ("c1", "c5")
+    N = datagen.CONFIGS[args.config].n_rows if args.rows is None else args.rows   # total rows, all ranks
+    lo, hi = shard(N, rank, world)
+    assert (lo, hi) == wmh.shard(N, rank, world)
     xd = None
-    if gpu_gen:       # counter-based configs generated on the device (bit-identical to the host recipe)
+    if args.config in ("c1", "c5"):   # counter-based: this rank's shard generated on the device (bit-identical to the host recipe)
         cfg = datagen.CONFIGS[args.config]
-        n = cfg.n_rows if args.rows is None else args.rows
+        n = hi - lo
         xd = torch.empty((n, cfg.dim), dtype=torch.uint8, device=dev)
         for a0 in range(0, n, 1 << 20):
             b0 = min(n, a0 + (1 << 20))
-            xd[a0:b0] = datagen.gpu_counter_rows(args.config, cfg.data_seed, rank * n + a0, b0 - a0, cfg.dim, dev)
-        data = datagen.CounterRows(args.config, cfg.data_seed, rank * n, n, cfg.dim)
+            xd[a0:b0] = datagen.gpu_counter_rows(args.config, cfg.data_seed, lo + a0, b0 - a0, cfg.dim, dev)
+        data = datagen.CounterRows(args.config, cfg.data_seed, lo, n, cfg.dim)
     else:
-        cfg, n, data = workload(args.config, rank, args.rows)
+        cfg, n, data = workload(args.config, rank, N, world)
     # f1 (c2r): real-valued rows -> Sec. 4 scale choice -> uint16 fixed point, on the
     # device and before the timed region (the paper's "one time pre-processing")
     quant = None
@@ -302,7 +368,7 @@ def main():
 
     def step(timed=False):
         wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig, chunk=args.chunk,
-                 horizon=args.horizon, time_kernel=timed)
+                 horizon=args.horizon, time_kernel=timed, tile=args.tile)
 
     clocks = ClockSampler(dev.index if world == 1 else local)
     clocks.start()
@@ -335,7 +401,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max_ms = float(t.item())
-    hashes_per_step_total = n * cfg.k * world
+    hashes_per_step_total = N * cfg.k                      # every rank's shard: the whole dataset
     value = hashes_per_step_total * args.steps / (t_max_ms / 1e3)
     ms_per_step = t_max_ms / args.steps
 
@@ -346,6 +412,10 @@ def main():
     else:
         x_sum = row_sums(data)
     draws = expected_draws(x_sum, M, cfg.k, cfg.cap)      # this rank's algorithmic draw-tests per launch
+    dt_ = torch.tensor([draws], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(dt_)
+    draws_total = float(dt_.item())
     kern_s = statistics.mean(kern_ms) / 1e3               # the dominant kernel's average launch (events)
     peaks = {}
     try:
@@ -381,10 +451,11 @@ def main():
         e2e = measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd)
 
     coll = None
-    if args.collide_pairs > 0:
+    n_pairs = cfg.n_pairs if args.collide_pairs < 0 else args.collide_pairs
+    if n_pairs > 0:
         gather_ms = None
         sig_c = sig
-        if world > 1:                   # the optional NCCL signature exchange, then pairs over all rows
+        if world > 1 and args.gather:   # the optional NCCL signature exchange, then pairs over all rows
             torch.cuda.synchronize()
             g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             g0.record()
@@ -392,28 +463,37 @@ def main():
             g1.record()
             torch.cuda.synchronize()
             gather_ms = g0.elapsed_time(g1)
-        coll = measure_collide(wmh, sig_c, args.collide_pairs, cfg, dev, peaks)
+        coll = measure_collide(wmh, sig_c, n_pairs, cfg, dev, peaks)
         coll["gather_ms"] = gather_ms
+        coll["pairs_over"] = "all ranks' rows (gathered)" if sig_c is not sig else \
+            ("this rank's shard" if world > 1 else "all rows")
 
+    # the oracle on a sample of the same N-row dataset (rank 0, host cores; the
+    # other ranks wait at the barrier): bounds from the oracle side, never the GPU
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        bnds = torch.stack([xd[a0:a0 + 65536].to(torch.int32).amax(0) for a0 in range(0, n, 65536)]).amax(0) \
-            .cpu().numpy().astype(np.uint32) if xd is not None \
-            else layout_bounds(cfg, data)
-        r, cores, sample = oracle_rate(cfg, data, bnds, args.cpu_seconds)
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    if rank == 0 and not args.no_cpu_baseline:
+        rcfg, rdata = reference_data(args.config, N) if xd is not None or world > 1 else (cfg, data)
+        if cfg.name == "c2r":
+            rdata = data
+        bnds = layout_bounds(rcfg, rdata)
+        r, cores, sample = oracle_rate(rcfg, rdata, bnds, args.cpu_seconds)
+        _, phys = host_cores()
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "physical_cores": phys, "kind": "oracle", "sample": sample}
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": desc(cfg, n), "global_rows": n * world, "k": cfg.k, "M": M,
-                       "algo": args.algo, "parallelism": f"rows sharded x{world}, no collective in the step",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": desc(cfg, N), "global_rows": N, "rows_per_gpu_max": -(-N // world),
+                       "k": cfg.k, "M": M, "algo": args.algo, "tile": args.tile,
+                       "parallelism": f"rows sharded x{world} (contiguous shard(N, r, G)), no collective in the step",
                        "l2": "flushed between steps (256 MiB write outside the timed events); "
                              f"inputs {in_bytes / 2**20:.0f} MiB + signatures "
                              f"{sig.numel() * sig.element_size() / 2**20:.0f} MiB per step",
-                       "expected_draws_per_step": draws * world,
+                       "expected_draws_per_step": draws_total,
                        "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)]},
             "roofline": roof,
             "collide": coll,

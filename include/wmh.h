@@ -110,6 +110,15 @@ wmh_status wmh_quantize(const float *in, int64_t n, float scale, uint16_t *out, 
 wmh_status wmh_scale_objective(const wmh_rows *rows_f32, const float *scales, int32_t n_scales, uint64_t *out,
                                void *stream);
 
+/* Sec. 4's scale choice itself: *best = the index in scales[] of the
+ * candidate with the largest mean effective sparsity num / den (from
+ * wmh_scale_objective, compared exactly in 128-bit integers) among those that
+ * saturate no uint16 weight; ties go to the smaller scale (reading R18).
+ * Synchronises `stream`.  Errors: EINVAL (no admissible scale; bad arguments),
+ * ENOMEM, ECUDA. */
+wmh_status wmh_choose_scale(const wmh_rows *rows_f32, const float *scales, int32_t n_scales, int32_t *best,
+                            void *stream);
+
 /* ---- a3 + a4: prefix sums and Alg. 4 ComputeHashMaps --------------------
  * Builds CompToM[c] = sum_{i<c} m_i (Eq. 3; exclusive prefix, interval
  * c = [CompToM[c], CompToM[c+1]), reading R3) and IntToComp[t] = c for every
@@ -148,6 +157,16 @@ wmh_status wmh_layout_tables(const wmh_layout *layout, const uint32_t **comp_to_
 
 void wmh_layout_free(wmh_layout *layout);
 
+/* Check rows against an existing layout: every weight x[n][c] <= m_c (the
+ * condition Eq. 2 and Alg. 5 rely on) and, for CSR, the
+ * structure (row_ptr monotone, columns ascending and < dim).  For rows that
+ * wmh_prepare did not see (streaming batches, a second dataset sketched with
+ * the first one's layout).  Reads the rows once (dense: one column-max pass;
+ * the first offender is located only on failure) and synchronises `stream`.
+ * Errors: EBOUND (first offending (row, col) / nonzero in wmh_last_error),
+ *         EINVAL (null, dim mismatch, malformed CSR), ENOMEM, ECUDA. */
+wmh_status wmh_check_rows(const wmh_layout *layout, const wmh_rows *rows, void *stream);
+
 /* ---- a5..a9: the hash ------------------------------------------------------
  * sig[n][j] = h_j(x_n), j = 0..k-1, row-major n_rows x k, for every row:
  *   S   = splitmix64(seed)                                   (reading R7)
@@ -160,7 +179,10 @@ void wmh_layout_free(wmh_layout *layout);
  * P:190-191) -- so rows may be sharded across GPUs freely.  An all-zero row
  * yields cap for every j (reading R12).
  *   rows must satisfy x <= bounds of `layout` (checked by wmh_prepare when
- *        given rows; NOT re-checked here) and rows->dim == layout dim.
+ *        given rows; not re-checked here unless wmh_hash_ex gets
+ *        WMH_OPT_VALIDATE -- otherwise a weight above its bound gives
+ *        signatures that are silently wrong and kernel-dependent; see
+ *        wmh_check_rows) and rows->dim == layout dim.
  *   k >= 1; 1 <= cap <= 2^(8*sig_bytes) - 1; sig_bytes in {1, 2}.
  *   sig_out: device, n_rows*k*sig_bytes bytes (uint8 or uint16 values).
  *   n_saturated: optional device uint64, INCREMENTED (not overwritten) by
@@ -197,16 +219,22 @@ typedef struct {
     uint32_t flags;      /* WMH_OPT_TIME_KERNEL: bracket the call's dominant (per-row)
                             kernel with CUDA events on `stream`; read with
                             wmh_last_kernel_ms.  WMH_OPT_TILE_BYTES /
-                            WMH_OPT_TILE_BITPLANES (exclusive): for TILED on
-                            dense rows, the byte tile or the bit-plane tile
-                            (default: bit planes when the byte tile would hold
-                            fewer than 128 rows).  Performance only. */
+                            WMH_OPT_TILE_BITPLANES / WMH_OPT_TILE_BITSLICE
+                            (exclusive): for TILED on dense rows, the byte tile,
+                            the round-1 bit-plane tile or the lane-per-draw
+                            bit-sliced tile (default: the bit-sliced tile when
+                            its planes fit).  Performance only. */
     int32_t reserved[3]; /* must be zero */
 } wmh_hash_opts;
 
 #define WMH_OPT_TIME_KERNEL 1u
 #define WMH_OPT_TILE_BYTES 2u
 #define WMH_OPT_TILE_BITPLANES 4u
+#define WMH_OPT_TILE_BITSLICE 8u
+#define WMH_OPT_VALIDATE 16u      /* check every row against the layout's bounds first
+                                     (wmh_check_rows): WMH_EBOUND instead of silently
+                                     wrong signatures for x_c > m_c.  One extra pass
+                                     over the rows and one synchronisation */
 
 wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t seed, uint32_t k,
                        uint32_t cap, int32_t sig_bytes, void *sig_out, uint64_t *n_saturated,
@@ -218,10 +246,11 @@ wmh_status wmh_hash_ex(const wmh_layout *layout, const wmh_rows *rows, uint64_t 
  * wmh_hasher_run then hashes a batch with the index kernel's row pass only.
  * Output is bit-identical to wmh_hash(layout, rows, seed, k, cap, ...).  The
  * hasher keeps a pointer to `layout` (keep it alive) and its device index
- * (freed by wmh_hasher_free, which synchronises the device).  Runs on one
- * hasher must not overlap in time (they share a row counter): issue them on
- * one stream.  Errors: as wmh_hash; k within the index kernel's limit
- * (WMH_ALGO_INDEX). */
+ * (freed by wmh_hasher_free, which synchronises the device).  Every run waits
+ * (stream-ordered, cudaStreamWaitEvent) for the build recorded on the create
+ * stream and uses a row counter of its own, so runs may be issued on any
+ * streams, concurrently.  Errors: as wmh_hash; k within the index kernel's
+ * limit (WMH_ALGO_INDEX). */
 typedef struct wmh_hasher wmh_hasher;
 wmh_status wmh_hasher_create(const wmh_layout *layout, uint64_t seed, uint32_t k, uint32_t cap, uint32_t horizon,
                              wmh_hasher **out, void *stream);
@@ -247,6 +276,16 @@ wmh_status wmh_hash_host(const wmh_layout *layout, const wmh_rows *rows_host, ui
  * Errors: EINVAL, ECUDA. */
 wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k, int64_t n_rows, const int64_t *pairs,
                        int64_t n_pairs, uint32_t *matches, float *jhat, int32_t check_pairs, void *stream);
+
+/* a10 across two signature buffers (e.g. a query set against a corpus, or two
+ * sketches made separately with the same seed, k, cap and layout): pair p
+ * compares row pairs[2p] of sig_a (n_a rows) with row pairs[2p+1] of sig_b
+ * (n_b rows); both k columns wide, sig_bytes each.  Same outputs, checks and
+ * errors as wmh_collide (check_pairs: indices outside [0, n_a) x [0, n_b)
+ * -> WMH_EINVAL after one synchronisation). */
+wmh_status wmh_collide2(const void *sig_a, int64_t n_a, const void *sig_b, int64_t n_b, int32_t sig_bytes,
+                        uint32_t k, const int64_t *pairs, int64_t n_pairs, uint32_t *matches, float *jhat,
+                        int32_t check_pairs, void *stream);
 
 /* Device time (ms) of the dominant kernel of the last wmh_hash_ex call on this
  * thread that set WMH_OPT_TIME_KERNEL (CUDA events on its stream).  Waits for

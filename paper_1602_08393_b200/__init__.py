@@ -158,7 +158,7 @@ def reduce_bounds(bounds: torch.Tensor, group=None) -> torch.Tensor:
 
     `group`: None = the default group when a multi-rank job is initialised,
     False = no reduction, else a ProcessGroup.  The uint32 bounds travel as an
-    int32 view (values <= 255, same bits) so NCCL and gloo both take them."""
+    int32 view (values <= 65535, so the bits are the same) so NCCL and gloo both take them."""
     dist = torch.distributed
     if group is False:
         return bounds
@@ -220,6 +220,13 @@ def prepare(rows: Rows | None = None, bounds: torch.Tensor | None = None, group=
     return Layout(h.value)
 
 
+def check_rows(layout: Layout, rows: Rows, stream=None) -> None:
+    """Raise WmhError (EBOUND / EINVAL) unless every weight of `rows` is within the
+    layout's bounds x_c <= m_c and CSR rows are well formed."""
+    _no_float(rows, "check_rows")
+    _lib.check(_lib.load().wmh_check_rows(layout.handle, ctypes.byref(rows._c()), _stream(stream)))
+
+
 last_algo = None     # name of the kernel the last hash() call ran ('simple' / 'tiled' / 'index')
 last_horizon = None  # the index horizon T of the last hash() call that ran the index kernel
 
@@ -227,10 +234,12 @@ last_horizon = None  # the index horizon T of the last hash() call that ran the 
 def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
          algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
          chunk: int = 0, horizon: int = 0, time_kernel: bool = False, stream=None,
-         tile: str = "auto") -> torch.Tensor:
+         tile: str = "auto", validate: bool = False) -> torch.Tensor:
     """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16).
-    `tile` ("auto", "bytes", "bitplanes") picks the TILED kernel's dense tile
-    (performance only)."""
+    `tile` ("auto", "bytes", "bitplanes", "bitslice") picks the TILED kernel's dense tile
+    (performance only).  `validate` checks every row against the layout's bounds
+    first (wmh_check_rows: WmhError EBOUND instead of silently wrong signatures
+    for rows prepare() did not see)."""
     if sig_bytes is None:
         sig_bytes = 1 if cap <= 255 else 2
     dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
@@ -242,10 +251,11 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
     _no_float(rows, "hash")
     if n_saturated is not None and (n_saturated.dtype not in (torch.int64, torch.uint64) or not n_saturated.is_cuda):
         raise ValueError("n_saturated must be a CUDA int64 tensor")
-    if tile not in ("auto", "bytes", "bitplanes"):
-        raise ValueError(f"tile must be auto, bytes or bitplanes, not {tile!r}")
-    flags = (_lib.WMH_OPT_TIME_KERNEL if time_kernel else 0) | \
-        {"auto": 0, "bytes": _lib.WMH_OPT_TILE_BYTES, "bitplanes": _lib.WMH_OPT_TILE_BITPLANES}[tile]
+    if tile not in ("auto", "bytes", "bitplanes", "bitslice"):
+        raise ValueError(f"tile must be auto, bytes, bitplanes or bitslice, not {tile!r}")
+    flags = (_lib.WMH_OPT_TIME_KERNEL if time_kernel else 0) | (_lib.WMH_OPT_VALIDATE if validate else 0) | \
+        {"auto": 0, "bytes": _lib.WMH_OPT_TILE_BYTES, "bitplanes": _lib.WMH_OPT_TILE_BITPLANES,
+         "bitslice": _lib.WMH_OPT_TILE_BITSLICE}[tile]
     opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon, flags)
     _lib.check(_lib.load().wmh_hash_ex(layout.handle, ctypes.byref(rows._c()), seed & (2**64 - 1), k, cap, sig_bytes,
                                        _ptr(out), _ptr(n_saturated), ctypes.byref(opts), _stream(stream)))
@@ -263,8 +273,19 @@ def hash_host(layout: Layout, rows_host, seed: int, k: int, cap: int, sig_bytes:
     if sig_bytes is None:
         sig_bytes = 1 if cap <= 255 else 2
     dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
+    for name in ("dense", "row_ptr", "col", "val"):
+        t = getattr(rows_host, name)
+        if t is not None and (t.is_cuda or not t.is_contiguous()):
+            raise ValueError(f"hash_host: rows_host.{name} must be a contiguous CPU tensor")
     if out is None:
         out = torch.empty((rows_host.n_rows, k), dtype=dtype)
+    elif isinstance(out, np.ndarray):
+        if out.dtype != (np.uint8 if sig_bytes == 1 else np.uint16) or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError("hash_host: out must be a C-contiguous uint8/uint16 array matching sig_bytes")
+        out = torch.from_numpy(out)
+    if out.is_cuda or out.dtype != dtype or not out.is_contiguous() or out.numel() != rows_host.n_rows * k:
+        raise ValueError(f"hash_host: out must be a contiguous CPU {dtype} tensor of n_rows*k = {rows_host.n_rows * k} "
+                         "elements")
     c = rows_host._c(device=False)
     _lib.check(_lib.load().wmh_hash_host(layout.handle, ctypes.byref(c), seed & (2**64 - 1), k, cap, sig_bytes,
                                          ctypes.c_void_p(out.data_ptr()), _stream(stream)))
@@ -301,19 +322,16 @@ def scale_objective(rows: Rows, scales, stream=None) -> list[tuple[int, int, int
 
 
 def choose_scale(rows: Rows, scales, stream=None) -> float:
-    """The candidate with the largest mean effective sparsity among those that do
-    not saturate a weight (ties: the smaller scale, i.e. the smaller M); Sec. 4's
-    alpha = argmax sum alpha x / sum ceil(alpha m)."""
-    obj = scale_objective(rows, scales, stream)
-    best = None
-    for s, (num, den, clipped) in sorted(zip(scales, obj), key=lambda t: t[0]):
-        if den == 0 or clipped:
-            continue
-        if best is None or num * best[2] > best[1] * den:
-            best = (s, num, den)
-    if best is None:
-        raise ValueError("every candidate scale quantises the rows to zero")
-    return float(best[0])
+    """Sec. 4's alpha = argmax sum alpha x / sum ceil(alpha m) over `scales`,
+    chosen in C (wmh_choose_scale): the candidate with the largest mean effective
+    sparsity among those that do not saturate a weight; ties: the smaller scale."""
+    if rows.weight_bytes != 4:
+        raise ValueError("choose_scale takes float32 rows")
+    sc = (ctypes.c_float * len(scales))(*[float(v) for v in scales])
+    best = ctypes.c_int32(-1)
+    _lib.check(_lib.load().wmh_choose_scale(ctypes.byref(rows._c()), sc, len(scales), ctypes.byref(best),
+                                            _stream(stream)))
+    return float(scales[best.value])
 
 
 def collide(sig: torch.Tensor, pairs: torch.Tensor, check_pairs: bool = True, stream=None):
@@ -361,9 +379,15 @@ def collide_sketches(a: Sketch, b: Sketch, ia: torch.Tensor, ib: torch.Tensor, s
         raise ValueError(f"sketches are not comparable: different {', '.join(diff)}")
     if a.sig.dtype != b.sig.dtype:
         raise ValueError("sketches have different signature widths")
-    both = torch.cat([a.sig, b.sig])
-    pairs = torch.stack([ia.to(torch.int64), ib.to(torch.int64) + a.sig.shape[0]], dim=1).contiguous()
-    return collide(both, pairs, stream=stream)
+    _need_cuda(a.sig, "a.sig")
+    _need_cuda(b.sig, "b.sig")
+    pairs = torch.stack([ia.to(torch.int64), ib.to(torch.int64)], dim=1).contiguous()
+    P = pairs.shape[0]
+    matches = torch.empty(P, dtype=torch.uint32, device=a.sig.device)
+    jhat = torch.empty(P, dtype=torch.float32, device=a.sig.device)
+    _lib.check(_lib.load().wmh_collide2(_ptr(a.sig), a.sig.shape[0], _ptr(b.sig), b.sig.shape[0], a.sig.element_size(),
+                                        a.k, _ptr(pairs), P, _ptr(matches), _ptr(jhat), 1, _stream(stream)))
+    return matches, jhat
 
 
 class Hasher:
@@ -379,8 +403,11 @@ class Hasher:
         self._h = h
 
     def hash(self, rows: Rows, sig_bytes: int | None = None, out: torch.Tensor | None = None,
-             n_saturated: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+             n_saturated: torch.Tensor | None = None, stream=None, validate: bool = False) -> torch.Tensor:
+        """`validate`: check the batch against the layout's bounds first (check_rows)."""
         _no_float(rows, "Hasher.hash")
+        if validate:
+            check_rows(self.layout, rows, stream)
         if sig_bytes is None:
             sig_bytes = 1 if self.cap <= 255 else 2
         dtype = torch.uint8 if sig_bytes == 1 else torch.uint16

@@ -13,6 +13,8 @@ WMH_DENSE, WMH_CSR = 0, 1
 WMH_OPT_TIME_KERNEL = 1
 WMH_OPT_TILE_BYTES = 2
 WMH_OPT_TILE_BITPLANES = 4
+WMH_OPT_TILE_BITSLICE = 8
+WMH_OPT_VALIDATE = 16
 ALGOS = {"auto": 0, "simple": 1, "tiled": 2, "index": 3}
 STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 4: "WMH_EOVERFLOW",
                 5: "WMH_ECUDA", 6: "WMH_ENOMEM"}
@@ -21,7 +23,8 @@ STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 
 EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_digest", "wmh_layout_tables", "wmh_layout_free",
            "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version",
            "wmh_kernel_launches", "wmh_last_kernel_ms", "wmh_quantize", "wmh_scale_objective", "wmh_lsh_build",
-           "wmh_lsh_query", "wmh_lsh_free", "wmh_hasher_create", "wmh_hasher_run", "wmh_hasher_free"]
+           "wmh_lsh_query", "wmh_lsh_free", "wmh_hasher_create", "wmh_hasher_run", "wmh_hasher_free",
+           "wmh_check_rows", "wmh_collide2", "wmh_choose_scale"]
 
 
 class WmhRows(ctypes.Structure):
@@ -70,6 +73,9 @@ def load() -> ctypes.CDLL:
             "wmh_hash_ex": (st, [vp, rows_p, u64, u32, u32, i32, vp, vp, ctypes.POINTER(WmhHashOpts), vp]),
             "wmh_hash_host": (st, [vp, rows_p, u64, u32, u32, i32, vp, vp]),
             "wmh_collide": (st, [vp, i32, u32, i64, vp, i64, vp, vp, i32, vp]),
+            "wmh_collide2": (st, [vp, i64, vp, i64, i32, u32, vp, i64, vp, vp, i32, vp]),
+            "wmh_check_rows": (st, [vp, rows_p, vp]),
+            "wmh_choose_scale": (st, [rows_p, ctypes.POINTER(ctypes.c_float), i32, ctypes.POINTER(i32), vp]),
             "wmh_last_error": (ctypes.c_char_p, []),
             "wmh_version": (ctypes.c_char_p, []),
             "wmh_kernel_launches": (ctypes.c_uint64, []),

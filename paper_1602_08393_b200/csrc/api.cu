@@ -107,7 +107,8 @@ wmh_status check_rows(const wmh_rows *rows, bool need_data) {
 // 16-byte aligned, a scalar lane-strided loop otherwise.  Equal halves /
 // bytes are counted from the xor of the two words.
 template <int SIGB, bool VEC>
-__global__ void __launch_bounds__(256) collide_kernel(const uint8_t *__restrict__ sig, uint32_t k, int64_t n_rows,
+__global__ void __launch_bounds__(256) collide_kernel(const uint8_t *__restrict__ sig_a, int64_t n_a,
+                                                      const uint8_t *__restrict__ sig_b, int64_t n_b, uint32_t k,
                                                       const int64_t *__restrict__ pairs, int64_t n_pairs,
                                                       uint32_t *__restrict__ matches, float *__restrict__ jhat,
                                                       unsigned long long *__restrict__ n_bad) {
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(256) collide_kernel(const uint8_t *__restrict_
     const int64_t row_bytes = (int64_t)k * SIGB;
     for (int64_t p = warp; p < n_pairs; p += nwarps) {
         const int64_t a = __ldg(pairs + 2 * p), b = __ldg(pairs + 2 * p + 1);
-        if (a < 0 || b < 0 || a >= n_rows || b >= n_rows) {
+        if (a < 0 || b < 0 || a >= n_a || b >= n_b) {
             if (lane == 0) {
                 matches[p] = 0;
                 if (jhat) jhat[p] = __int_as_float(0x7fc00000);
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(256) collide_kernel(const uint8_t *__restrict_
             }
             continue;
         }
-        const uint8_t *ra = sig + a * row_bytes, *rb = sig + b * row_bytes;
+        const uint8_t *ra = sig_a + a * row_bytes, *rb = sig_b + b * row_bytes;
         uint32_t cnt = 0;
         if (VEC) {
             const uint4 *va = reinterpret_cast<const uint4 *>(ra), *vb = reinterpret_cast<const uint4 *>(rb);
@@ -241,15 +242,21 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
     uint32_t horizon = 0;
     if (opts) {
         algo = opts->algo;
-        if (opts->flags & ~(uint32_t)(WMH_OPT_TIME_KERNEL | WMH_OPT_TILE_BYTES | WMH_OPT_TILE_BITPLANES)) { set_error("wmh_hash_ex: unknown flags 0x%x", opts->flags); return WMH_EINVAL; }
-        if ((opts->flags & WMH_OPT_TILE_BYTES) && (opts->flags & WMH_OPT_TILE_BITPLANES)) { set_error("wmh_hash_ex: WMH_OPT_TILE_BYTES and WMH_OPT_TILE_BITPLANES are exclusive"); return WMH_EINVAL; }
-        tile = (opts->flags & WMH_OPT_TILE_BYTES) ? 1 : (opts->flags & WMH_OPT_TILE_BITPLANES) ? 2 : 0;
+        const uint32_t tiles = WMH_OPT_TILE_BYTES | WMH_OPT_TILE_BITPLANES | WMH_OPT_TILE_BITSLICE;
+        if (opts->flags & ~(uint32_t)(WMH_OPT_TIME_KERNEL | WMH_OPT_VALIDATE | tiles)) { set_error("wmh_hash_ex: unknown flags 0x%x", opts->flags); return WMH_EINVAL; }
+        if (__builtin_popcount(opts->flags & tiles) > 1) { set_error("wmh_hash_ex: the WMH_OPT_TILE_* flags are exclusive"); return WMH_EINVAL; }
+        tile = (opts->flags & WMH_OPT_TILE_BYTES) ? 1 : (opts->flags & WMH_OPT_TILE_BITPLANES) ? 2
+             : (opts->flags & WMH_OPT_TILE_BITSLICE) ? 3 : 0;
         for (int i = 0; i < 3; i++)
             if (opts->reserved[i]) { set_error("wmh_hash_ex: reserved option fields must be zero"); return WMH_EINVAL; }
         chunk = opts->chunk;
         horizon = opts->horizon;
         if (chunk != 0 && chunk != 4 && chunk != 8 && chunk != 16 && chunk != 32) { set_error("wmh_hash_ex: chunk=%d not in {0,4,8,16,32}", chunk); return WMH_EINVAL; }
         if (algo < WMH_ALGO_AUTO || algo > WMH_ALGO_INDEX) { set_error("wmh_hash_ex: unknown algo %d", algo); return WMH_EINVAL; }
+    }
+    if (opts && (opts->flags & WMH_OPT_VALIDATE)) {
+        st = wmh_check_rows(L, rows, stream);
+        if (st != WMH_OK) return st;
     }
     int used = 0;
     g_ktimer.on = opts && (opts->flags & WMH_OPT_TIME_KERNEL);
@@ -270,6 +277,7 @@ struct wmh_hasher {
     uint64_t seed = 0;
     uint32_t k = 0, cap = 0;
     IndexBuilt ix;
+    cudaEvent_t built = nullptr;     // recorded after the build on the create stream
 };
 
 extern "C" wmh_status wmh_hasher_create(const wmh_layout *L, uint64_t seed, uint32_t k, uint32_t cap, uint32_t horizon,
@@ -292,6 +300,14 @@ extern "C" wmh_status wmh_hasher_create(const wmh_layout *L, uint64_t seed, uint
     h->cap = cap;
     wmh_status st = index_build(a, horizon, &h->ix);
     if (st != WMH_OK) { delete h; return st; }
+    if (cudaEventCreateWithFlags(&h->built, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(h->built, a.stream) != cudaSuccess) {
+        const cudaError_t e = cudaGetLastError();
+        index_free(h->ix, a.stream);
+        if (h->built) cudaEventDestroy(h->built);
+        delete h;
+        return cuda_fail(e, "wmh_hasher_create event");
+    }
     *out = h;
     return WMH_OK;
 }
@@ -312,12 +328,15 @@ extern "C" wmh_status wmh_hasher_run(const wmh_hasher *h, const wmh_rows *rows, 
     a.sig = sig_out;
     a.n_sat = reinterpret_cast<unsigned long long *>(n_saturated);
     a.stream = (cudaStream_t)stream;
+    // runs on any stream see the finished build (create may have used another)
+    WMH_CUDA_TRY(cudaStreamWaitEvent(a.stream, h->built, 0), "wmh_hasher_run wait for the build");
     return index_rows(a, h->ix);
 }
 
 extern "C" void wmh_hasher_free(wmh_hasher *h) {
     if (!h) return;
     if (h->ix.scr) cudaFree(h->ix.scr);          // (pool memory: cudaFree synchronises)
+    if (h->built) cudaEventDestroy(h->built);
     delete h;
 }
 
@@ -543,24 +562,25 @@ extern "C" wmh_status wmh_hash_host(const wmh_layout *L, const wmh_rows *rows_ho
     return WMH_OK;
 }
 
-extern "C" wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k, int64_t n_rows, const int64_t *pairs,
-                                  int64_t n_pairs, uint32_t *matches, float *jhat, int32_t check_pairs, void *stream) {
-    if (sig_bytes != 1 && sig_bytes != 2) { set_error("wmh_collide: sig_bytes=%d not in {1,2}", (int)sig_bytes); return WMH_EINVAL; }
-    if (k < 1) { set_error("wmh_collide: k must be >= 1"); return WMH_EINVAL; }
-    if (n_pairs < 0 || n_rows < 0) { set_error("wmh_collide: negative sizes"); return WMH_EINVAL; }
+static wmh_status collide_impl(const char *who, const void *sig_a, int64_t n_a, const void *sig_b, int64_t n_b,
+                               int32_t sig_bytes, uint32_t k, const int64_t *pairs, int64_t n_pairs, uint32_t *matches,
+                               float *jhat, int32_t check_pairs, void *stream) {
+    if (sig_bytes != 1 && sig_bytes != 2) { set_error("%s: sig_bytes=%d not in {1,2}", who, (int)sig_bytes); return WMH_EINVAL; }
+    if (k < 1) { set_error("%s: k must be >= 1", who); return WMH_EINVAL; }
+    if (n_pairs < 0 || n_a < 0 || n_b < 0) { set_error("%s: negative sizes", who); return WMH_EINVAL; }
     if (n_pairs == 0) return WMH_OK;
-    if (!sig || !pairs || !matches) { set_error("wmh_collide: NULL pointer"); return WMH_EINVAL; }
+    if (!sig_a || !sig_b || !pairs || !matches) { set_error("%s: NULL pointer", who); return WMH_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long *bad = nullptr;
     if (check_pairs) {
         WMH_CUDA_TRY(cudaMallocAsync((void **)&bad, sizeof(unsigned long long), s), "collide scratch");
         WMH_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s), "collide scratch memset");
     }
-    const bool vec = (((uintptr_t)sig) % 16 == 0) && (((int64_t)k * sig_bytes) % 16 == 0);
+    const bool vec = (((uintptr_t)sig_a) % 16 == 0) && (((uintptr_t)sig_b) % 16 == 0) && (((int64_t)k * sig_bytes) % 16 == 0);
     const int threads = 256;
     int64_t blocks = min((int64_t)num_sms() * 16, (n_pairs * 32 + threads - 1) / threads);
-    const uint8_t *sg = (const uint8_t *)sig;
-#define WMH_COLLIDE(SB, V) collide_kernel<SB, V><<<(unsigned)blocks, threads, 0, s>>>(sg, k, n_rows, pairs, n_pairs, matches, jhat, bad)
+    const uint8_t *ga = (const uint8_t *)sig_a, *gb = (const uint8_t *)sig_b;
+#define WMH_COLLIDE(SB, V) collide_kernel<SB, V><<<(unsigned)blocks, threads, 0, s>>>(ga, n_a, gb, n_b, k, pairs, n_pairs, matches, jhat, bad)
     if (sig_bytes == 2) { if (vec) WMH_COLLIDE(2, true); else WMH_COLLIDE(2, false); }
     else { if (vec) WMH_COLLIDE(1, true); else WMH_COLLIDE(1, false); }
 #undef WMH_COLLIDE
@@ -571,9 +591,22 @@ extern "C" wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k
         cudaError_t e2 = cudaStreamSynchronize(s);
         cudaFreeAsync(bad, s);
         if (e1 != cudaSuccess || e2 != cudaSuccess) return cuda_fail(e1 != cudaSuccess ? e1 : e2, "collide readback");
-        if (nb) { set_error("wmh_collide: %llu pairs index rows outside [0, %lld)", nb, (long long)n_rows); return WMH_EINVAL; }
+        if (nb) { set_error("%s: %llu pairs index rows outside [0, %lld) x [0, %lld)", who, nb, (long long)n_a, (long long)n_b); return WMH_EINVAL; }
     }
     return WMH_OK;
+}
+
+extern "C" wmh_status wmh_collide(const void *sig, int32_t sig_bytes, uint32_t k, int64_t n_rows, const int64_t *pairs,
+                                  int64_t n_pairs, uint32_t *matches, float *jhat, int32_t check_pairs, void *stream) {
+    return collide_impl("wmh_collide", sig, n_rows, sig, n_rows, sig_bytes, k, pairs, n_pairs, matches, jhat, check_pairs,
+                        stream);
+}
+
+extern "C" wmh_status wmh_collide2(const void *sig_a, int64_t n_a, const void *sig_b, int64_t n_b, int32_t sig_bytes,
+                                   uint32_t k, const int64_t *pairs, int64_t n_pairs, uint32_t *matches, float *jhat,
+                                   int32_t check_pairs, void *stream) {
+    return collide_impl("wmh_collide2", sig_a, n_a, sig_b, n_b, sig_bytes, k, pairs, n_pairs, matches, jhat, check_pairs,
+                        stream);
 }
 
 extern "C" const char *wmh_last_error(void) { return g_err; }

@@ -125,7 +125,7 @@ struct HashArgs {
     cudaStream_t stream;
     int chunk;           // TILED: 0 = auto, else 4/8/16/32
     uint32_t horizon;    // INDEX: draws filed per hash (0 = auto)
-    int tile = 0;        // TILED dense: 0 auto, 1 byte tile, 2 bit-plane tile
+    int tile = 0;        // TILED dense: 0 auto, 1 byte tile, 2 bit-plane tile, 3 bit-sliced tile
 };
 
 wmh_status launch_hash_simple(const HashArgs &a);
@@ -133,6 +133,8 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled);
+wmh_status launch_hash_bitslice(const HashArgs &a, bool *handled);
+bool bitslice_handles(const HashArgs &a);
 bool tiled_cm_full_tile(const HashArgs &a);
 wmh_status launch_hash_index(const HashArgs &a, uint32_t horizon);
 uint32_t index_k_max();

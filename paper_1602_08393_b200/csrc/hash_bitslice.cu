@@ -1,0 +1,667 @@
+// hash_bitslice.cu -- WMH_ALGO_TILED for dense uint8 rows: the bit-sliced tile,
+// lane = draw.
+//
+// Same draws, same result as every other kernel (the draw stream of hash j does
+// not depend on x, so one draw serves every row of a tile).  A CTA
+// stages R = 32*G rows as bit planes: for column c and a group g of 32 rows, P
+// words whose bit i is bit b of min(x[32g + i][c], 2^P - 1).  Alg. 5's test of
+// one draw (c, off) against the 32 rows of a group is the carry out of the
+// bit-serial sum x + L with L = 2^P - 1 - off:
+//
+//   green(x) <=> x > off <=> x + L >= 2^P,   carry_{b+1} = MAJ(x_b, L_b, carry_b)
+//
+// one LOP3 per plane for 32 rows (reading R2: strict, integer cells).
+//
+// Work of a warp per round: its 32 lanes take 64 consecutive draws t = tb + lane
+// and tb + 32 + lane of one hash (Alg. 3's loop, unrolled over
+// lanes).  Each lane decodes a draw once (column, offset, the L_b masks) and
+// tests it against all G groups.
+// Before loading any plane it compares the offset with the group's column
+// maximum gmax[c][g] (kept next to the planes): off >= gmax means no row of the
+// group is green, so most draws touch 2 bytes of shared memory instead of 4*P.
+// Rows green among the first 32 draws keep those masks (one REDUX.OR finds
+// them), the rest take the second 32; the merged masks (lane = draw, bit = row)
+// are transposed with five shuffle stages so that lane = row holds its draws as
+// bits, and the first green draw of every pending row is one __ffs: h = t + 1
+// (reading R1).
+// A row stays pending until it is green or the cap is reached (h = cap, R9);
+// all-zero rows never turn green and take the cap at once (R12).
+//
+// Clamped planes (CLAMP): when the bit count NB of the largest bound would not
+// let two groups fit, P = NB - 1 planes hold min(x, 2^P - 1) and gmax the true
+// maximum.  A draw with off >= 2^P - 1 is green only for rows whose clamped value
+// is all ones; when gmax says such a row exists (rare: the top cells of the few
+// columns with a large bound), those candidate rows are tested on their bytes
+// in global memory.
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace wmh {
+
+constexpr int BV_HB = 8;                  // hashes per claimed block (results flushed 8 per row)
+
+struct BvParams {
+    const uint8_t *x;
+    int64_t n_rows;
+    int D;
+    int n_hchunks, hchunk;
+    int64_t n_items;
+    uint32_t k, cap, M, uni_m;
+    uint64_t S;
+    int vec_flush, sigb;
+    const uint32_t *table;       // [k][T0] draw words (c << 8) | off; 0xFF (never green) at t >= cap
+    const uint32_t *pack;
+    void *sig;
+    unsigned long long *n_sat;
+    unsigned long long *item_ctr;
+    int or_bound;                // 1: gmax holds the OR of the group's bytes (an upper bound on the max)
+};
+
+// the draw word of cell r: (c << 8) | (r - CompToM[c]); t >= cap -> 0xFF, which
+// no group maximum exceeds (bounds <= 255), so the draw is red everywhere
+__device__ __forceinline__ uint32_t bv_word(uint32_t r, const uint32_t *pack, uint32_t uni_m, uint32_t t, uint32_t cap) {
+    return t < cap ? cell_of(r, pack, uni_m) : 0xFFu;
+}
+
+__global__ void bv_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
+                                const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t cap) {
+    const int64_t total = (int64_t)k * T0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
+        table[i] = bv_word(draw_r(S, j, t, M), pack, uni_m, t, cap);
+    }
+}
+
+__device__ __forceinline__ uint32_t bv_prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t bv_rotl(uint32_t y, uint32_t n) {
+    uint32_t d;
+    asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(d) : "r"(y), "r"(n));
+    return d;
+}
+
+// Per-lane constants of the 32x32 bit transpose (lane i holds row i of the
+// matrix; afterwards lane r holds column r).  Stage s swaps the off-diagonal
+// s x s blocks between lanes i and i ^ s: lanes with bit s clear keep their bits
+// r with r & s == 0 and take the partner's bits shifted up by s; the others keep
+// r & s != 0 and take the partner's bits shifted down.  Stages 16 and 8 move
+// whole bytes (one PRMT), stages 4, 2, 1 a rotate plus a select (LOP3).
+struct BvTranspose {
+    uint32_t sel16, sel8, amt4, keep4, amt2, keep2, amt1, keep1;
+    __device__ __forceinline__ explicit BvTranspose(int lane) {
+        sel16 = (lane & 16) ? 0x3276u : 0x5410u;
+        sel8 = (lane & 8) ? 0x3715u : 0x6240u;
+        amt4 = (lane & 4) ? 28u : 4u;
+        keep4 = (lane & 4) ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
+        amt2 = (lane & 2) ? 30u : 2u;
+        keep2 = (lane & 2) ? 0xCCCCCCCCu : 0x33333333u;
+        amt1 = (lane & 1) ? 31u : 1u;
+        keep1 = (lane & 1) ? 0xAAAAAAAAu : 0x55555555u;
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+        uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, 16);
+        x = bv_prmt(x, y, sel16);
+        y = __shfl_xor_sync(0xFFFFFFFFu, x, 8);
+        x = bv_prmt(x, y, sel8);
+        y = __shfl_xor_sync(0xFFFFFFFFu, x, 4);
+        x = (x & keep4) | (bv_rotl(y, amt4) & ~keep4);
+        y = __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+        x = (x & keep2) | (bv_rotl(y, amt2) & ~keep2);
+        y = __shfl_xor_sync(0xFFFFFFFFu, x, 1);
+        x = (x & keep1) | (bv_rotl(y, amt1) & ~keep1);
+        return x;
+    }
+};
+
+// 8x8 bit transpose of (hi:lo), byte i = row i -> byte b = bit b of rows 0..7
+__device__ __forceinline__ void bv_t8(uint32_t &lo, uint32_t &hi) {
+    uint32_t t;
+    t = (lo ^ (lo >> 7)) & 0x00AA00AAu; lo ^= t ^ (t << 7);
+    t = (hi ^ (hi >> 7)) & 0x00AA00AAu; hi ^= t ^ (t << 7);
+    t = (lo ^ (lo >> 14)) & 0x0000CCCCu; lo ^= t ^ (t << 14);
+    t = (hi ^ (hi >> 14)) & 0x0000CCCCu; hi ^= t ^ (t << 14);
+    t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
+}
+
+// Column block of the planes: W = G*P words.  P % 4 == 0: group-major [g][b]
+// (each group's planes one or two 16-byte loads, loaded only when the group
+// needs them); else plane-major [b][g] (the whole block in 16/8/4-byte loads).
+template <int P, int G>
+struct BvLayout {
+    static constexpr int W = G * P;
+    static constexpr bool GROUP_MAJOR = P % 4 == 0;
+    static __device__ __forceinline__ int idx(int g, int b) { return GROUP_MAJOR ? g * P + b : b * G + g; }
+};
+
+template <int P, int G>
+__device__ __forceinline__ void bv_load_group(const uint32_t *blk, int g, uint32_t (&x)[P]) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(blk + g * P);
+#pragma unroll
+    for (int i = 0; i < P / 4; i++) {
+        const uint4 v = q[i];
+        x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
+    }
+}
+
+template <int P, int G>
+__device__ __forceinline__ void bv_load_all(const uint32_t *blk, uint32_t (&x)[G][P]) {
+    constexpr int W = G * P;
+    uint32_t v[W];
+    if constexpr (W % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < W / 4; i++) {
+            const uint4 a = reinterpret_cast<const uint4 *>(blk)[i];
+            v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
+        }
+    } else if constexpr (W % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < W / 2; i++) {
+            const uint2 a = reinterpret_cast<const uint2 *>(blk)[i];
+            v[2 * i] = a.x; v[2 * i + 1] = a.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; i++) v[i] = blk[i];
+    }
+#pragma unroll
+    for (int g = 0; g < G; g++)
+#pragma unroll
+        for (int b = 0; b < P; b++) x[g][b] = v[BvLayout<P, G>::idx(g, b)];
+}
+
+// carry out of x + L over the P planes; m[b] = all-ones where bit b of L is set
+template <int P>
+__device__ __forceinline__ uint32_t bv_chain(const uint32_t (&x)[P], const uint32_t (&m)[P]) {
+    uint32_t c = x[0] & m[0];
+#pragma unroll
+    for (int b = 1; b < P; b++) c = (x[b] & m[b]) | (x[b] & c) | (m[b] & c);
+    return c;
+}
+
+// group maxima per column: G bytes (G <= 4) in one 1/2/4-byte word
+template <int G>
+using bv_gmax_t = typename std::conditional<G == 1, uint8_t, typename std::conditional<G == 2, uint16_t, uint32_t>::type>::type;
+
+// CLAMP: the draw (c, off >= 2^P - 1) against the rows of group g whose clamped
+// value is all ones (cand), read from the rows in global memory
+__device__ __noinline__ uint32_t bv_slow(const uint8_t *x, int64_t grow0, int D, uint32_t c, uint32_t off, uint32_t cand) {
+    uint32_t m = 0;
+    while (cand) {
+        const int i = __ffs(cand) - 1;
+        cand &= cand - 1;
+        m |= (uint32_t)(__ldg(x + (grow0 + i) * (int64_t)D + c) > off) << i;
+    }
+    return m;
+}
+
+// Green masks of the draw word w against the G groups (pending groups only):
+// the L_b masks are built once per draw; a group whose column maximum is at or
+// below the offset is red without touching its planes (R2).
+template <int P, int G, bool CLAMP>
+__device__ __forceinline__ void bv_test(const BvParams &p, const uint32_t *planes, const bv_gmax_t<G> *gmax, int64_t row0,
+                                        uint32_t w, const uint32_t (&pend)[G], uint32_t (&mask)[G]) {
+    constexpr int W = G * P;
+    constexpr uint32_t TOP = (1u << P) - 1u;
+    const uint32_t c = w >> 8, off = w & 0xFFu;
+    const uint32_t gm = (uint32_t)gmax[c];
+    const uint32_t *blk = planes + (size_t)c * W;
+    const uint32_t L = CLAMP ? (off < TOP ? TOP - off : 0u) : TOP - off;
+    const uint32_t Xh = L * 0x08040201u, Xl = L * 0x80402010u;
+    uint32_t m[P];
+#pragma unroll
+    for (int b = 0; b < P; b++) m[b] = bv_prmt(b < 4 ? Xl : Xh, 0, 0x8888u + 0x1111u * (uint32_t)(3 - (b & 3)));
+    bool need[G];
+    bool need_any = false;
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+        need[g] = pend[g] != 0u && off < ((gm >> (8 * g)) & 0xFFu);
+        need_any |= need[g];
+    }
+    if constexpr (BvLayout<P, G>::GROUP_MAJOR) {
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            uint32_t xg[P];
+#pragma unroll
+            for (int b = 0; b < P; b++) xg[b] = 0u;
+            if (need[g]) bv_load_group<P, G>(blk, g, xg);
+            mask[g] = bv_chain<P>(xg, m);
+            if (CLAMP && need[g] && off >= TOP) {
+                uint32_t cand = xg[0];
+#pragma unroll
+                for (int b = 1; b < P; b++) cand &= xg[b];
+                mask[g] = bv_slow(p.x, row0 + 32 * g, p.D, c, off, cand);
+            }
+        }
+    } else {
+        uint32_t xa[G][P];
+#pragma unroll
+        for (int g = 0; g < G; g++)
+#pragma unroll
+            for (int b = 0; b < P; b++) xa[g][b] = 0u;
+        if (need_any) bv_load_all<P, G>(blk, xa);
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            mask[g] = need[g] ? bv_chain<P>(xa[g], m) : 0u;
+            if (CLAMP && need[g] && off >= TOP) {
+                uint32_t cand = xa[g][0];
+#pragma unroll
+                for (int b = 1; b < P; b++) cand &= xa[g][b];
+                mask[g] = bv_slow(p.x, row0 + 32 * g, p.D, c, off, cand);
+            }
+        }
+    }
+}
+
+template <int P, int G, bool CLAMP, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvParams p) {
+    constexpr int R = 32 * G;
+    constexpr int W = G * P;
+    constexpr uint32_t TOP = (1u << P) - 1u;
+    using gm_t = bv_gmax_t<G>;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *planes = smem;                                                         // [D][W]
+    gm_t *gmax = reinterpret_cast<gm_t *>(planes + (size_t)p.D * W);                 // [D] (G bytes each)
+    uint16_t *hres_all = reinterpret_cast<uint16_t *>(
+        reinterpret_cast<uint8_t *>(gmax) + (((size_t)p.D * sizeof(gm_t) + 15) & ~(size_t)15));   // [NW][HB][R]
+    uint8_t *gbytes = reinterpret_cast<uint8_t *>(gmax);
+    uint8_t *pbytes = reinterpret_cast<uint8_t *>(planes);
+    __shared__ long long s_item, s_next;
+    __shared__ int s_hash;
+    __shared__ uint32_t s_live[G];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint16_t *hres_blk = hres_all + warp * BV_HB * R;
+    unsigned long long sat = 0;
+    const int quads = p.D >> 2;                        // D % 4 == 0 (launcher)
+    const BvTranspose tr(lane);
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(p.item_ctr, 1ull);
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_item = s_next;
+            s_next = (long long)atomicAdd(p.item_ctr, 1ull);
+            s_hash = 0;
+        }
+        if (threadIdx.x < G) s_live[threadIdx.x] = 0;
+        __syncthreads();
+        const long long item = s_item;
+        if (item >= p.n_items) break;
+        if (s_next < p.n_items) {                      // warm L2 with the next item's rows
+            const int64_t nrow0 = (s_next / p.n_hchunks) * R;
+            const int64_t nbytes = min((int64_t)R, p.n_rows - nrow0) * (int64_t)p.D;
+            const char *base = reinterpret_cast<const char *>(p.x + nrow0 * (int64_t)p.D);
+            for (int64_t off = (int64_t)threadIdx.x * 128; off < nbytes; off += (int64_t)NT * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        }
+        const int64_t tile = item / p.n_hchunks;
+        const int hc = (int)(item % p.n_hchunks);
+        const int64_t row0 = tile * R;
+        const int nr = (int)min((int64_t)R, p.n_rows - row0);
+        const uint32_t j0 = (uint32_t)hc * p.hchunk, j1 = min(p.k, j0 + (uint32_t)p.hchunk);
+
+        // ---- a5: stage the tile as bit planes + per-(column, group) maxima.
+        //      Unit = (column quad, group, octet of 8 rows), octet fastest: 8
+        //      words in, 4 columns x P plane bytes out; the 4 octet lanes of a
+        //      (quad, group) combine their column maxima with two shuffles
+        for (int u = threadIdx.x; u < quads * G * 4; u += NT) {
+            const int o = u & 3, g = (u >> 2) % G, cq = (u >> 2) / G;
+            const int rb = 32 * g + 8 * o;
+            uint32_t w[8];
+            uint32_t live = 0, mx = 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const bool ok = rb + i < nr;
+                w[i] = ok ? __ldg(reinterpret_cast<const uint32_t *>(p.x + (row0 + rb + i) * (int64_t)p.D) + cq) : 0u;
+                live |= (w[i] != 0u) << i;
+                mx = p.or_bound ? (mx | w[i]) : __vmaxu4(mx, w[i]);
+                if (CLAMP) w[i] = __vminu4(w[i], TOP * 0x01010101u);
+            }
+            const unsigned am = __activemask();
+            if (p.or_bound) {
+                mx |= __shfl_xor_sync(am, mx, 1);
+                mx |= __shfl_xor_sync(am, mx, 2);
+            } else {
+                mx = __vmaxu4(mx, __shfl_xor_sync(am, mx, 1));
+                mx = __vmaxu4(mx, __shfl_xor_sync(am, mx, 2));
+            }
+            if (o == 0) {
+#pragma unroll
+                for (int u4 = 0; u4 < 4; u4++) gbytes[(size_t)(4 * cq + u4) * sizeof(gm_t) + g] = (uint8_t)(mx >> (8 * u4));
+            }
+            if (live) atomicOr(&s_live[g], live << (8 * o));
+            // 4x4 byte transposes: col[u4] = byte u4 of rows 0..3 (lo) and 4..7 (hi)
+            uint32_t lo[4], hi[4];
+            {
+                const uint32_t t0 = bv_prmt(w[0], w[1], 0x5140), t1 = bv_prmt(w[0], w[1], 0x7362);
+                const uint32_t t2 = bv_prmt(w[2], w[3], 0x5140), t3 = bv_prmt(w[2], w[3], 0x7362);
+                lo[0] = bv_prmt(t0, t2, 0x5410); lo[1] = bv_prmt(t0, t2, 0x7632);
+                lo[2] = bv_prmt(t1, t3, 0x5410); lo[3] = bv_prmt(t1, t3, 0x7632);
+                const uint32_t s0 = bv_prmt(w[4], w[5], 0x5140), s1 = bv_prmt(w[4], w[5], 0x7362);
+                const uint32_t s2 = bv_prmt(w[6], w[7], 0x5140), s3 = bv_prmt(w[6], w[7], 0x7362);
+                hi[0] = bv_prmt(s0, s2, 0x5410); hi[1] = bv_prmt(s0, s2, 0x7632);
+                hi[2] = bv_prmt(s1, s3, 0x5410); hi[3] = bv_prmt(s1, s3, 0x7632);
+            }
+#pragma unroll
+            for (int u4 = 0; u4 < 4; u4++) {
+                uint32_t a = lo[u4], b = hi[u4];
+                bv_t8(a, b);
+                uint8_t *dst = pbytes + (size_t)(4 * cq + u4) * W * 4 + o;
+#pragma unroll
+                for (int pb = 0; pb < P; pb++)
+                    dst[4 * BvLayout<P, G>::idx(g, pb)] = (uint8_t)((pb < 4 ? a : b) >> (8 * (pb & 3)));
+            }
+        }
+        __syncthreads();
+
+        // ---- hashes: a warp claims blocks of BV_HB consecutive hashes (the next
+        //      block one block ahead) and flushes a block's results with one
+        //      16-byte store per row
+        auto grab = [&]() {
+            int bb = 0;
+            if (lane == 0) bb = atomicAdd(&s_hash, 1);
+            return min(j1, j0 + (uint32_t)BV_HB * (uint32_t)__shfl_sync(0xFFFFFFFFu, bb, 0));
+        };
+        uint32_t pend0[G], dead[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const uint32_t valid = 32 * g + 32 <= nr ? 0xFFFFFFFFu : (32 * g >= nr ? 0u : (1u << (nr - 32 * g)) - 1u);
+            pend0[g] = s_live[g] & valid;
+            dead[g] = valid & ~s_live[g];
+        }
+        uint32_t jb = grab();                          // current block [jb, je)
+        uint32_t je = min(j1, jb + BV_HB);
+        uint32_t jb_next = jb < j1 ? grab() : j1;
+        uint32_t j = jb;
+        // draw words: lane holds t = tb + lane (A) and tb + 32 + lane (B) of the
+        // current round, the next round's pair, and the next hash's first pair
+        uint32_t na = 0, nb = 0;
+        if (j < j1) {
+            na = __ldg(p.table + (int64_t)j * T0 + lane);
+            nb = __ldg(p.table + (int64_t)j * T0 + 32 + lane);
+        }
+        while (j < j1) {
+            const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
+            uint16_t *hres = hres_blk + (j - jb) * R;
+            const uint32_t *tj = p.table + (int64_t)j * T0;
+            const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
+            uint32_t wA = na, wB = nb;
+            uint32_t xA = 0, xB = 0;                   // the next round's words
+            if (64 < T0) {
+                xA = __ldg(tj + 64 + lane);
+                xB = __ldg(tj + 96 + lane);
+            }
+            if (jn < j1) {                             // one hash ahead
+                na = __ldg(p.table + (int64_t)jn * T0 + lane);
+                nb = __ldg(p.table + (int64_t)jn * T0 + 32 + lane);
+            }
+            // all-zero rows: cap at once (lane = row)
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                if ((dead[g] >> lane) & 1u) hres[32 * g + lane] = (uint16_t)p.cap;
+                sat += (lane == 0) ? __popc(dead[g]) : 0;
+            }
+            uint32_t pend[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) pend[g] = pend0[g];
+            for (uint32_t tb = 0;; tb += 64) {
+                uint32_t anyp = 0;
+#pragma unroll
+                for (int g = 0; g < G; g++) anyp |= pend[g];
+                if (!anyp) break;
+                if (tb >= p.cap) {                     // a8: no green draw before the cap
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        if ((pend[g] >> lane) & 1u) hres[32 * g + lane] = (uint16_t)p.cap;
+                        sat += (lane == 0) ? __popc(pend[g]) : 0;
+                    }
+                    break;
+                }
+                const uint32_t w0 = wA, w1 = wB;
+                // prefetch the round after next (the table holds t < T0; later draws are computed)
+                wA = xA;
+                wB = xB;
+                {
+                    const uint32_t t2 = tb + 128 + lane;
+                    if (tb + 128 < (uint32_t)T0) {
+                        xA = __ldg(tj + t2);
+                        xB = __ldg(tj + t2 + 32);
+                    } else if (tb + 128 < p.cap) {
+                        xA = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t2), p.M), p.pack, p.uni_m, t2, p.cap);
+                        xB = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)(t2 + 32)), p.M), p.pack, p.uni_m, t2 + 32, p.cap);
+                    }
+                }
+                uint32_t mA[G], mB[G];
+                bv_test<P, G, CLAMP>(p, planes, gmax, row0, w0, pend, mA);
+                bv_test<P, G, CLAMP>(p, planes, gmax, row0, w1, pend, mB);
+                // ---- a8: the first green draw of each pending row.  Rows green among
+                //      the first 32 draws (RA) keep those; the others take the second
+                //      32; one transpose per group then gives lane = row its draws
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    const uint32_t a = mA[g] & pend[g];
+                    const uint32_t RA = __reduce_or_sync(0xFFFFFFFFu, a);
+                    const uint32_t u = a | (mB[g] & pend[g] & ~RA);
+                    const uint32_t Rall = __reduce_or_sync(0xFFFFFFFFu, u);
+                    if (Rall) {                                               // warp-uniform
+                        const uint32_t wt = tr(u);                            // bit i: draw (tb or tb+32) + i green for row lane
+                        if (wt) hres[32 * g + lane] = (uint16_t)(tb + (((RA >> lane) & 1u) ? 0u : 32u) + (uint32_t)__ffs(wt));
+                        pend[g] &= ~Rall;
+                    }
+                }
+            }
+            __syncwarp();
+            if (j + 1 == je) {
+                // ---- a9: flush the block: row r's hashes jb..je-1 are contiguous in sig
+                const int64_t eoff = (row0 + lane) * (int64_t)p.k + jb;
+                const int nh = (int)(je - jb);
+                if (nh == BV_HB && p.vec_flush) {
+                    for (int r = lane; r < nr; r += 32) {
+                        const int64_t e = eoff + (int64_t)(r - lane) * p.k;
+                        uint32_t hv[BV_HB];
+#pragma unroll
+                        for (int u = 0; u < BV_HB; u++) hv[u] = hres_blk[u * R + r];
+                        if (p.sigb == 2) {
+                            uint16_t *ptr = reinterpret_cast<uint16_t *>(p.sig) + e;
+                            const uint4 v = make_uint4(hv[0] | (hv[1] << 16), hv[2] | (hv[3] << 16),
+                                                       hv[4] | (hv[5] << 16), hv[6] | (hv[7] << 16));
+                            if (p.vec_flush == 2) {
+                                *reinterpret_cast<uint4 *>(ptr) = v;
+                            } else {
+                                reinterpret_cast<uint2 *>(ptr)[0] = make_uint2(v.x, v.y);
+                                reinterpret_cast<uint2 *>(ptr)[1] = make_uint2(v.z, v.w);
+                            }
+                        } else {
+                            uint8_t *ptr = reinterpret_cast<uint8_t *>(p.sig) + e;
+                            *reinterpret_cast<uint2 *>(ptr) = make_uint2(hv[0] | (hv[1] << 8) | (hv[2] << 16) | (hv[3] << 24),
+                                                                         hv[4] | (hv[5] << 8) | (hv[6] << 16) | (hv[7] << 24));
+                        }
+                    }
+                } else {
+                    for (int r = lane; r < nr; r += 32) {
+                        const int64_t e = eoff + (int64_t)(r - lane) * p.k;
+                        for (int u = 0; u < nh; u++) {
+                            if (p.sigb == 2) reinterpret_cast<uint16_t *>(p.sig)[e + u] = hres_blk[u * R + r];
+                            else reinterpret_cast<uint8_t *>(p.sig)[e + u] = (uint8_t)hres_blk[u * R + r];
+                        }
+                    }
+                }
+                __syncwarp();
+                jb = jb_next;
+                je = min(j1, jb + BV_HB);
+                jb_next = jb < j1 ? grab() : j1;
+            }
+            j = jn;
+        }
+    }
+    if (p.n_sat) {
+        for (int o = 16; o; o >>= 1) sat += __shfl_xor_sync(0xFFFFFFFFu, sat, o);
+        if (lane == 0 && sat) atomicAdd(p.n_sat, sat);
+    }
+}
+
+static size_t bv_smem(int D, int G, int P, int NT) {
+    const size_t gm_bytes = (size_t)D * (G == 1 ? 1 : G == 2 ? 2 : 4);
+    return (size_t)D * G * P * 4 + ((gm_bytes + 15) & ~(size_t)15) + (size_t)(NT / 32) * BV_HB * 32 * G * 2;
+}
+
+template <int P, int G, bool CLAMP, int NT>
+static void bv_launch(const BvParams &p, size_t smem, int grid, cudaStream_t s) {
+    auto kern = hash_bitslice_kernel<P, G, CLAMP, NT>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_timer_begin(s);
+    kern<<<grid, NT, smem, s>>>(p);
+    kernel_timer_end(s);
+}
+
+template <int P, bool CLAMP>
+static void bv_launch_g(int G, int NT, const BvParams &p, size_t smem, int grid, cudaStream_t s) {
+    if (NT == 256) {
+        if (G == 4) bv_launch<P, 4, CLAMP, 256>(p, smem, grid, s);
+        else if (G == 2) bv_launch<P, 2, CLAMP, 256>(p, smem, grid, s);
+        else bv_launch<P, 1, CLAMP, 256>(p, smem, grid, s);
+    } else {
+        if (G == 4) bv_launch<P, 4, CLAMP, 512>(p, smem, grid, s);
+        else if (G == 2) bv_launch<P, 2, CLAMP, 512>(p, smem, grid, s);
+        else bv_launch<P, 1, CLAMP, 512>(p, smem, grid, s);
+    }
+}
+
+template <int P>
+static void bv_launch_p(int G, bool clamp, int NT, const BvParams &p, size_t smem, int grid, cudaStream_t s) {
+    if (clamp) {
+        if constexpr (P >= 4 && P < 8) bv_launch_g<P, true>(G, NT, p, smem, grid, s);
+        return;
+    }
+    bv_launch_g<P, false>(G, NT, p, smem, grid, s);
+}
+
+#define WMH_BV_P_SWITCH(PV, CALL) \
+    switch (PV) {                 \
+        case 1: CALL(1); break;   \
+        case 2: CALL(2); break;   \
+        case 3: CALL(3); break;   \
+        case 4: CALL(4); break;   \
+        case 5: CALL(5); break;   \
+        case 6: CALL(6); break;   \
+        case 7: CALL(7); break;   \
+        default: CALL(8); break;  \
+    }
+
+// Shape of the tile for a layout: planes P (clamped: NB - 1), groups G of 32
+// rows, threads per CTA NT and CTAs per SM (512 -> 1, 256 -> 2); G = 0 when
+// the rows are too long for even one group of exact planes.
+struct BvShape {
+    int P, G;
+    bool clamp;
+    int NT, ctas;
+};
+
+static BvShape bv_shape(const HashArgs &a) {
+    const int D = (int)a.rows.dim;
+    const int NB = 32 - __builtin_clz(a.L->max_bound);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int smem_optin = 0, smem_sm = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    static const int g_env = getenv("WMH_BV_GROUPS") ? atoi(getenv("WMH_BV_GROUPS")) : 0;
+    static const int c_env = getenv("WMH_BV_CTAS") ? atoi(getenv("WMH_BV_CTAS")) : 1;
+    const int gmax_try = (g_env == 1 || g_env == 2 || g_env == 4) ? g_env : 4;
+    const int ctas = c_env == 2 ? 2 : 1, NT = 512 / ctas;
+    const size_t budget = std::min((size_t)smem_optin, (size_t)smem_sm / ctas - 1024) - 64;
+    for (int G = gmax_try; G >= 1; G /= 2) {
+        if (bv_smem(D, G, NB, NT) <= budget) return {NB, G, false, NT, ctas};
+        // one plane fewer (clamped) when it buys this group count
+        if (G >= 2 && NB >= 5 && bv_smem(D, G, NB - 1, NT) <= budget) return {NB - 1, G, true, NT, ctas};
+    }
+    return {NB, 0, false, NT, ctas};
+}
+
+bool bitslice_handles(const HashArgs &a) {
+    const int D = (int)a.rows.dim;
+    if (a.rows.kind != WMH_DENSE || (D & 3) || ((uintptr_t)a.rows.dense & 3)) return false;
+    if ((a.L->flags & WMH_LAYOUT_WIDE) || weight_bytes(a.rows) != 1 || a.L->max_bound == 0 || a.L->max_bound > 255) return false;
+    if ((uint64_t)D >= (1ull << 24)) return false;
+    return bv_shape(a).G >= 1;
+}
+
+wmh_status launch_hash_bitslice(const HashArgs &a, bool *handled) {
+    *handled = false;
+    if (!bitslice_handles(a)) return WMH_OK;
+    const int D = (int)a.rows.dim;
+    const BvShape sh = bv_shape(a);
+    const int G = sh.G, P = sh.P, R = 32 * G;
+    const size_t smem = bv_smem(D, G, P, sh.NT);
+    *handled = true;
+
+    const int64_t n_tiles = (a.rows.n_rows + R - 1) / R;
+    const int sms = num_sms();
+    // >= 8 items per SM for balance, but >= WMH_MIN_HCHUNK hashes per item: each
+    // item stages its whole tile, so small batches must not slice k too thin
+    static const int min_hc = getenv("WMH_MIN_HCHUNK") ? std::max(8, atoi(getenv("WMH_MIN_HCHUNK"))) : 128;
+    int n_hchunks = (int)std::max((int64_t)1, std::min((int64_t)(a.k + min_hc - 1) / min_hc, ((int64_t)sms * sh.ctas * 8 + n_tiles - 1) / n_tiles));
+    const int hchunk = (int)(((a.k + n_hchunks - 1) / n_hchunks + BV_HB - 1) / BV_HB * BV_HB);
+    n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
+
+    uint8_t *scratch = nullptr;
+    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint32_t);
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "bitslice scratch alloc");
+    uint32_t *table = reinterpret_cast<uint32_t *>(scratch);
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
+    WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "bitslice counter memset");
+    const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
+    {
+        const int64_t total = (int64_t)a.k * T0;
+        const int blocks = (int)std::min((int64_t)sms * 8, (total + 255) / 256);
+        bv_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, (uint32_t)a.L->M, a.L->cell_pack, uni_m, a.cap);
+        count_launch();
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { cudaFreeAsync(scratch, a.stream); return cuda_fail(e, "bitslice table launch"); }
+    }
+
+    BvParams p;
+    p.x = a.rows.dense;
+    p.n_rows = a.rows.n_rows;
+    p.D = D;
+    p.n_hchunks = n_hchunks;
+    p.hchunk = hchunk;
+    p.n_items = n_tiles * n_hchunks;
+    p.k = a.k;
+    p.cap = a.cap;
+    p.M = (uint32_t)a.L->M;
+    p.uni_m = uni_m;
+    p.S = a.S;
+    p.sigb = a.sig_bytes;
+    p.vec_flush = 0;
+    if (a.sig_bytes == 2 && a.k % 4 == 0 && (uintptr_t)a.sig % 8 == 0)
+        p.vec_flush = (a.k % 8 == 0 && (uintptr_t)a.sig % 16 == 0) ? 2 : 1;
+    if (a.sig_bytes == 1 && a.k % 8 == 0 && (uintptr_t)a.sig % 8 == 0) p.vec_flush = 1;
+    p.table = table;
+    p.pack = a.L->cell_pack;
+    p.sig = a.sig;
+    p.n_sat = a.n_sat;
+    p.item_ctr = ctr;
+    static const int or_env = getenv("WMH_BV_OR") ? atoi(getenv("WMH_BV_OR")) : 0;
+    p.or_bound = or_env;
+    const int grid = (int)std::min((int64_t)sms * sh.ctas, p.n_items);
+#define WMH_BV_GO(V) bv_launch_p<V>(G, sh.clamp, sh.NT, p, smem, grid, a.stream)
+    WMH_BV_P_SWITCH(P, WMH_BV_GO)
+#undef WMH_BV_GO
+    WMH_LAUNCH_CHECK("hash_bitslice launch");
+    if (getenv("WMH_TILED_STATS"))
+        fprintf(stderr, "[wmh bitslice] P=%d clamp=%d G=%d NT=%d grid=%d items=%lld hchunk=%d smem=%zu or=%d\n", P, (int)sh.clamp, G,
+                sh.NT, grid, (long long)p.n_items, hchunk, smem, p.or_bound);
+    cudaFreeAsync(scratch, a.stream);
+    return WMH_OK;
+}
+
+}  // namespace wmh

@@ -995,9 +995,12 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     const wmh_layout *L = a.L;
     const uint32_t M = (uint32_t)L->M;
     if (a.rows.n_rows == 0) return WMH_OK;
-    WMH_CUDA_TRY(cudaMemsetAsync(ix.ctr, 0, 8, a.stream), "index row counter");
+    // a row counter of this call's own (stream-ordered): two runs of one index
+    // on different streams must not share the work-stealing counter
+    unsigned long long *ctr = nullptr;
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&ctr, 8, a.stream), "index row counter alloc");
+    if (cudaMemsetAsync(ctr, 0, 8, a.stream) != cudaSuccess) { cudaFreeAsync(ctr, a.stream); return cuda_fail(cudaGetLastError(), "index row counter"); }
     wmh_status st = WMH_OK;
-    unsigned long long *ctr = ix.ctr;
     const uint32_t *pos = ix.pos, *vals = ix.vals;
     const uint2 *table = ix.table;
     const IxEpochs ep = ix.ep;
@@ -1042,12 +1045,19 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     uint8_t *oscr = nullptr;
     if ((order_env == 1 || (order_env < 0 && big_tables)) && a.rows.n_rows >= 4096 && a.rows.n_rows < (1ll << 32)) {
         const size_t pe_b = ((size_t)a.rows.n_rows + 255) & ~(size_t)255, pm_b = (size_t)a.rows.n_rows * 4;
-        WMH_CUDA_TRY(cudaMallocAsync((void **)&oscr, pe_b + pm_b + 2 * IX_MAXE * 4 + 256, a.stream), "index order alloc");
+        if (cudaMallocAsync((void **)&oscr, pe_b + pm_b + 2 * IX_MAXE * 4 + 256, a.stream) != cudaSuccess) {
+            cudaFreeAsync(ctr, a.stream);
+            return cuda_fail(cudaGetLastError(), "index order alloc");
+        }
         uint8_t *row_epoch = oscr;
         uint32_t *perm = reinterpret_cast<uint32_t *>(oscr + pe_b);
         unsigned int *cnt = reinterpret_cast<unsigned int *>(oscr + pe_b + ((pm_b + 255) & ~(size_t)255));
         unsigned int *cursor = cnt + IX_MAXE;
-        WMH_CUDA_TRY(cudaMemsetAsync(cnt, 0, 2 * IX_MAXE * 4, a.stream), "index order memset");
+        if (cudaMemsetAsync(cnt, 0, 2 * IX_MAXE * 4, a.stream) != cudaSuccess) {
+            cudaFreeAsync(oscr, a.stream);
+            cudaFreeAsync(ctr, a.stream);
+            return cuda_fail(cudaGetLastError(), "index order memset");
+        }
         const int blocks = (int)std::min<int64_t>((int64_t)num_sms() * 8, (a.rows.n_rows * 32 + 255) / 256);
         const int wbo = weight_bytes(a.rows);
         if (csr) {
@@ -1061,7 +1071,7 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
         const int sblocks = (int)std::min<int64_t>((int64_t)num_sms() * 8, (a.rows.n_rows + 255) / 256);
         ix_order_scatter<<<sblocks, 256, 0, a.stream>>>(a.rows.n_rows, ep.E, row_epoch, cnt, cursor, perm);
         count_launch();
-        if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(oscr, a.stream); return cuda_fail(cudaGetLastError(), "index order"); }
+        if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(oscr, a.stream); cudaFreeAsync(ctr, a.stream); return cuda_fail(cudaGetLastError(), "index order"); }
         p.perm = perm;
     }
     // warps per row: >= 2; keep <= ~128 KiB of h[] per SM at 64 resident warps
@@ -1073,6 +1083,7 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     if (a.sig_bytes == 1) st = csr ? ix_launch_w<1, true>(p, nw, wb, a.stream) : ix_launch_w<1, false>(p, nw, wb, a.stream);
     else st = csr ? ix_launch_w<2, true>(p, nw, wb, a.stream) : ix_launch_w<2, false>(p, nw, wb, a.stream);
     if (oscr) cudaFreeAsync(oscr, a.stream);
+    cudaFreeAsync(ctr, a.stream);
     return st;
 }
 

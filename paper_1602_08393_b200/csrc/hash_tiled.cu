@@ -394,6 +394,13 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     // (measured: c5's recipe, 10^6 rows, NB = 6: 18.1 vs 21.2 ms; on c2's
     // 128-row tile the SWAR byte tile stays ahead, 0.58 vs 0.75 ms);
     // WMH_TILED_BS=1 / 0 or the WMH_OPT_TILE_* flags force the choice
+    // the lane-per-draw bit-sliced tile (hash_bitslice.cu) first: AUTO or
+    // WMH_OPT_TILE_BITSLICE; WMH_TILED_BV=0 drops it from AUTO
+    static const int bv_env = getenv("WMH_TILED_BV") ? atoi(getenv("WMH_TILED_BV")) : -1;
+    if (!force_rm && (a.tile == 3 || (a.tile == 0 && bv_env != 0))) {
+        const wmh_status vst = launch_hash_bitslice(a, handled);
+        if (vst != WMH_OK || *handled) return vst;
+    }
     static const int bs_env = getenv("WMH_TILED_BS") ? atoi(getenv("WMH_TILED_BS")) : -1;
     const bool want_bs = a.tile == 2 || (a.tile == 0 && (bs_env == 1 || (bs_env != 0 && !tiled_cm_full_tile(a))));
     if (!force_rm && want_bs) {

@@ -485,6 +485,69 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     return WMH_OK;
 }
 
+// Rows against an existing layout (Eq. 2 needs x_c <= m_c for every row that is
+// hashed, not only for the rows prepare saw): the same checks as wmh_prepare's
+// bounds pass -- one column-max pass for dense rows (the first offender located
+// only when a column fails), one warp per CSR row.  Synchronises once.
+extern "C" wmh_status wmh_check_rows(const wmh_layout *L, const wmh_rows *rows, void *stream) {
+    if (!L) { set_error("wmh_check_rows: layout is NULL"); return WMH_EINVAL; }
+    wmh_status st = check_rows(rows, true);
+    if (st != WMH_OK) return st;
+    if (rows->dim != L->dim) { set_error("wmh_check_rows: rows dim %lld != layout dim %lld", (long long)rows->dim, (long long)L->dim); return WMH_EINVAL; }
+    if (rows->n_rows == 0) return WMH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t dim = L->dim;
+    const int sms = num_sms();
+    uint8_t *scr = nullptr;
+    const size_t scr_b = 256 + (rows->kind == WMH_DENSE ? sizeof(uint32_t) * (size_t)dim : 0);
+    WMH_CUDA_TRY(cudaMallocAsync((void **)&scr, scr_b, s), "check_rows scratch alloc");
+    unsigned long long *bad = reinterpret_cast<unsigned long long *>(scr);
+    unsigned long long fb = ~0ull;
+    cudaMemcpyAsync(bad, &fb, sizeof fb, cudaMemcpyHostToDevice, s);
+    if (rows->kind == WMH_DENSE) {
+        uint32_t *cm = reinterpret_cast<uint32_t *>(scr + 256);
+        st = wmh_colmax(rows, cm, stream);
+        if (st != WMH_OK) { cudaFreeAsync(scr, s); return st; }
+        colmax_exceeds<<<(unsigned)((dim + 255) / 256), 256, 0, s>>>(cm, L->bounds, dim, bad);
+    } else if (weight_bytes(*rows) == 2) {
+        check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, reinterpret_cast<const uint16_t *>(rows->val),
+                                          rows->n_rows, dim, rows->nnz, L->bounds, bad);
+    } else {
+        check_csr<<<sms * 8, 256, 0, s>>>(rows->row_ptr, rows->col, rows->val, rows->n_rows, dim, rows->nnz, L->bounds, bad);
+    }
+    count_launch();
+    cudaMemcpyAsync(&fb, bad, sizeof fb, cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && fb != ~0ull && rows->kind == WMH_DENSE) {      // locate the first offender
+        fb = ~0ull;
+        cudaMemcpyAsync(bad, &fb, sizeof fb, cudaMemcpyHostToDevice, s);
+        if (weight_bytes(*rows) == 2)
+            check_dense_bounds<<<sms * 8, 256, 0, s>>>(reinterpret_cast<const uint16_t *>(rows->dense), rows->n_rows, dim,
+                                                       L->bounds, bad);
+        else
+            check_dense_bounds<<<sms * 8, 256, 0, s>>>(rows->dense, rows->n_rows, dim, L->bounds, bad);
+        count_launch();
+        cudaMemcpyAsync(&fb, bad, sizeof fb, cudaMemcpyDeviceToHost, s);
+        e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) {
+            cudaFreeAsync(scr, s);
+            set_error("wmh_check_rows: weight x[%lld][%lld] exceeds its bound", (long long)(fb / (unsigned long long)dim),
+                      (long long)(fb % (unsigned long long)dim));
+            return WMH_EBOUND;
+        }
+    }
+    cudaFreeAsync(scr, s);
+    if (e != cudaSuccess) return cuda_fail(e, "check_rows readback");
+    if (fb != ~0ull) {
+        const unsigned code = (unsigned)(fb & 7ull);
+        static const char *what[] = {"", "column index out of range", "columns not strictly ascending",
+                                     "value exceeds its bound", "row_ptr malformed"};
+        set_error("wmh_check_rows: CSR nonzero %lld: %s", (long long)(fb >> 3), what[code <= 4 ? code : 0]);
+        return code == 3 ? WMH_EBOUND : WMH_EINVAL;
+    }
+    return WMH_OK;
+}
+
 extern "C" wmh_status wmh_layout_digest(const wmh_layout *L, uint64_t *digest) {
     if (!L || !digest) { set_error("wmh_layout_digest: NULL argument"); return WMH_EINVAL; }
     *digest = L->digest;

@@ -148,3 +148,29 @@ extern "C" wmh_status wmh_scale_objective(const wmh_rows *rows, const float *sca
     cudaFreeAsync(scr, s);
     return st;
 }
+
+// Sec. 4's alpha = arg max sum(alpha x) / sum(ceil(alpha m)) over the
+// candidate grid, evaluated with wmh_scale_objective: among the scales that do
+// not saturate a uint16 weight, the largest mean effective sparsity
+// num / den (compared exactly as num_a * den_b > num_b * den_a in 128 bits);
+// ties go to the smaller scale (the smaller M; reading R18).
+extern "C" wmh_status wmh_choose_scale(const wmh_rows *rows, const float *scales, int32_t n_scales, int32_t *best,
+                                       void *stream) {
+    if (!best) { set_error("wmh_choose_scale: best is NULL"); return WMH_EINVAL; }
+    *best = -1;
+    if (n_scales < 1 || n_scales > 1024) { set_error("wmh_choose_scale: n_scales=%d not in [1, 1024]", (int)n_scales); return WMH_EINVAL; }
+    uint64_t obj[3 * 1024];
+    wmh_status st = wmh_scale_objective(rows, scales, n_scales, obj, stream);
+    if (st != WMH_OK) return st;
+    int b = -1;
+    for (int a = 0; a < n_scales; a++) {
+        const uint64_t num = obj[3 * a], den = obj[3 * a + 1], clipped = obj[3 * a + 2];
+        if (den == 0 || clipped) continue;
+        if (b < 0) { b = a; continue; }
+        const unsigned __int128 lhs = (unsigned __int128)num * obj[3 * b + 1], rhs = (unsigned __int128)obj[3 * b] * den;
+        if (lhs > rhs || (lhs == rhs && scales[a] < scales[b])) b = a;
+    }
+    if (b < 0) { set_error("wmh_choose_scale: every candidate scale quantises the rows to zero or saturates a weight"); return WMH_EINVAL; }
+    *best = b;
+    return WMH_OK;
+}

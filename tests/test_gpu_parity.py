@@ -169,13 +169,13 @@ def test_hash_edge_cases_dense(wmh, algo):
     assert out.shape == (0, 8)
 
 
-@pytest.mark.parametrize("tile", ["bitplanes", "bytes"])
+@pytest.mark.parametrize("tile", ["bitslice", "bitplanes", "bytes"])
 @pytest.mark.parametrize("D,n", [(64, 333), (1024, 200), (2048, 100), (4096, 70)])
 @pytest.mark.parametrize("mx", [1, 2, 3, 7, 12, 16, 31, 50, 100, 255])
 def test_tiled_bitplanes(wmh, D, n, mx, tile):
-    """Both dense tiles; the bit-sliced one (hash_tiled_bs.cu) at every plane count NB = 1..8 (the
-    largest bound mx), 8/4/2/1 groups of 32 rows and padded or packed plane blocks (D), ragged last tile, all-zero
-    rows, rows at the bound, a small cap and the uint8 signature width."""
+    """The three dense tiles; the bit-sliced ones (hash_bitslice.cu, hash_tiled_bs.cu) at every plane count
+    NB = 1..8 (the largest bound mx), 8/4/2/1 groups of 32 rows and group- or plane-major plane blocks (D),
+    ragged last tile, all-zero rows, rows at the bound, a small cap and the uint8 signature width."""
     rng = np.random.default_rng(1000 * mx + D)
     x = rng.integers(0, mx + 1, size=(n, D)).astype(np.uint8)
     x[rng.random((n, D)) < 0.7] = 0
@@ -197,7 +197,7 @@ def test_tiled_bitplanes(wmh, D, n, mx, tile):
         assert dead * k <= int(nsat.item()) <= int((s == cap).sum())
 
 
-@pytest.mark.parametrize("tile", ["bitplanes", "auto"])
+@pytest.mark.parametrize("tile", ["bitplanes", "bitslice", "auto"])
 def test_tiled_bitplanes_clamped(wmh, tile, capfd, monkeypatch):
     """Long rows whose largest bound needs one plane more than two groups can
     hold (D = 4096, bounds <= 63 except two columns at 100): the planes store
@@ -220,7 +220,34 @@ def test_tiled_bitplanes_clamped(wmh, tile, capfd, monkeypatch):
         sig, L, _ = _run(wmh, data, cfg, k, cap, 2, "tiled", seed=31, tile=tile)
         _assert_sig_equal(sig, oracle_hash(L, data, 31, k, cap), f"clamped {tile} k={k}")
     err = capfd.readouterr().err
-    assert "planes=6" in err and "NB=7" in err, err[-300:]
+    if tile == "bitplanes":
+        assert "planes=6" in err and "NB=7" in err, err[-300:]
+    else:
+        assert "[wmh bitslice] P=6 clamp=1 G=2" in err, err[-300:]
+
+
+def test_bitslice_clamped_group_major(wmh, capfd, monkeypatch):
+    """The bit-sliced tile with 4 clamped planes in group-major blocks (D = 2912,
+    bounds up to 31: five planes would leave two groups, four give four): the
+    draws in cells >= 15 of a column are tested on the candidate rows' bytes
+    whenever the group's column maximum says one of them can be green."""
+    monkeypatch.setenv("WMH_TILED_STATS", "1")
+    rng = np.random.default_rng(78)
+    n, D = 300, 2912
+    x = rng.integers(0, 16, size=(n, D)).astype(np.uint8)
+    x[rng.random((n, D)) < 0.6] = 0
+    hi = rng.random((n, D)) < 0.01
+    x[hi] = rng.integers(16, 32, size=int(hi.sum())).astype(np.uint8)
+    x[0, 0] = 31
+    x[20] = 0
+    x[20, 5] = 31                                # green only in cells 0..30 of column 5
+    data = datagen.Dense(x)
+    cfg = datagen.Config("bvc", n, D, 1, 255, 1)
+    for k, cap in [(96, 65535), (24, 50)]:
+        sig, L, _ = _run(wmh, data, cfg, k, cap, 2, "tiled", seed=5, tile="bitslice")
+        _assert_sig_equal(sig, oracle_hash(L, data, 5, k, cap), f"bitslice clamped P=4 k={k}")
+    err = capfd.readouterr().err
+    assert "[wmh bitslice] P=4 clamp=1 G=4" in err, err[-300:]
 
 
 @pytest.mark.parametrize("algo", ALGOS)

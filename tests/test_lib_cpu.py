@@ -19,7 +19,7 @@ def lib():
 def _header_functions():
     src = open(os.path.join(ROOT, "include", "wmh.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(wmh_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(wmh_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(lib):
