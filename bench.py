@@ -55,6 +55,9 @@ def parse():
     p.add_argument("--chunk", type=int, default=0, help="tiled: draws per re-queue (0 = auto)")
     p.add_argument("--horizon", type=int, default=0, help="index: draws filed per hash (0 = auto)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--graph", action="store_true",
+                   help="replay the step as a captured CUDA graph (launch-bound c1), and report the library's "
+                        "empty-launch floor measured the same way")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
@@ -368,7 +371,37 @@ def main():
 
     def step(timed=False):
         wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo=args.algo, out=sig, chunk=args.chunk,
-                 horizon=args.horizon, time_kernel=timed, tile=args.tile)
+                 horizon=args.horizon, time_kernel=timed and not args.graph, tile=args.tile)
+
+    graph = None
+    floor = None
+    if args.graph:                      # capture the step (kernels only: no allocation, no sync on this path)
+        step()
+        torch.cuda.synchronize()
+        l0 = wmh.kernel_launches()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph_launches = wmh.kernel_launches() - l0
+        eg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(eg):
+            wmh.empty_launch()
+        torch.cuda.synchronize()
+        fl = []
+        for _ in range(max(3, args.warmup)):
+            eg.replay()
+        for _ in range(max(5, args.steps)):
+            fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.zero_()
+            fa.record(stream)
+            eg.replay()
+            fb.record(stream)
+            torch.cuda.synchronize()
+            fl.append(fa.elapsed_time(fb))
+        floor = {"empty_launch_graph_ms": statistics.median(fl), "kernels_per_step": graph_launches}
+
+        def step(timed=False):         # noqa: F811  (the graph replaces the eager call)
+            graph.replay()
 
     clocks = ClockSampler(dev.index if world == 1 else local)
     clocks.start()
@@ -387,9 +420,10 @@ def main():
         a.record(stream)
         l0 = wmh.kernel_launches()
         step(timed=True)                     # + CUDA events around the dominant kernel, on its stream
-        launches += wmh.kernel_launches() - l0
+        launches += (wmh.kernel_launches() - l0) if graph is None else floor["kernels_per_step"]
         b.record(stream)
-        kern_ms.append(wmh.last_kernel_ms())  # waits for the kernel (after b is queued)
+        if graph is None:
+            kern_ms.append(wmh.last_kernel_ms())  # waits for the kernel (after b is queued)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -416,6 +450,8 @@ def main():
     if world > 1:
         dist.all_reduce(dt_)
     draws_total = float(dt_.item())
+    if not kern_ms:                                       # graph replay: the step is the kernel
+        kern_ms = step_ms
     kern_s = statistics.mean(kern_ms) / 1e3               # the dominant kernel's average launch (events)
     peaks = {}
     try:
@@ -426,6 +462,9 @@ def main():
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     algo_used = wmh.last_algo or args.algo
     roof = roofline(algo_used, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
+    if algo_used == "tiled" and wmh.last_tile == "bitslice":
+        roof = roofline_bitslice(x_sum, M, cfg, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(),
+                                 peaks, draws)
     if algo_used == "index":
         if xd is not None:
             nnz = sum(int((xd[a0:a0 + 65536].to(torch.int32) != 0).sum().item()) for a0 in range(0, n, 65536))
@@ -501,6 +540,7 @@ def main():
             "e2e": e2e,
             "clocks": clocks.summary(),
             "quantization": quant,
+            "graph": floor,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
@@ -529,6 +569,73 @@ def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
                            f"/ {i_draw:.0f} lane-instr per draw-test ({algo})",
             "frac_vs_paper_loop": achieved / (issue / I_DRAW["simple"] / 1e9),
             "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3, "t_kernel_ms": kern_s * 1e3}
+
+
+def group_expected_max(x_sum: np.ndarray, M: int, cap: int, sample: int = 4096, seed: int = 3) -> tuple[float, int]:
+    """E[max over the live rows r of a 32-row group of min(G_r, cap)], G_r ~ Geom(s_r)
+    (Theorem 2), summed over the groups of consecutive 32 rows the
+    bit-sliced tile tests together: sum_t P(max > t) = sum_t 1 - prod_r (1 - (1 - s_r)^t).
+    Exact per group; computed on a seeded sample of groups and scaled when there
+    are more than `sample` groups.  Returns (sum over groups, groups sampled)."""
+    s = x_sum.astype(np.float64) / M
+    n_groups = (len(s) + 31) // 32
+    pad = np.zeros(n_groups * 32)
+    pad[:len(s)] = s
+    g = pad.reshape(n_groups, 32)
+    idx = np.arange(n_groups)
+    if n_groups > sample:
+        idx = np.sort(np.random.default_rng(seed).choice(n_groups, size=sample, replace=False))
+    g = g[idx]
+    live = g > 0
+    lq = np.where(live, np.log1p(-np.minimum(g, 1 - 1e-15)), 0.0)          # log(1 - s_r)
+    total = np.zeros(len(g))
+    done = ~live.any(axis=1)
+    t = 0
+    step = 64
+    while t < cap and not done.all():
+        ts = np.arange(t, min(cap, t + step), dtype=np.float64)
+        # P(max > t) = 1 - prod_r (1 - q_r^t) over live rows (dead rows contribute 1)
+        qt = np.exp(lq[:, :, None] * ts[None, None, :])                   # [G, 32, T]
+        with np.errstate(divide="ignore"):                                # t = 0: log(1 - 1) = -inf, P = 1
+            logp = np.where(live[:, :, None], np.log1p(-qt), 0.0).sum(axis=1)
+        tail = -np.expm1(logp)                                            # P(max > t)
+        tail[done] = 0.0
+        total += tail.sum(axis=1)
+        done |= tail[:, -1] < 1e-12
+        t += step
+    return float(total.sum() * n_groups / len(g)), len(g)
+
+
+def roofline_bitslice(x_sum, M, cfg, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks, draws):
+    """The bit-sliced tile (hash_bitslice.cu): integer-issue bound.  Algorithmic
+    work = the group-draws bit-slicing must test -- for every 32-row group and
+    hash, the draws up to its last row's first green, E[max_r min(G_r, cap)]
+    (Theorem 2 per row) -- times the lane-instructions one group-draw costs in
+    the kernel's own round loop (test + first-green combine), counted statically
+    from SASS (profiles/r2_sass_bitslice.json, scripts/sass_budget.py).  Waste
+    the bound does not pay for: rounds of 64 draws past the max, staging the
+    tile, flushing signatures, issue stalls."""
+    sass = json.load(open(os.path.join(ROOT, "profiles", "r2_sass_bitslice.json")))
+    reg = sass["by_region"]
+    n_test = next(v for k_, v in reg.items() if k_.startswith("test"))
+    n_comb = next(v for k_, v in reg.items() if k_.startswith("combine"))
+    G = sass.get("groups", 2)
+    lane_per_gd = 32.0 * (n_test + n_comb) / (64.0 * G)            # lane-instructions per group-draw
+    emax, sampled = group_expected_max(x_sum, M, cfg.cap)
+    group_draws = cfg.k * emax
+    issue = n_sm * 4 * 32 * sm_mhz * 1e6                            # lane-instructions / s
+    t_floor = group_draws * lane_per_gd / issue
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    return {"bound": "alu", "achieved": group_draws / kern_s / 1e9, "peak": issue / lane_per_gd / 1e9,
+            "unit": "Ggroup-draws/s", "frac": t_floor / kern_s, "traffic": None, "kernel": "tiled/bitslice",
+            "peak_source": f"{n_sm} SMs x 128 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) / "
+                           f"{lane_per_gd:.1f} lane-instr per group-draw (32 x ({n_test} test + {n_comb} combine) "
+                           f"SASS instructions per 64-draw round of {G} groups, profiles/r2_sass_bitslice.json)",
+            "group_draws_required": group_draws, "groups_sampled": sampled,
+            "t_floor_ms": t_floor * 1e3, "t_kernel_ms": kern_s * 1e3,
+            "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3,
+            "frac_vs_theorem2_rowtests": draws * (32.0 * n_test / (64.0 * G)) / 32.0 / issue / kern_s,
+            "frac_vs_paper_loop": draws / kern_s / 1e9 / (issue / I_DRAW["simple"] / 1e9)}
 
 
 def index_epochs(T: int):

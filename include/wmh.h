@@ -224,6 +224,14 @@ typedef struct {
                             the round-1 bit-plane tile or the lane-per-draw
                             bit-sliced tile (default: the bit-sliced tile when
                             its planes fit).  Performance only. */
+    void *plan_out;      /* optional device uint8[n_rows] (may be NULL): when the INDEX
+                            kernel runs, its per-row plan code -- bits 0-3 the epoch
+                            (horizon) the row picked, bit 4 columns staged in shared
+                            memory, bit 5 Alg. 3's fallback loop ran, bit 6 more
+                            nonzeros than one range batch, bit 7 all-zero row.  For
+                            tests that must cover every plan; results do not depend on it */
+    int32_t tile_used;   /* OUTPUT: with algo_used == WMH_ALGO_TILED on dense rows, the tile
+                            that ran: 1 byte tile, 2 bit-plane tile, 3 bit-sliced tile */
     int32_t reserved[3]; /* must be zero */
 } wmh_hash_opts;
 
@@ -316,6 +324,10 @@ void wmh_lsh_free(wmh_lsh *index);
 
 /* Thread-local description of the last failure ("" if none). */
 const char *wmh_last_error(void);
+
+/* One empty kernel launched on `stream`: the launch floor against which the
+ * launch-bound configuration c1 is reported (bench.py --graph).  Errors: ECUDA. */
+wmh_status wmh_empty_launch(void *stream);
 
 /* Library version string, e.g. "wmh 0.1 sm_100a". */
 const char *wmh_version(void);

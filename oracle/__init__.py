@@ -28,11 +28,21 @@ _lib = None
 OK, EINVAL, EEMPTY, EOVERFLOW, EBOUND, ENOMEM = 0, -1, -2, -3, -4, -5
 
 
+# WMH_ORACLE_SANITIZE=1: load an AddressSanitizer + UndefinedBehaviorSanitizer
+# build instead (run python with LD_PRELOAD=$(gcc -print-file-name=libasan.so)
+# and ASAN_OPTIONS=detect_leaks=0; scripts/sanitize_oracle.sh)
+_SAN = os.environ.get("WMH_ORACLE_SANITIZE") == "1"
+if _SAN:
+    _SO = os.path.join(_HERE, "libwmh_oracle_san.so")
+
+
 def build(force: bool = False) -> str:
     """Compile wmh_oracle.c into libwmh_oracle.so (plain gcc -O2, no fast-math)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-pthread",
+        flags = ["-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=undefined",
+                 "-fno-omit-frame-pointer"] if _SAN else ["-O2"]
+        subprocess.check_call(["gcc", *flags, "-std=gnu11", "-fPIC", "-shared", "-pthread",
                                "-o", tmp, _SRC])
         os.replace(tmp, _SO)
     return _SO

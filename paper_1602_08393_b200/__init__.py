@@ -229,17 +229,19 @@ def check_rows(layout: Layout, rows: Rows, stream=None) -> None:
 
 last_algo = None     # name of the kernel the last hash() call ran ('simple' / 'tiled' / 'index')
 last_horizon = None  # the index horizon T of the last hash() call that ran the index kernel
+last_tile = None     # the dense tile of the last hash() call that ran TILED ('bytes' / 'bitplanes' / 'bitslice')
 
 
 def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
          algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
          chunk: int = 0, horizon: int = 0, time_kernel: bool = False, stream=None,
-         tile: str = "auto", validate: bool = False) -> torch.Tensor:
+         tile: str = "auto", validate: bool = False, plan_out: torch.Tensor | None = None) -> torch.Tensor:
     """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16).
     `tile` ("auto", "bytes", "bitplanes", "bitslice") picks the TILED kernel's dense tile
     (performance only).  `validate` checks every row against the layout's bounds
     first (wmh_check_rows: WmhError EBOUND instead of silently wrong signatures
-    for rows prepare() did not see)."""
+    for rows prepare() did not see).  `plan_out` (uint8 [n_rows], tests): the INDEX
+    kernel's per-row plan codes (include/wmh.h, wmh_hash_opts.plan_out)."""
     if sig_bytes is None:
         sig_bytes = 1 if cap <= 255 else 2
     dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
@@ -256,12 +258,15 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
     flags = (_lib.WMH_OPT_TIME_KERNEL if time_kernel else 0) | (_lib.WMH_OPT_VALIDATE if validate else 0) | \
         {"auto": 0, "bytes": _lib.WMH_OPT_TILE_BYTES, "bitplanes": _lib.WMH_OPT_TILE_BITPLANES,
          "bitslice": _lib.WMH_OPT_TILE_BITSLICE}[tile]
-    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon, flags)
+    if plan_out is not None and (plan_out.dtype != torch.uint8 or plan_out.numel() < rows.n_rows or not plan_out.is_cuda):
+        raise ValueError("plan_out must be a CUDA uint8 tensor of >= n_rows elements")
+    opts = _lib.WmhHashOpts(_lib.ALGOS[algo], chunk, 0, horizon, flags, None if plan_out is None else plan_out.data_ptr())
     _lib.check(_lib.load().wmh_hash_ex(layout.handle, ctypes.byref(rows._c()), seed & (2**64 - 1), k, cap, sig_bytes,
                                        _ptr(out), _ptr(n_saturated), ctypes.byref(opts), _stream(stream)))
-    global last_algo, last_horizon
+    global last_algo, last_horizon, last_tile
     last_algo = {v: n for n, v in _lib.ALGOS.items()}.get(opts.algo_used, "?")
     last_horizon = int(opts.horizon) if last_algo == "index" else None
+    last_tile = {1: "bytes", 2: "bitplanes", 3: "bitslice"}.get(int(opts.tile_used))
     return out
 
 
@@ -474,6 +479,11 @@ def last_kernel_ms() -> float:
     ms = ctypes.c_float()
     _lib.check(_lib.load().wmh_last_kernel_ms(ctypes.byref(ms)))
     return float(ms.value)
+
+
+def empty_launch(stream=None) -> None:
+    """One empty kernel of the library on the stream (the launch floor)."""
+    _lib.check(_lib.load().wmh_empty_launch(_stream(stream)))
 
 
 def kernel_launches() -> int:

@@ -24,7 +24,7 @@ EXPORTS = ["wmh_colmax", "wmh_prepare", "wmh_layout_info", "wmh_layout_digest", 
            "wmh_hash", "wmh_hash_ex", "wmh_hash_host", "wmh_collide", "wmh_last_error", "wmh_version",
            "wmh_kernel_launches", "wmh_last_kernel_ms", "wmh_quantize", "wmh_scale_objective", "wmh_lsh_build",
            "wmh_lsh_query", "wmh_lsh_free", "wmh_hasher_create", "wmh_hasher_run", "wmh_hasher_free",
-           "wmh_check_rows", "wmh_collide2", "wmh_choose_scale"]
+           "wmh_check_rows", "wmh_collide2", "wmh_choose_scale", "wmh_empty_launch"]
 
 
 class WmhRows(ctypes.Structure):
@@ -35,7 +35,8 @@ class WmhRows(ctypes.Structure):
 
 class WmhHashOpts(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("chunk", ctypes.c_int32), ("algo_used", ctypes.c_int32),
-                ("horizon", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32 * 3)]
+                ("horizon", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("plan_out", ctypes.c_void_p),
+                ("tile_used", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class WmhError(RuntimeError):
@@ -75,6 +76,7 @@ def load() -> ctypes.CDLL:
             "wmh_collide": (st, [vp, i32, u32, i64, vp, i64, vp, vp, i32, vp]),
             "wmh_collide2": (st, [vp, i64, vp, i64, i32, u32, vp, i64, vp, vp, i32, vp]),
             "wmh_check_rows": (st, [vp, rows_p, vp]),
+            "wmh_empty_launch": (st, [vp]),
             "wmh_choose_scale": (st, [rows_p, ctypes.POINTER(ctypes.c_float), i32, ctypes.POINTER(i32), vp]),
             "wmh_last_error": (ctypes.c_char_p, []),
             "wmh_version": (ctypes.c_char_p, []),

@@ -184,7 +184,8 @@ static bool tiny_batch(const wmh_layout *L, const wmh_rows *rows, uint32_t k, ui
 
 static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
                                 int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, int algo, int chunk,
-                                uint32_t horizon, cudaStream_t s, int *algo_used, int tile = 0) {
+                                uint32_t horizon, cudaStream_t s, int *algo_used, int tile = 0, void *plan_out = nullptr,
+                                int *tile_used = nullptr) {
     *algo_used = algo == WMH_ALGO_AUTO ? WMH_ALGO_SIMPLE : algo;
     if (rows->n_rows == 0) return WMH_OK;
     HashArgs a;
@@ -200,6 +201,8 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     a.chunk = chunk;
     a.horizon = horizon;
     a.tile = tile;
+    a.plan_out = plan_out;
+    a.tile_used = tile_used;
     if (algo == WMH_ALGO_INDEX) {
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
@@ -249,6 +252,7 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
              : (opts->flags & WMH_OPT_TILE_BITSLICE) ? 3 : 0;
         for (int i = 0; i < 3; i++)
             if (opts->reserved[i]) { set_error("wmh_hash_ex: reserved option fields must be zero"); return WMH_EINVAL; }
+        opts->tile_used = 0;
         chunk = opts->chunk;
         horizon = opts->horizon;
         if (chunk != 0 && chunk != 4 && chunk != 8 && chunk != 16 && chunk != 32) { set_error("wmh_hash_ex: chunk=%d not in {0,4,8,16,32}", chunk); return WMH_EINVAL; }
@@ -262,7 +266,7 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
     g_ktimer.on = opts && (opts->flags & WMH_OPT_TIME_KERNEL);
     if (g_ktimer.on) g_ktimer.recorded = false;
     st = hash_dispatch(L, rows, seed, k, cap, sig_bytes, sig_out, n_saturated, algo, chunk, horizon, (cudaStream_t)stream,
-                       &used, tile);
+                       &used, tile, opts ? opts->plan_out : nullptr, opts ? &opts->tile_used : nullptr);
     g_ktimer.on = false;
     if (opts) {
         opts->algo_used = used;
@@ -607,6 +611,18 @@ extern "C" wmh_status wmh_collide2(const void *sig_a, int64_t n_a, const void *s
                                    int32_t check_pairs, void *stream) {
     return collide_impl("wmh_collide2", sig_a, n_a, sig_b, n_b, sig_bytes, k, pairs, n_pairs, matches, jhat, check_pairs,
                         stream);
+}
+
+namespace wmh {
+__global__ void empty_kernel() {}
+}  // namespace wmh
+
+// The launch floor: one empty kernel on `stream` (what a launch- or graph-node-
+// bound configuration such as c1 is measured against).
+extern "C" wmh_status wmh_empty_launch(void *stream) {
+    wmh::empty_kernel<<<1, 32, 0, (cudaStream_t)stream>>>();
+    WMH_LAUNCH_CHECK("empty launch");
+    return WMH_OK;
 }
 
 extern "C" const char *wmh_last_error(void) { return g_err; }

@@ -126,6 +126,8 @@ struct HashArgs {
     int chunk;           // TILED: 0 = auto, else 4/8/16/32
     uint32_t horizon;    // INDEX: draws filed per hash (0 = auto)
     int tile = 0;        // TILED dense: 0 auto, 1 byte tile, 2 bit-plane tile, 3 bit-sliced tile
+    void *plan_out = nullptr;    // INDEX: optional per-row plan codes (wmh_hash_opts.plan_out)
+    int *tile_used = nullptr;    // TILED dense: written with the tile that ran (1/2/3)
 };
 
 wmh_status launch_hash_simple(const HashArgs &a);

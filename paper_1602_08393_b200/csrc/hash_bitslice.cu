@@ -43,6 +43,7 @@
 namespace wmh {
 
 constexpr int BV_HB = 8;                  // hashes per claimed block (results flushed 8 per row)
+constexpr int BV_SB = 2;                  // staging units per thread whose loads are in flight together
 
 struct BvParams {
     const uint8_t *x;
@@ -58,7 +59,6 @@ struct BvParams {
     void *sig;
     unsigned long long *n_sat;
     unsigned long long *item_ctr;
-    int or_bound;                // 1: gmax holds the OR of the group's bytes (an upper bound on the max)
 };
 
 // the draw word of cell r: (c << 8) | (r - CompToM[c]); t >= cap -> 0xFF, which
@@ -131,6 +131,15 @@ __device__ __forceinline__ void bv_t8(uint32_t &lo, uint32_t &hi) {
     t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
 }
 
+// Delta swap of bit blocks between two row words (one stage of an 8x8 bit
+// transpose per byte): bits j of a with j & S != 0 <-> bits j - S of b.
+template <int S>
+__device__ __forceinline__ void bv_swap(uint32_t &a, uint32_t &b, uint32_t m) {
+    const uint32_t x = a >> S, y = b << S;
+    b = (b & ~m) | (x & m);
+    a = (a & ~(m << S)) | (y & (m << S));
+}
+
 // Column block of the planes: W = G*P words.  P % 4 == 0: group-major [g][b]
 // (each group's planes one or two 16-byte loads, loaded only when the group
 // needs them); else plane-major [b][g] (the whole block in 16/8/4-byte loads).
@@ -141,35 +150,42 @@ struct BvLayout {
     static __device__ __forceinline__ int idx(int g, int b) { return GROUP_MAJOR ? g * P + b : b * G + g; }
 };
 
-template <int P, int G>
-__device__ __forceinline__ void bv_load_group(const uint32_t *blk, int g, uint32_t (&x)[P]) {
-    const uint4 *q = reinterpret_cast<const uint4 *>(blk + g * P);
-#pragma unroll
-    for (int i = 0; i < P / 4; i++) {
-        const uint4 v = q[i];
-        x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
-    }
+// Predicated shared-memory loads at 32-bit shared addresses: when `p` is false
+// the registers keep whatever they held (the caller masks those lanes' results).
+__device__ __forceinline__ void bv_lds4(uint32_t addr, bool p, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+                 : "+r"(a), "+r"(b), "+r"(c), "+r"(d) : "r"(addr), "r"((int)p));
+}
+__device__ __forceinline__ void bv_lds2(uint32_t addr, bool p, uint32_t &a, uint32_t &b) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.shared.v2.u32 {%0, %1}, [%2];\n\t}"
+                 : "+r"(a), "+r"(b) : "r"(addr), "r"((int)p));
+}
+__device__ __forceinline__ void bv_lds1(uint32_t addr, bool p, uint32_t &a) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
+                 : "+r"(a) : "r"(addr), "r"((int)p));
 }
 
+// group g's P plane words of the column block at shared address blk (group-major)
 template <int P, int G>
-__device__ __forceinline__ void bv_load_all(const uint32_t *blk, uint32_t (&x)[G][P]) {
+__device__ __forceinline__ void bv_load_group(uint32_t blk, int g, bool p, uint32_t (&x)[P]) {
+#pragma unroll
+    for (int i = 0; i < P / 4; i++) bv_lds4(blk + 16u * (uint32_t)(g * P / 4 + i), p, x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+}
+
+// the whole column block (W = G*P words) in 16/8/4-byte loads
+template <int P, int G>
+__device__ __forceinline__ void bv_load_all(uint32_t blk, bool p, uint32_t (&x)[G][P]) {
     constexpr int W = G * P;
     uint32_t v[W];
     if constexpr (W % 4 == 0) {
 #pragma unroll
-        for (int i = 0; i < W / 4; i++) {
-            const uint4 a = reinterpret_cast<const uint4 *>(blk)[i];
-            v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
-        }
+        for (int i = 0; i < W / 4; i++) bv_lds4(blk + 16u * i, p, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     } else if constexpr (W % 2 == 0) {
 #pragma unroll
-        for (int i = 0; i < W / 2; i++) {
-            const uint2 a = reinterpret_cast<const uint2 *>(blk)[i];
-            v[2 * i] = a.x; v[2 * i + 1] = a.y;
-        }
+        for (int i = 0; i < W / 2; i++) bv_lds2(blk + 8u * i, p, v[2 * i], v[2 * i + 1]);
     } else {
 #pragma unroll
-        for (int i = 0; i < W; i++) v[i] = blk[i];
+        for (int i = 0; i < W; i++) bv_lds1(blk + 4u * i, p, v[i]);
     }
 #pragma unroll
     for (int g = 0; g < G; g++)
@@ -206,13 +222,13 @@ __device__ __noinline__ uint32_t bv_slow(const uint8_t *x, int64_t grow0, int D,
 // the L_b masks are built once per draw; a group whose column maximum is at or
 // below the offset is red without touching its planes (R2).
 template <int P, int G, bool CLAMP>
-__device__ __forceinline__ void bv_test(const BvParams &p, const uint32_t *planes, const bv_gmax_t<G> *gmax, int64_t row0,
+__device__ __forceinline__ void bv_test(const BvParams &p, uint32_t planes_s, const bv_gmax_t<G> *gmax, int64_t row0,
                                         uint32_t w, const uint32_t (&pend)[G], uint32_t (&mask)[G]) {
     constexpr int W = G * P;
     constexpr uint32_t TOP = (1u << P) - 1u;
     const uint32_t c = w >> 8, off = w & 0xFFu;
     const uint32_t gm = (uint32_t)gmax[c];
-    const uint32_t *blk = planes + (size_t)c * W;
+    const uint32_t blk = planes_s + c * (uint32_t)(W * 4);
     const uint32_t L = CLAMP ? (off < TOP ? TOP - off : 0u) : TOP - off;
     const uint32_t Xh = L * 0x08040201u, Xl = L * 0x80402010u;
     uint32_t m[P];
@@ -228,11 +244,11 @@ __device__ __forceinline__ void bv_test(const BvParams &p, const uint32_t *plane
     if constexpr (BvLayout<P, G>::GROUP_MAJOR) {
 #pragma unroll
         for (int g = 0; g < G; g++) {
+            mask[g] = 0u;
+            if (pend[g] == 0u) continue;                 // warp-uniform
             uint32_t xg[P];
-#pragma unroll
-            for (int b = 0; b < P; b++) xg[b] = 0u;
-            if (need[g]) bv_load_group<P, G>(blk, g, xg);
-            mask[g] = bv_chain<P>(xg, m);
+            bv_load_group<P, G>(blk, g, need[g], xg);
+            mask[g] = need[g] ? bv_chain<P>(xg, m) : 0u;
             if (CLAMP && need[g] && off >= TOP) {
                 uint32_t cand = xg[0];
 #pragma unroll
@@ -242,13 +258,11 @@ __device__ __forceinline__ void bv_test(const BvParams &p, const uint32_t *plane
         }
     } else {
         uint32_t xa[G][P];
-#pragma unroll
-        for (int g = 0; g < G; g++)
-#pragma unroll
-            for (int b = 0; b < P; b++) xa[g][b] = 0u;
-        if (need_any) bv_load_all<P, G>(blk, xa);
+        bv_load_all<P, G>(blk, need_any, xa);
 #pragma unroll
         for (int g = 0; g < G; g++) {
+            mask[g] = 0u;
+            if (pend[g] == 0u) continue;                 // warp-uniform: a finished group costs nothing
             mask[g] = need[g] ? bv_chain<P>(xa[g], m) : 0u;
             if (CLAMP && need[g] && off >= TOP) {
                 uint32_t cand = xa[g][0];
@@ -273,7 +287,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
         reinterpret_cast<uint8_t *>(gmax) + (((size_t)p.D * sizeof(gm_t) + 15) & ~(size_t)15));   // [NW][HB][R]
     uint8_t *gbytes = reinterpret_cast<uint8_t *>(gmax);
     uint8_t *pbytes = reinterpret_cast<uint8_t *>(planes);
-    __shared__ long long s_item, s_next;
+    __shared__ long long s_next;
     __shared__ int s_hash;
     __shared__ uint32_t s_live[G];
 
@@ -282,26 +296,18 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
     unsigned long long sat = 0;
     const int quads = p.D >> 2;                        // D % 4 == 0 (launcher)
     const BvTranspose tr(lane);
-    if (threadIdx.x == 0) s_next = (long long)atomicAdd(p.item_ctr, 1ull);
+    const uint32_t planes_s = (uint32_t)__cvta_generic_to_shared(planes);
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(p.item_ctr, 1ull);     // the first item
 
     for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            s_item = s_next;
-            s_next = (long long)atomicAdd(p.item_ctr, 1ull);
-            s_hash = 0;
-        }
+        // items are claimed one ahead, during the previous item's hashes (warp 0),
+        // so no thread waits here on a global atomic
+        __syncthreads();                               // previous hashes done: planes free, s_next visible
+        const long long item = s_next;
+        if (threadIdx.x == 0) s_hash = 0;
         if (threadIdx.x < G) s_live[threadIdx.x] = 0;
-        __syncthreads();
-        const long long item = s_item;
+        __syncthreads();                               // everyone has read s_next before warp 0 replaces it
         if (item >= p.n_items) break;
-        if (s_next < p.n_items) {                      // warm L2 with the next item's rows
-            const int64_t nrow0 = (s_next / p.n_hchunks) * R;
-            const int64_t nbytes = min((int64_t)R, p.n_rows - nrow0) * (int64_t)p.D;
-            const char *base = reinterpret_cast<const char *>(p.x + nrow0 * (int64_t)p.D);
-            for (int64_t off = (int64_t)threadIdx.x * 128; off < nbytes; off += (int64_t)NT * 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
-        }
         const int64_t tile = item / p.n_hchunks;
         const int hc = (int)(item % p.n_hchunks);
         const int64_t row0 = tile * R;
@@ -311,56 +317,112 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
         // ---- a5: stage the tile as bit planes + per-(column, group) maxima.
         //      Unit = (column quad, group, octet of 8 rows), octet fastest: 8
         //      words in, 4 columns x P plane bytes out; the 4 octet lanes of a
-        //      (quad, group) combine their column maxima with two shuffles
-        for (int u = threadIdx.x; u < quads * G * 4; u += NT) {
-            const int o = u & 3, g = (u >> 2) % G, cq = (u >> 2) / G;
-            const int rb = 32 * g + 8 * o;
-            uint32_t w[8];
-            uint32_t live = 0, mx = 0;
+        //      (quad, group) combine their column maxima with two shuffles.
+        //      BV_SB units per batch: all their loads are issued before any is
+        //      used (one memory round trip per batch, not per unit)
+        const int n_units = quads * G * 4;
+        auto stage_load = [&](int u0, uint32_t (&wb)[BV_SB][8]) {
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const bool ok = rb + i < nr;
-                w[i] = ok ? __ldg(reinterpret_cast<const uint32_t *>(p.x + (row0 + rb + i) * (int64_t)p.D) + cq) : 0u;
-                live |= (w[i] != 0u) << i;
-                mx = p.or_bound ? (mx | w[i]) : __vmaxu4(mx, w[i]);
-                if (CLAMP) w[i] = __vminu4(w[i], TOP * 0x01010101u);
-            }
-            const unsigned am = __activemask();
-            if (p.or_bound) {
-                mx |= __shfl_xor_sync(am, mx, 1);
-                mx |= __shfl_xor_sync(am, mx, 2);
-            } else {
-                mx = __vmaxu4(mx, __shfl_xor_sync(am, mx, 1));
-                mx = __vmaxu4(mx, __shfl_xor_sync(am, mx, 2));
-            }
-            if (o == 0) {
+            for (int bi = 0; bi < BV_SB; bi++) {
+                const int u = u0 + bi * NT;
+                const int o = u & 3, g = (u >> 2) % G, cq = (u >> 2) / G;
+                const int rb = 32 * g + 8 * o;
+                const uint8_t *xr = p.x + (row0 + rb) * (int64_t)p.D + 4 * cq;
 #pragma unroll
-                for (int u4 = 0; u4 < 4; u4++) gbytes[(size_t)(4 * cq + u4) * sizeof(gm_t) + g] = (uint8_t)(mx >> (8 * u4));
+                for (int i = 0; i < 8; i++) {
+                    const bool ok = u < n_units && rb + i < nr;
+                    wb[bi][i] = ok ? __ldg(reinterpret_cast<const uint32_t *>(xr + (int64_t)i * p.D)) : 0u;
+                }
             }
-            if (live) atomicOr(&s_live[g], live << (8 * o));
-            // 4x4 byte transposes: col[u4] = byte u4 of rows 0..3 (lo) and 4..7 (hi)
-            uint32_t lo[4], hi[4];
-            {
-                const uint32_t t0 = bv_prmt(w[0], w[1], 0x5140), t1 = bv_prmt(w[0], w[1], 0x7362);
-                const uint32_t t2 = bv_prmt(w[2], w[3], 0x5140), t3 = bv_prmt(w[2], w[3], 0x7362);
-                lo[0] = bv_prmt(t0, t2, 0x5410); lo[1] = bv_prmt(t0, t2, 0x7632);
-                lo[2] = bv_prmt(t1, t3, 0x5410); lo[3] = bv_prmt(t1, t3, 0x7632);
-                const uint32_t s0 = bv_prmt(w[4], w[5], 0x5140), s1 = bv_prmt(w[4], w[5], 0x7362);
-                const uint32_t s2 = bv_prmt(w[6], w[7], 0x5140), s3 = bv_prmt(w[6], w[7], 0x7362);
-                hi[0] = bv_prmt(s0, s2, 0x5410); hi[1] = bv_prmt(s0, s2, 0x7632);
-                hi[2] = bv_prmt(s1, s3, 0x5410); hi[3] = bv_prmt(s1, s3, 0x7632);
+        };
+        auto stage_proc = [&](int u0, uint32_t (&wb)[BV_SB][8]) {
+#pragma unroll
+            for (int bi = 0; bi < BV_SB; bi++) {
+                const int u = u0 + bi * NT;
+                if (u >= n_units) break;                 // uniform over the 4 octet lanes of a unit
+                const int o = u & 3, g = (u >> 2) % G, cq = (u >> 2) / G;
+                uint32_t *w = wb[bi];
+                if (CLAMP) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) w[i] = __vminu4(w[i], TOP * 0x01010101u);
+                }
+                // 8x8 bit transposes of the 4 byte columns at once: delta swaps
+                // across the 8 row words; afterwards w[b] = plane b (byte u4 =
+                // column u4, bit i = row 8o + i)
+                bv_swap<1>(w[0], w[1], 0x55555555u); bv_swap<1>(w[2], w[3], 0x55555555u);
+                bv_swap<1>(w[4], w[5], 0x55555555u); bv_swap<1>(w[6], w[7], 0x55555555u);
+                bv_swap<2>(w[0], w[2], 0x33333333u); bv_swap<2>(w[1], w[3], 0x33333333u);
+                bv_swap<2>(w[4], w[6], 0x33333333u); bv_swap<2>(w[5], w[7], 0x33333333u);
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    if (i < P) bv_swap<4>(w[i], w[i + 4], 0x0F0F0F0Fu);
+                // 4x4 byte transpose across the 4 octet lanes: lane o then holds the
+                // full 32-row plane words of column 4cq + o
+                const unsigned am = __activemask();
+                const uint32_t s1 = (o & 1) ? 0x3715u : 0x6240u, s2 = (o & 2) ? 0x3276u : 0x5410u;
+                uint32_t pw[P];
+#pragma unroll
+                for (int b = 0; b < P; b++) {
+                    uint32_t x = w[b];
+                    x = bv_prmt(x, __shfl_xor_sync(am, x, 1), s1);
+                    pw[b] = bv_prmt(x, __shfl_xor_sync(am, x, 2), s2);
+                }
+                const int c = 4 * cq + o;
+                uint32_t *dst = planes + (size_t)c * W;
+#pragma unroll
+                for (int b = 0; b < P; b++) dst[BvLayout<P, G>::idx(g, b)] = pw[b];
+                // the column's maximum over the group: bit descent on the planes
+                uint32_t cand = 0u, mx = 0u;
+#pragma unroll
+                for (int b = 0; b < P; b++) cand |= pw[b];
+                const uint32_t live = cand;              // rows of the group nonzero in this column
+#pragma unroll
+                for (int b = P - 1; b >= 0; b--) {
+                    const uint32_t t = pw[b] & cand;
+                    if (t) { cand = t; mx |= 1u << b; }
+                }
+                // clamped planes saturate at TOP: then only "some row >= TOP" is known,
+                // so the flagged draws of this column keep testing (bv_slow is exact)
+                gbytes[(size_t)c * sizeof(gm_t) + g] = (uint8_t)((CLAMP && mx == TOP) ? 0xFFu : mx);
+                const int first = __ffs(am) - 1;
+#pragma unroll
+                for (int gg = 0; gg < G; gg++) {
+                    const uint32_t lv = __reduce_or_sync(am, g == gg ? live : 0u);
+                    if (lane == first && lv) atomicOr(&s_live[gg], lv);
+                }
             }
-#pragma unroll
-            for (int u4 = 0; u4 < 4; u4++) {
-                uint32_t a = lo[u4], b = hi[u4];
-                bv_t8(a, b);
-                uint8_t *dst = pbytes + (size_t)(4 * cq + u4) * W * 4 + o;
-#pragma unroll
-                for (int pb = 0; pb < P; pb++)
-                    dst[4 * BvLayout<P, G>::idx(g, pb)] = (uint8_t)((pb < 4 ? a : b) >> (8 * (pb & 3)));
+        };
+        // two batches of BV_SB units in flight: the next batch's loads are issued
+        // before the current one is transposed
+        {
+            uint32_t bufA[BV_SB][8], bufB[BV_SB][8];
+            int u0 = threadIdx.x;
+            stage_load(u0, bufA);
+            for (; u0 < n_units; u0 += 2 * BV_SB * NT) {
+                const int u1 = u0 + BV_SB * NT;
+                if (u1 < n_units) stage_load(u1, bufB);
+                stage_proc(u0, bufA);
+                if (u1 >= n_units) break;
+                if (u1 + BV_SB * NT < n_units) stage_load(u1 + BV_SB * NT, bufA);
+                stage_proc(u1, bufB);
             }
         }
         __syncthreads();
+
+        // ---- warp 0 claims the next item now and warms L2 with its rows
+        if (warp == 0) {
+            long long nx = 0;
+            if (lane == 0) nx = (long long)atomicAdd(p.item_ctr, 1ull);
+            nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
+            if (lane == 0) s_next = nx;
+            if (nx < p.n_items) {
+                const int64_t nrow0 = (nx / p.n_hchunks) * R;
+                const int64_t nbytes = min((int64_t)R, p.n_rows - nrow0) * (int64_t)p.D;
+                const char *base = reinterpret_cast<const char *>(p.x + nrow0 * (int64_t)p.D);
+                for (int64_t off = (int64_t)lane * 128; off < nbytes; off += 32 * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+            }
+        }
 
         // ---- hashes: a warp claims blocks of BV_HB consecutive hashes (the next
         //      block one block ahead) and flushes a block's results with one
@@ -425,36 +487,42 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
                     }
                     break;
                 }
-                const uint32_t w0 = wA, w1 = wB;
-                // prefetch the round after next (the table holds t < T0; later draws are computed)
+                uint32_t w0 = wA, w1 = wB;
+                if (tb >= (uint32_t)T0) {              // beyond the table (rare): draw them here
+                    const uint32_t t0 = tb + lane;
+                    w0 = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t0), p.M), p.pack, p.uni_m, t0, p.cap);
+                    w1 = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)(t0 + 32)), p.M), p.pack, p.uni_m, t0 + 32, p.cap);
+                }
+                // prefetch the round after next from the table (T0 draws per hash)
                 wA = xA;
                 wB = xB;
-                {
-                    const uint32_t t2 = tb + 128 + lane;
-                    if (tb + 128 < (uint32_t)T0) {
-                        xA = __ldg(tj + t2);
-                        xB = __ldg(tj + t2 + 32);
-                    } else if (tb + 128 < p.cap) {
-                        xA = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t2), p.M), p.pack, p.uni_m, t2, p.cap);
-                        xB = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)(t2 + 32)), p.M), p.pack, p.uni_m, t2 + 32, p.cap);
-                    }
+                if (tb + 128 < (uint32_t)T0) {
+                    xA = __ldg(tj + tb + 128 + lane);
+                    xB = __ldg(tj + tb + 160 + lane);
                 }
                 uint32_t mA[G], mB[G];
-                bv_test<P, G, CLAMP>(p, planes, gmax, row0, w0, pend, mA);
-                bv_test<P, G, CLAMP>(p, planes, gmax, row0, w1, pend, mB);
+                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w0, pend, mA);
+                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w1, pend, mB);
                 // ---- a8: the first green draw of each pending row.  Rows green among
                 //      the first 32 draws (RA) keep those; the others take the second
                 //      32; one transpose per group then gives lane = row its draws
+                uint32_t RA[G], Rall[G], u[G], anyR = 0u;
 #pragma unroll
-                for (int g = 0; g < G; g++) {
-                    const uint32_t a = mA[g] & pend[g];
-                    const uint32_t RA = __reduce_or_sync(0xFFFFFFFFu, a);
-                    const uint32_t u = a | (mB[g] & pend[g] & ~RA);
-                    const uint32_t Rall = __reduce_or_sync(0xFFFFFFFFu, u);
-                    if (Rall) {                                               // warp-uniform
-                        const uint32_t wt = tr(u);                            // bit i: draw (tb or tb+32) + i green for row lane
-                        if (wt) hres[32 * g + lane] = (uint16_t)(tb + (((RA >> lane) & 1u) ? 0u : 32u) + (uint32_t)__ffs(wt));
-                        pend[g] &= ~Rall;
+                for (int g = 0; g < G; g++) {                 // all groups' reductions in flight together
+                    const uint32_t a = mA[g] & pend[g], bq = mB[g] & pend[g];
+                    RA[g] = __reduce_or_sync(0xFFFFFFFFu, a);
+                    Rall[g] = RA[g] | __reduce_or_sync(0xFFFFFFFFu, bq);
+                    u[g] = a | (bq & ~RA[g]);
+                    anyR |= Rall[g];
+                }
+                if (anyR) {                                   // warp-uniform; the G transposes interleave
+                    uint32_t wt[G];
+#pragma unroll
+                    for (int g = 0; g < G; g++) wt[g] = tr(u[g]);   // bit i: draw (tb or tb+32) + i green for row lane
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        if (wt[g]) hres[32 * g + lane] = (uint16_t)(tb + (((RA[g] >> lane) & 1u) ? 0u : 32u) + (uint32_t)__ffs(wt[g]));
+                        pend[g] &= ~Rall[g];
                     }
                 }
             }
@@ -650,16 +718,14 @@ wmh_status launch_hash_bitslice(const HashArgs &a, bool *handled) {
     p.sig = a.sig;
     p.n_sat = a.n_sat;
     p.item_ctr = ctr;
-    static const int or_env = getenv("WMH_BV_OR") ? atoi(getenv("WMH_BV_OR")) : 0;
-    p.or_bound = or_env;
     const int grid = (int)std::min((int64_t)sms * sh.ctas, p.n_items);
 #define WMH_BV_GO(V) bv_launch_p<V>(G, sh.clamp, sh.NT, p, smem, grid, a.stream)
     WMH_BV_P_SWITCH(P, WMH_BV_GO)
 #undef WMH_BV_GO
     WMH_LAUNCH_CHECK("hash_bitslice launch");
     if (getenv("WMH_TILED_STATS"))
-        fprintf(stderr, "[wmh bitslice] P=%d clamp=%d G=%d NT=%d grid=%d items=%lld hchunk=%d smem=%zu or=%d\n", P, (int)sh.clamp, G,
-                sh.NT, grid, (long long)p.n_items, hchunk, smem, p.or_bound);
+        fprintf(stderr, "[wmh bitslice] P=%d clamp=%d G=%d NT=%d grid=%d items=%lld hchunk=%d smem=%zu\n", P, (int)sh.clamp, G,
+                sh.NT, grid, (long long)p.n_items, hchunk, smem);
     cudaFreeAsync(scratch, a.stream);
     return WMH_OK;
 }

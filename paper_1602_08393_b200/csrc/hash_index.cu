@@ -268,6 +268,7 @@ struct IxParams {
     unsigned long long *n_sat;
     unsigned long long *row_ctr;
     const uint32_t *perm;        // rows in processing order (deepest epoch first), or null
+    uint8_t *plan;               // optional [n_rows]: the row's plan code (wmh_hash_opts.plan_out)
 };
 
 // x_c of the current row: dense byte, or a lower_bound over the CSR slice
@@ -477,11 +478,15 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
             for (int i = threadIdx.x; i < n; i += NT) xs += __ldg(xrow + i);
         }
         xs = block_sum<NW>(xs);
+        // plan code (tests): epoch | staged << 4 | fallback ran << 5 | several range batches << 6 | zero row << 7
+        uint32_t plan = (staged ? 16u : 0u) | (n > CAPR ? 64u : 0u);
         if (xs == 0) {                           // an all-zero row never turns green (reading R12)
             for (uint32_t j = threadIdx.x; j < p.k; j += NT) h[j] = IX_SAT;
+            plan |= 128u;
         } else {
             const float s = (float)((double)xs / (double)p.M);
             const int e = ix_plan(p, s, CSR ? (staged ? p.cf_smem : p.cf_global) : p.cf_dense);
+            plan |= (uint32_t)e;
             const uint32_t T = p.ep.B[e + 1];
             const uint32_t *pe = p.pos + (uint64_t)e * p.M;
             const uint32_t *ce = p.colstart + (uint64_t)e * (p.D + 1);
@@ -616,6 +621,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                     __syncthreads();
                     const uint32_t U = min(s_nu, (uint32_t)CAPR);
                     if (U == 0) break;
+                    plan |= 32u;
                     if constexpr (NW < 8) {
                     // IX_FB slots per warp, each with its own hash and draw position;
                     // a slot whose hash resolves (or reaches the cap) takes the next
@@ -737,6 +743,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
             }
         }
         __syncthreads();
+        if (p.plan && threadIdx.x == 0) p.plan[row] = (uint8_t)plan;
         // ---- a9: h = t + 1, or the cap
         using sig_t = typename std::conditional<SIGB == 1, uint8_t, uint16_t>::type;
         sig_t *out = reinterpret_cast<sig_t *>(p.sig) + row * (int64_t)p.k;
@@ -1034,6 +1041,7 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     p.n_sat = a.n_sat;
     p.row_ctr = ctr;
     p.perm = nullptr;
+    p.plan = reinterpret_cast<uint8_t *>(a.plan_out);
     // processing order by planned epoch when the per-cell tables are far larger
     // than L2 (measured: c4's 535 MB pos[] 22.8 -> 20.2 ms; c3's 194 MB and c2r
     // gain nothing and pay the pre-pass); WMH_INDEX_ORDER=0/1 forces it off/on

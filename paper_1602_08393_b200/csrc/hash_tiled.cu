@@ -399,16 +399,19 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     static const int bv_env = getenv("WMH_TILED_BV") ? atoi(getenv("WMH_TILED_BV")) : -1;
     if (!force_rm && (a.tile == 3 || (a.tile == 0 && bv_env != 0))) {
         const wmh_status vst = launch_hash_bitslice(a, handled);
+        if (*handled && a.tile_used) *a.tile_used = 3;
         if (vst != WMH_OK || *handled) return vst;
     }
     static const int bs_env = getenv("WMH_TILED_BS") ? atoi(getenv("WMH_TILED_BS")) : -1;
     const bool want_bs = a.tile == 2 || (a.tile == 0 && (bs_env == 1 || (bs_env != 0 && !tiled_cm_full_tile(a))));
     if (!force_rm && want_bs) {
         const wmh_status bst = launch_hash_tiled_bs(a, handled);
+        if (*handled && a.tile_used) *a.tile_used = 2;
         if (bst != WMH_OK || *handled) return bst;
     }
     if (!force_rm) {
         const wmh_status cst = launch_hash_tiled_cm(a, handled);
+        if (*handled && a.tile_used) *a.tile_used = 1;
         if (cst != WMH_OK || *handled) return cst;
     }
     const int D = (int)a.rows.dim;

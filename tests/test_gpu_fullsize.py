@@ -1,10 +1,14 @@
 """Full-size parity at BASELINE.json's sizes, in the launch configuration bench.py
 times (wmh.hash with algo="auto"): every a1-a4 table is checked whole where the
-oracle can build it, and signatures are checked bit-exactly on seeded row
-samples the oracle hashes one by one; the c5 collide runs on all 10^7 pairs
-(match counts exact on a sample, the 3-sigma Jaccard law on all of them)."""
+oracle can build it, and signatures are checked bit-exactly against the oracle
+(SURVEY §8c P9): every row of c2, seeded >= 1% row samples of c4 and c5, and
+>= 2,000 rows of c3 stratified so that every per-row plan the INDEX kernel
+picks (epoch, staged or not, fallback loop, several range batches, all-zero)
+is checked; the c5 collide runs on all 10^7 pairs (match counts exact on a
+sample, the 3-sigma Jaccard law on all of them)."""
 import math
 import os
+from multiprocessing import Pool
 
 import numpy as np
 import pytest
@@ -50,7 +54,17 @@ def _check_rows(sig_gpu, L, data, cfg, rows):
     assert len(bad) == 0, f"{len(bad)} mismatches, first row {rows[bad[0][0]]} hash {bad[0][1]}"
 
 
+def _c5_rows(rows):
+    """Host regeneration of c5 rows (datagen's counter recipe), in parallel."""
+    cfg = datagen.CONFIGS["c5"]
+    parts = np.array_split(np.asarray(rows, np.int64), max(1, min(64, len(rows) // 2048)))
+    with Pool(min(len(parts), os.cpu_count() or 1)) as pool:
+        xs = pool.starmap(datagen.gen_counter_c5_rows, [(cfg.data_seed, p, cfg.dim) for p in parts])
+    return np.concatenate(xs)
+
+
 def test_c2_full(wmh):
+    """Every one of c2's 10^5 x 500 signatures against the oracle."""
     cfg, data = datagen.make("c2")
     rows = to_rows(data)
     layout = wmh.prepare(rows)
@@ -61,10 +75,8 @@ def test_c2_full(wmh):
     nsat = torch.zeros(1, dtype=torch.int64, device="cuda")
     sig = wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, n_saturated=nsat)
     assert wmh.last_algo == "tiled"
-    _check_rows(sig, L, data, cfg, _sample(cfg.n_rows, 96, 11))
+    _check_rows(sig, L, data, cfg, np.arange(cfg.n_rows))
     assert int(nsat.item()) == 0               # s ~ 0.05: P(no green in 65535 draws) is nil
-    sig_simple = wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, algo="simple")
-    assert torch.equal(sig.view(torch.int16), sig_simple.view(torch.int16))   # both kernels, every signature
 
 
 def test_c5_full_and_collide_10M(wmh):
@@ -89,11 +101,14 @@ def test_c5_full_and_collide_10M(wmh):
     L = oracle.Layout(gold)
     assert layout.M == L.M
     sig = wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes)
-    sample = _sample(cfg.n_rows, 48, 12)
-    host = datagen.Dense(datagen.gen_counter_c5_rows(cfg.data_seed, sample, cfg.dim))
-    ref = L.hash_dense(host.x, cfg.seed, cfg.k, cfg.cap)
+    # >= 1% of the rows (160,000, seeded uniform plus the first and last), regenerated on the host
+    sample = _sample(cfg.n_rows, cfg.n_rows // 100, 12)
+    host = _c5_rows(sample)
+    ref = L.hash_dense(host, cfg.seed, cfg.k, cfg.cap)
     got = _rows_of(sig, sample)
-    assert np.array_equal(got, ref)
+    bad = np.argwhere(got != ref)
+    assert len(bad) == 0, f"{len(bad)} mismatches, first row {sample[bad[0][0]]} hash {bad[0][1]}"
+    del host, ref, got
 
     pairs = datagen.random_pairs(cfg.data_seed, cfg.n_rows, cfg.n_pairs)
     pairs_d = torch.from_numpy(pairs).cuda()
@@ -137,7 +152,7 @@ def test_c4_full(wmh):
     L = oracle.Layout(np.full(cfg.dim, 255, np.uint32))
     assert layout.M == L.M and layout.flags & 1
     sig = wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes)
-    _check_rows(sig, L, data, cfg, _sample(cfg.n_rows, 24, 14))
+    _check_rows(sig, L, data, cfg, _sample(cfg.n_rows, cfg.n_rows // 100, 14))      # >= 1%: 2,000 rows
 
 
 def test_c3_full(wmh):
@@ -149,8 +164,27 @@ def test_c3_full(wmh):
     L = oracle.Layout(m)
     assert layout.M == L.M
     nsat = torch.zeros(1, dtype=torch.int64, device="cuda")
-    sig = wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, n_saturated=nsat)
-    _check_rows(sig, L, data, cfg, _sample(cfg.n_rows, 12, 15))
+    plan = torch.zeros(cfg.n_rows, dtype=torch.uint8, device="cuda")
+    sig = wmh.hash(layout, rows, cfg.seed, cfg.k, cfg.cap, cfg.sig_bytes, n_saturated=nsat, plan_out=plan)
+    assert wmh.last_algo == "index"
+    # stratified over the kernel's own per-row plans: up to 40 rows of every plan
+    # code it used, then seeded uniform rows up to 2,000
+    plan = plan.cpu().numpy()
+    rng = np.random.default_rng(15)
+    picked = []
+    codes = np.unique(plan)
+    for c in codes:
+        idx = np.flatnonzero(plan == c)
+        picked.append(rng.choice(idx, size=min(len(idx), 40), replace=False))
+    picked = np.unique(np.concatenate(picked + [_sample(cfg.n_rows, 2000, 16)]))
+    rest = np.setdiff1d(np.arange(cfg.n_rows), picked)
+    extra = max(0, 2000 - len(picked))
+    sample = np.sort(np.concatenate([picked, rng.choice(rest, size=extra, replace=False)]))
+    assert len(sample) >= 2000
+    assert set(np.unique(plan[sample]).tolist()) == set(codes.tolist())      # every plan the kernel ran is checked
+    epochs = set((codes & 15).tolist())
+    assert len(epochs) >= 2 and any(c & 32 for c in codes), codes           # several horizons, and the fallback loop
+    _check_rows(sig, L, data, cfg, sample)
     # ~11% of c3's hashes saturate; every saturated entry reads cap
     frac = int(nsat.item()) / (cfg.n_rows * cfg.k)
     assert 0.03 < frac < 0.3

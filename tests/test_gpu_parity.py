@@ -475,6 +475,46 @@ def test_collide_estimates_jaccard_c5_recipe(wmh):
     assert 0.75 <= z.var() <= 1.25
 
 
+def test_collide_unbiased_over_seeds(wmh):
+    """Eq. 14-15 on the GPU path across independent hash seeds:
+    E[J-hat] = J(1 - q) + q ~ J and Var(J-hat) = J(1-J)/k per seed, so the
+    mean over 16 seeds of J-hat for each of 10^5 pairs has z-scores
+    (mean - J) / sqrt(J(1-J)/(16k)) with mean ~0 and variance ~1.  The pairs
+    span J in (0.25, 1): x from the c5 recipe (D = 1024) and y = x with every
+    entry replaced, with a per-pair probability, by an independent c5 entry.
+    The per-seed common shift of reading R16 (sd ~0.2 in z for one seed)
+    averages down to ~0.05 over 16 seeds."""
+    n, D, k, S = 100_000, 1024, 1024, 16
+    x = datagen.gen_counter_c5_rows(2101, np.arange(n), D)
+    alt = datagen.gen_counter_c5_rows(2102, np.arange(n), D)
+    q = np.random.default_rng(5).random(n)[:, None]
+    repl = np.random.default_rng(6).random((n, D)) < q
+    y = np.where(repl, alt, x)
+    xy = torch.from_numpy(np.concatenate([x, y])).cuda()
+    rows = wmh.Rows.from_dense(xy)
+    layout = wmh.prepare(rows)
+    pairs = torch.stack([torch.arange(n), torch.arange(n) + n], 1).cuda()
+    xa, xb = xy[:n].int(), xy[n:].int()
+    J = (torch.minimum(xa, xb).sum(1).double() / torch.maximum(xa, xb).sum(1).double())
+    ok = (J > 0) & (J < 1)
+    assert float(J[ok].min()) < 0.35 and float(J[ok].max()) > 0.95
+    acc = torch.zeros(n, dtype=torch.float64, device="cuda")
+    seed_mean_z = []
+    for seed in range(S):
+        sig = wmh.hash(layout, rows, 1000 + seed, k, 65535)
+        _, jhat = wmh.collide(sig, pairs)
+        acc += jhat.double()
+        zs = ((jhat.double() - J) / torch.sqrt(J * (1 - J) / k))[ok]
+        seed_mean_z.append(float(zs.mean()))
+    z = ((acc / S - J) / torch.sqrt(J * (1 - J) / (S * k)))[ok]
+    P = int(ok.sum().item())
+    assert abs(float(z.mean())) <= 0.25, (float(z.mean()), seed_mean_z)
+    assert 0.85 <= float(z.var()) <= 1.15, float(z.var())
+    assert int((z.abs() > 3).sum().item()) <= 0.01 * P
+    sd = float(np.std(seed_mean_z))
+    assert sd < 0.5 and abs(float(np.mean(seed_mean_z))) <= 3 * max(sd, 0.05) / math.sqrt(S), seed_mean_z
+
+
 def test_hasher_streams_batches(wmh):
     """wmh_hasher: the draws filed once, several row batches hashed with the row
     pass only -- identical to wmh_hash on the whole matrix and to the oracle."""
