@@ -713,9 +713,39 @@ def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd=None):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = float(t.item())
-    return {"value": n * cfg.k * world * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(out.numel() * out.element_size()), "steps": steps,
-            "api": "wmh_hash_host (pinned host rows -> H2D -> hash -> D2H signatures, synchronised)"}
+    d2h = int(out.numel() * out.element_size())
+    bound_s = pcie_bound(h2d, d2h, dev)
+    value = n * cfg.k * world * steps / dt
+    return {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": d2h, "steps": steps, "rows": n,
+            "api": "wmh_hash_host (pinned host rows -> H2D -> hash -> D2H signatures, synchronised)",
+            "pcie_bound_ms": bound_s * 1e3, "ms_per_call": dt / steps * 1e3,
+            "frac_of_pcie_bound": bound_s / (dt / steps),
+            "pcie_bound_how": "the same byte counts copied pinned H2D and D2H at once on two streams (torch), "
+                              "best of 3; the call cannot beat it"}
+
+
+def pcie_bound(h2d: int, d2h: int, dev) -> float:
+    """Seconds to move h2d bytes in and d2h bytes out at once over this box's link
+    (pinned buffers, two streams, best of 3) -- the e2e call's copy floor."""
+    import torch
+    hi = torch.empty(h2d, dtype=torch.uint8).pin_memory()
+    di = torch.empty(h2d, dtype=torch.uint8, device=dev)
+    ho = torch.empty(d2h, dtype=torch.uint8).pin_memory()
+    do = torch.empty(d2h, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = float("inf")
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            di.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(s2):
+            ho.copy_(do, non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    del hi, di, ho, do
+    return best
 
 
 

@@ -196,7 +196,8 @@ wmh_status wmh_hash(const wmh_layout *layout, const wmh_rows *rows, uint64_t see
 typedef enum {
     WMH_ALGO_AUTO = 0,   /* pick per input (the default used by wmh_hash)         */
     WMH_ALGO_SIMPLE = 1, /* one thread per (row, j), global-table lookups         */
-    WMH_ALGO_TILED = 2,  /* rows staged in shared memory, draws shared by a tile  */
+    WMH_ALGO_TILED = 2,  /* dense rows staged in shared memory, draws shared by a tile
+                            (CSR rows: WMH_EINVAL "does not take this input shape") */
     WMH_ALGO_INDEX = 3   /* draws (j, t < T) filed once per call under their cell; a
                             row visits only its green draws, then Alg. 3's loop from
                             t = T for hashes still unresolved; k up to ~54,000 on

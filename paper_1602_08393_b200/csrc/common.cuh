@@ -132,7 +132,6 @@ struct HashArgs {
 
 wmh_status launch_hash_simple(const HashArgs &a);
 wmh_status launch_hash_tiled(const HashArgs &a, bool *handled);
-wmh_status launch_hash_tiled_csr(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_cm(const HashArgs &a, bool *handled);
 wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled);
 wmh_status launch_hash_bitslice(const HashArgs &a, bool *handled);

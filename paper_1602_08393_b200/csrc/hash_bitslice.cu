@@ -244,8 +244,6 @@ __device__ __forceinline__ void bv_test(const BvParams &p, uint32_t planes_s, co
     if constexpr (BvLayout<P, G>::GROUP_MAJOR) {
 #pragma unroll
         for (int g = 0; g < G; g++) {
-            mask[g] = 0u;
-            if (pend[g] == 0u) continue;                 // warp-uniform
             uint32_t xg[P];
             bv_load_group<P, G>(blk, g, need[g], xg);
             mask[g] = need[g] ? bv_chain<P>(xg, m) : 0u;
@@ -261,9 +259,7 @@ __device__ __forceinline__ void bv_test(const BvParams &p, uint32_t planes_s, co
         bv_load_all<P, G>(blk, need_any, xa);
 #pragma unroll
         for (int g = 0; g < G; g++) {
-            mask[g] = 0u;
-            if (pend[g] == 0u) continue;                 // warp-uniform: a finished group costs nothing
-            mask[g] = need[g] ? bv_chain<P>(xa[g], m) : 0u;
+            mask[g] = need[g] ? bv_chain<P>(xa[g], m) : 0u;   // branch-free: the two draws' tests interleave
             if (CLAMP && need[g] && off >= TOP) {
                 uint32_t cand = xa[g][0];
 #pragma unroll
@@ -445,10 +441,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
         uint32_t j = jb;
         // draw words: lane holds t = tb + lane (A) and tb + 32 + lane (B) of the
         // current round, the next round's pair, and the next hash's first pair
-        uint32_t na = 0, nb = 0;
+        uint32_t na = 0, nb = 0, nc = 0, nd = 0;      // the next hash's rounds 0 and 1
         if (j < j1) {
-            na = __ldg(p.table + (int64_t)j * T0 + lane);
-            nb = __ldg(p.table + (int64_t)j * T0 + 32 + lane);
+            const uint32_t *t0 = p.table + (int64_t)j * T0;
+            na = __ldg(t0 + lane);
+            nb = __ldg(t0 + 32 + lane);
+            nc = __ldg(t0 + 64 + lane);
+            nd = __ldg(t0 + 96 + lane);
         }
         while (j < j1) {
             const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
@@ -456,14 +455,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
             const uint32_t *tj = p.table + (int64_t)j * T0;
             const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
             uint32_t wA = na, wB = nb;
-            uint32_t xA = 0, xB = 0;                   // the next round's words
-            if (64 < T0) {
-                xA = __ldg(tj + 64 + lane);
-                xB = __ldg(tj + 96 + lane);
-            }
-            if (jn < j1) {                             // one hash ahead
-                na = __ldg(p.table + (int64_t)jn * T0 + lane);
-                nb = __ldg(p.table + (int64_t)jn * T0 + 32 + lane);
+            uint32_t xA = nc, xB = nd;                 // the next round's words
+            if (jn < j1) {                             // one hash ahead: its rounds 0 and 1
+                const uint32_t *tn = p.table + (int64_t)jn * T0;
+                na = __ldg(tn + lane);
+                nb = __ldg(tn + 32 + lane);
+                nc = __ldg(tn + 64 + lane);
+                nd = __ldg(tn + 96 + lane);
             }
             // all-zero rows: cap at once (lane = row)
 #pragma unroll

@@ -385,7 +385,8 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     *handled = false;
     // the tiles test uint8 weights against 8-bit cell offsets: narrow layouts only
     if ((a.L->flags & WMH_LAYOUT_WIDE) || weight_bytes(a.rows) != 1) return WMH_OK;
-    if (a.rows.kind != WMH_DENSE) return launch_hash_tiled_csr(a, handled);
+    // sparse rows are hashed by the INDEX kernel (or SIMPLE); the tiles test dense rows
+    if (a.rows.kind != WMH_DENSE) return WMH_OK;
     // column-major tile with the SIMD first round (hash_tiled_cm.cu) unless
     // WMH_TILED_RM=1 selects this row-major kernel
     static const bool force_rm = getenv("WMH_TILED_RM") != nullptr;
