@@ -240,6 +240,10 @@ typedef struct {
 #define WMH_OPT_TILE_BYTES 2u
 #define WMH_OPT_TILE_BITPLANES 4u
 #define WMH_OPT_TILE_BITSLICE 8u
+#define WMH_OPT_ISGREEN_BINSEARCH 32u  /* Alg. 5's component lookup by binary search over
+                                         CompToM (Sec. 3.3) instead of the IntToComp
+                                         table: SIMPLE per draw, the tiles' draw tables.
+                                         Same results; the measured alternative */
 #define WMH_OPT_VALIDATE 16u      /* check every row against the layout's bounds first
                                      (wmh_check_rows): WMH_EBOUND instead of silently
                                      wrong signatures for x_c > m_c.  One extra pass

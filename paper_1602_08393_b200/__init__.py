@@ -235,13 +235,16 @@ last_tile = None     # the dense tile of the last hash() call that ran TILED ('b
 def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int | None = None,
          algo: str = "auto", out: torch.Tensor | None = None, n_saturated: torch.Tensor | None = None,
          chunk: int = 0, horizon: int = 0, time_kernel: bool = False, stream=None,
-         tile: str = "auto", validate: bool = False, plan_out: torch.Tensor | None = None) -> torch.Tensor:
+         tile: str = "auto", validate: bool = False, plan_out: torch.Tensor | None = None,
+         isgreen: str = "table") -> torch.Tensor:
     """a5-a9: signatures sig[n][j] = h_j(x_n) (uint8 when sig_bytes = 1, else uint16).
     `tile` ("auto", "bytes", "bitplanes", "bitslice") picks the TILED kernel's dense tile
     (performance only).  `validate` checks every row against the layout's bounds
     first (wmh_check_rows: WmhError EBOUND instead of silently wrong signatures
     for rows prepare() did not see).  `plan_out` (uint8 [n_rows], tests): the INDEX
-    kernel's per-row plan codes (include/wmh.h, wmh_hash_opts.plan_out)."""
+    kernel's per-row plan codes (include/wmh.h, wmh_hash_opts.plan_out).  `isgreen` ("table" or
+    "bsearch"): Alg. 5's component lookup by IntToComp or by binary search over CompToM (Sec. 3.3;
+    SIMPLE per draw, the bit-sliced tile's draw table) -- same results."""
     if sig_bytes is None:
         sig_bytes = 1 if cap <= 255 else 2
     dtype = torch.uint8 if sig_bytes == 1 else torch.uint16
@@ -255,7 +258,10 @@ def hash(layout: Layout, rows: Rows, seed: int, k: int, cap: int, sig_bytes: int
         raise ValueError("n_saturated must be a CUDA int64 tensor")
     if tile not in ("auto", "bytes", "bitplanes", "bitslice"):
         raise ValueError(f"tile must be auto, bytes, bitplanes or bitslice, not {tile!r}")
+    if isgreen not in ("table", "bsearch"):
+        raise ValueError("isgreen must be 'table' (IntToComp) or 'bsearch' (binary search over CompToM)")
     flags = (_lib.WMH_OPT_TIME_KERNEL if time_kernel else 0) | (_lib.WMH_OPT_VALIDATE if validate else 0) | \
+        (_lib.WMH_OPT_ISGREEN_BINSEARCH if isgreen == "bsearch" else 0) | \
         {"auto": 0, "bytes": _lib.WMH_OPT_TILE_BYTES, "bitplanes": _lib.WMH_OPT_TILE_BITPLANES,
          "bitslice": _lib.WMH_OPT_TILE_BITSLICE}[tile]
     if plan_out is not None and (plan_out.dtype != torch.uint8 or plan_out.numel() < rows.n_rows or not plan_out.is_cuda):

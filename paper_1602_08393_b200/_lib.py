@@ -15,6 +15,7 @@ WMH_OPT_TILE_BYTES = 2
 WMH_OPT_TILE_BITPLANES = 4
 WMH_OPT_TILE_BITSLICE = 8
 WMH_OPT_VALIDATE = 16
+WMH_OPT_ISGREEN_BINSEARCH = 32
 ALGOS = {"auto": 0, "simple": 1, "tiled": 2, "index": 3}
 STATUS_NAMES = {0: "WMH_OK", 1: "WMH_EINVAL", 2: "WMH_EBOUND", 3: "WMH_EEMPTY", 4: "WMH_EOVERFLOW",
                 5: "WMH_ECUDA", 6: "WMH_ENOMEM"}

@@ -185,7 +185,7 @@ static bool tiny_batch(const wmh_layout *L, const wmh_rows *rows, uint32_t k, ui
 static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint64_t seed, uint32_t k, uint32_t cap,
                                 int32_t sig_bytes, void *sig_out, uint64_t *n_saturated, int algo, int chunk,
                                 uint32_t horizon, cudaStream_t s, int *algo_used, int tile = 0, void *plan_out = nullptr,
-                                int *tile_used = nullptr) {
+                                int *tile_used = nullptr, bool bsearch = false) {
     *algo_used = algo == WMH_ALGO_AUTO ? WMH_ALGO_SIMPLE : algo;
     if (rows->n_rows == 0) return WMH_OK;
     HashArgs a;
@@ -203,6 +203,7 @@ static wmh_status hash_dispatch(const wmh_layout *L, const wmh_rows *rows, uint6
     a.tile = tile;
     a.plan_out = plan_out;
     a.tile_used = tile_used;
+    a.isgreen_bsearch = bsearch;
     if (algo == WMH_ALGO_INDEX) {
         *algo_used = WMH_ALGO_INDEX;
         return launch_hash_index(a, horizon);
@@ -246,7 +247,7 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
     if (opts) {
         algo = opts->algo;
         const uint32_t tiles = WMH_OPT_TILE_BYTES | WMH_OPT_TILE_BITPLANES | WMH_OPT_TILE_BITSLICE;
-        if (opts->flags & ~(uint32_t)(WMH_OPT_TIME_KERNEL | WMH_OPT_VALIDATE | tiles)) { set_error("wmh_hash_ex: unknown flags 0x%x", opts->flags); return WMH_EINVAL; }
+        if (opts->flags & ~(uint32_t)(WMH_OPT_TIME_KERNEL | WMH_OPT_VALIDATE | WMH_OPT_ISGREEN_BINSEARCH | tiles)) { set_error("wmh_hash_ex: unknown flags 0x%x", opts->flags); return WMH_EINVAL; }
         if (__builtin_popcount(opts->flags & tiles) > 1) { set_error("wmh_hash_ex: the WMH_OPT_TILE_* flags are exclusive"); return WMH_EINVAL; }
         tile = (opts->flags & WMH_OPT_TILE_BYTES) ? 1 : (opts->flags & WMH_OPT_TILE_BITPLANES) ? 2
              : (opts->flags & WMH_OPT_TILE_BITSLICE) ? 3 : 0;
@@ -266,7 +267,8 @@ extern "C" wmh_status wmh_hash_ex(const wmh_layout *L, const wmh_rows *rows, uin
     g_ktimer.on = opts && (opts->flags & WMH_OPT_TIME_KERNEL);
     if (g_ktimer.on) g_ktimer.recorded = false;
     st = hash_dispatch(L, rows, seed, k, cap, sig_bytes, sig_out, n_saturated, algo, chunk, horizon, (cudaStream_t)stream,
-                       &used, tile, opts ? opts->plan_out : nullptr, opts ? &opts->tile_used : nullptr);
+                       &used, tile, opts ? opts->plan_out : nullptr, opts ? &opts->tile_used : nullptr,
+                       opts && (opts->flags & WMH_OPT_ISGREEN_BINSEARCH));
     g_ktimer.on = false;
     if (opts) {
         opts->algo_used = used;

@@ -110,6 +110,22 @@ __device__ __forceinline__ uint2 cell_lookup(uint32_t r, const uint32_t *__restr
     return make_uint2(c, r - __ldg(c2m + c));
 }
 
+// Sec. 3.3's alternative to the IntToComp table ("binary search over
+// CompToM"): the component c with CompToM[c] <= r < CompToM[c+1], found in
+// ceil(log2 D) dependent loads of the (D+1)-entry prefix array instead of one
+// load of the M-entry table.  Zero-width components (CompToM[c] = CompToM[c+1],
+// reading R11) never satisfy the bracket.  The measured alternative
+// (WMH_OPT_ISGREEN_BINSEARCH).
+__device__ __forceinline__ uint2 cell_bsearch(uint32_t r, const uint32_t *__restrict__ c2m, uint32_t D) {
+    uint32_t lo = 0, hi = D;                     // CompToM[lo] <= r < CompToM[hi] (CompToM[D] = M > r)
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(c2m + mid) <= r) lo = mid;
+        else hi = mid;
+    }
+    return make_uint2(lo, r - __ldg(c2m + lo));
+}
+
 // weight width of a batch (wmh_rows.weight_bytes: 0 or 1 -> 1)
 inline int weight_bytes(const wmh_rows &r) { return r.weight_bytes == 2 ? 2 : 1; }
 
@@ -128,6 +144,7 @@ struct HashArgs {
     int tile = 0;        // TILED dense: 0 auto, 1 byte tile, 2 bit-plane tile, 3 bit-sliced tile
     void *plan_out = nullptr;    // INDEX: optional per-row plan codes (wmh_hash_opts.plan_out)
     int *tile_used = nullptr;    // TILED dense: written with the tile that ran (1/2/3)
+    bool isgreen_bsearch = false;  // WMH_OPT_ISGREEN_BINSEARCH: cells by binary search over CompToM
 };
 
 wmh_status launch_hash_simple(const HashArgs &a);

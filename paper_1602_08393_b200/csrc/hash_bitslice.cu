@@ -67,12 +67,21 @@ __device__ __forceinline__ uint32_t bv_word(uint32_t r, const uint32_t *pack, ui
     return t < cap ? cell_of(r, pack, uni_m) : 0xFFu;
 }
 
+// the first T0 draw words of every hash; cells by the packed IntToComp table or
+// (c2m != null, WMH_OPT_ISGREEN_BINSEARCH) by binary search over CompToM
 __global__ void bv_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
-                                const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t cap) {
+                                const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t cap,
+                                const uint32_t *__restrict__ c2m, uint32_t D) {
     const int64_t total = (int64_t)k * T0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
-        table[i] = bv_word(draw_r(S, j, t, M), pack, uni_m, t, cap);
+        const uint32_t r = draw_r(S, j, t, M);
+        if (c2m) {
+            const uint2 cell = cell_bsearch(r, c2m, D);
+            table[i] = t < cap ? (cell.x << 8) | cell.y : 0xFFu;
+        } else {
+            table[i] = bv_word(r, pack, uni_m, t, cap);
+        }
     }
 }
 
@@ -688,7 +697,8 @@ wmh_status launch_hash_bitslice(const HashArgs &a, bool *handled) {
     {
         const int64_t total = (int64_t)a.k * T0;
         const int blocks = (int)std::min((int64_t)sms * 8, (total + 255) / 256);
-        bv_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, (uint32_t)a.L->M, a.L->cell_pack, uni_m, a.cap);
+        bv_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, (uint32_t)a.L->M, a.L->cell_pack, uni_m, a.cap,
+                                                      a.isgreen_bsearch ? a.L->comp_to_m : nullptr, (uint32_t)D);
         count_launch();
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { cudaFreeAsync(scratch, a.stream); return cuda_fail(e, "bitslice table launch"); }

@@ -26,7 +26,7 @@ __device__ __forceinline__ uint32_t csr_value(const int32_t *__restrict__ col, c
     return (lo < b && (uint32_t)__ldg(col + lo) == c) ? (uint32_t)__ldg(val + lo) : 0u;
 }
 
-template <int SIGB, bool CSR, typename W>
+template <int SIGB, bool CSR, typename W, bool BSEARCH = false>
 __global__ void __launch_bounds__(256) hash_simple_kernel(
     const W *__restrict__ dense, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
     const W *__restrict__ val, int64_t n_rows, int64_t dim, const uint32_t *__restrict__ pack, uint32_t uni_m,
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) hash_simple_kernel(
         if (!CSR || a < b) {
             for (uint32_t t = 0; t < cap; t++) {
                 const uint32_t r = mulhi_range(splitmix64(keyj ^ (uint64_t)t), M);
-                const uint2 cell = cell_lookup(r, pack, uni_m, i2c, c2m);
+                const uint2 cell = BSEARCH ? cell_bsearch(r, c2m, (uint32_t)dim) : cell_lookup(r, pack, uni_m, i2c, c2m);
                 const uint32_t c = cell.x, off = cell.y;
                 uint32_t xv;
                 if (CSR) xv = csr_value(col, val, a, b, c);
@@ -74,7 +74,8 @@ wmh_status launch_hash_simple(const HashArgs &a) {
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
     const uint32_t *pack = (a.L->flags & WMH_LAYOUT_WIDE) ? nullptr : a.L->cell_pack;
 #define WMH_SIMPLE(SB, CS, W)                                                                                    \
-    hash_simple_kernel<SB, CS, W><<<(unsigned)blocks, threads, 0, a.stream>>>(                                   \
+    (a.isgreen_bsearch ? hash_simple_kernel<SB, CS, W, true> : hash_simple_kernel<SB, CS, W, false>)             \
+        <<<(unsigned)blocks, threads, 0, a.stream>>>(                                                            \
         reinterpret_cast<const W *>(a.rows.dense), a.rows.row_ptr, a.rows.col, reinterpret_cast<const W *>(a.rows.val), \
         a.rows.n_rows, a.rows.dim, pack, uni_m, a.L->int_to_comp, a.L->comp_to_m, M, a.S, a.k, a.cap, a.sig, a.n_sat)
     kernel_timer_begin(a.stream);

@@ -395,10 +395,13 @@ wmh_status launch_hash_tiled(const HashArgs &a, bool *handled) {
     // (measured: c5's recipe, 10^6 rows, NB = 6: 18.1 vs 21.2 ms; on c2's
     // 128-row tile the SWAR byte tile stays ahead, 0.58 vs 0.75 ms);
     // WMH_TILED_BS=1 / 0 or the WMH_OPT_TILE_* flags force the choice
-    // the lane-per-draw bit-sliced tile (hash_bitslice.cu) first: AUTO or
-    // WMH_OPT_TILE_BITSLICE; WMH_TILED_BV=0 drops it from AUTO
+    // the lane-per-draw bit-sliced tile (hash_bitslice.cu) for long rows, where
+    // the byte tile would hold fewer than 128 rows (c5, D = 4096: 12.4 ms per
+    // 2^20 rows vs 17.95 for the round-1 bit-plane tile and 21 for the byte
+    // tile); on c2's 128-row byte tile the SWAR byte test stays ahead (0.58 vs
+    // 1.03 ms).  WMH_OPT_TILE_BITSLICE forces it; WMH_TILED_BV=0 drops it from AUTO
     static const int bv_env = getenv("WMH_TILED_BV") ? atoi(getenv("WMH_TILED_BV")) : -1;
-    if (!force_rm && (a.tile == 3 || (a.tile == 0 && bv_env != 0))) {
+    if (!force_rm && (a.tile == 3 || (a.tile == 0 && bv_env != 0 && (bv_env == 1 || !tiled_cm_full_tile(a))))) {
         const wmh_status vst = launch_hash_bitslice(a, handled);
         if (*handled && a.tile_used) *a.tile_used = 3;
         if (vst != WMH_OK || *handled) return vst;

@@ -57,6 +57,7 @@ def disasm(obj, kernel_match):
     text = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubins[0])], capture_output=True,
                           text=True, check=True).stdout
     out, cur, take, name = [], None, False, None
+    labels, pending = {}, []
     for l in text.split("\n"):
         m = re.match(r"\s*\.section\s+\.text\.(\S+),", l)
         if m:
@@ -70,11 +71,21 @@ def disasm(obj, kernel_match):
         if m:
             cur = (m.group(1), int(m.group(2)))
             continue
+        m = re.match(r"^(\.L_x_\d+):", l.strip())
+        if m:
+            pending.append(m.group(1))
+            continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?)\s*;", l)
         if m:
-            out.append((int(m.group(1), 16), cur, m.group(2).strip()))
+            a = int(m.group(1), 16)
+            for lb in pending:
+                labels[lb] = a
+            pending = []
+            out.append((a, cur, m.group(2).strip()))
     if not out:
         raise SystemExit(f"no kernel matching {kernel_match}")
+    # branch targets as addresses
+    out = [(a, c, re.sub(r"`\((\.L_x_\d+)\)", lambda mm: hex(labels.get(mm.group(1), -1)), op)) for a, c, op in out]
     return name, out
 
 
@@ -115,17 +126,91 @@ def bitslice_regions():
     }
 
 
+def per_unit_budget(obj, kernel_match, src, first_marker, last_marker, unit_op, unit_name, out, extra_lines=(),
+                    loop=False, unit_prefix=True):
+    """Static SASS of the (unrolled) source lines [first_marker, last_marker] of
+    `src`, divided by the number of `unit_op` instructions they contain (one per
+    unit of work: a draw-test or a visited entry): lane-instructions per unit."""
+    import collections
+    f = os.path.join(CSRC, src)
+    l0, l1 = line_of(f, first_marker), line_of(f, last_marker)
+    lines = set(range(l0, l1 + 1)) | {line_of(f, m) for m in extra_lines}
+    name, ins = disasm(os.path.join(BUILD, src + ".o"), kernel_match)
+    marked = [x for x in ins if x[1] and x[1][0] == src and x[1][1] in lines]
+    lo, hi = min(x[0] for x in marked), max(x[0] for x in marked)
+    if loop:                       # the innermost natural loop around the marked lines
+        best = None                # the back-edge enclosing the most marked instructions, then the tightest
+        for addr, c, op in ins:
+            m = re.match(r"(?:@!?U?P\w+\s+)?BRA(?:\.\w+)*\s+0x([0-9a-f]+)", op)
+            if not m or int(m.group(1), 16) >= addr:
+                continue
+            t = int(m.group(1), 16)
+            n_in = sum(1 for x in marked if t <= x[0] <= addr)
+            key = (n_in, -(addr - t))
+            if best is None or key > best[0]:
+                best = (key, t, addr)
+        lo, hi = best[1], best[2]
+    # every instruction in the span (inlined helpers included)
+    body = [x for x in ins if lo <= x[0] <= hi]
+    ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", op).split()[0] for _, _, op in body)
+    units = sum(v for k, v in ops.items() if k == unit_op or (unit_prefix and k.startswith(unit_op + ".")))
+    res = {"kernel": name.split(",")[0], "source": f"{src}:{l0}-{l1}", "span": [hex(lo), hex(hi)],
+           "span_is": "innermost loop around the lines" if loop else "address span of the (unrolled) lines",
+           "instructions": len(body),
+           "units": units, "unit": unit_name, "unit_op": unit_op,
+           "lane_instr_per_unit": len(body) / max(units, 1), "opcodes": dict(ops.most_common())}
+    json.dump(res, open(out + ".json", "w"), indent=1)
+    open(out + ".txt", "w").write("\n".join(f"/*{a:05x}*/ {op:60s} // {c[0]}:{c[1]}" for a, c, op in body) + "\n")
+    print(json.dumps({k: v for k, v in res.items() if k != "opcodes"}, indent=1))
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["bitslice"])
+    ap.add_argument("which", choices=["bitslice", "cm", "index", "simple"])
     ap.add_argument("--kernel-match", nargs="+", default=["bitslice_kernel", "ILi6ELi2ELb0ELi512"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_sass_bitslice"))
     a = ap.parse_args()
+    if a.which == "cm":            # the byte tile's SWAR round: one LDS of a 4-row word per draw
+        return per_unit_budget("hash_tiled_cm.cu", ["hash_tiled_cm_kernel", "ILi2ELi1ELi1ELi1E"], "hash_tiled_cm.cu",
+                               "for (int u = PER - 1; u >= 0; u--) {",
+                               "h4 = (h4 & ~m) | ((uint32_t)(part * PD + PER * i4 + u) * 0x01010101u & m);",
+                               "LDS", "draw tested against a 4-row word (4 row-tests)",
+                               os.path.join(ROOT, "profiles", "r2_sass_cm"), extra_lines=["const uint4 q4 = e4[i4];"],
+                               unit_prefix=False)
+    if a.which == "index":         # the INDEX rows kernel's entry walk: one global load of a filed draw per entry
+        return per_unit_budget("hash_index.cu", ["hash_index_kernel", "ILi2ELb1ELi2E"], "hash_index.cu",
+                               "for (uint32_t w = w0; w < w1; w += IX_U) {",
+                               "if (v[u] != IX_NONE) atomicMin(h + (v[u] >> 16), v[u] & 0xFFFFu);",
+                               "LDG", "visited entry (filed draw) per lane",
+                               os.path.join(ROOT, "profiles", "r2_sass_index"), loop=True)
+    if a.which == "simple":        # the paper's loop: one cell load per draw
+        return per_unit_budget("hash_simple.cu", ["hash_simple_kernel", "ILi1ELb0EhLb0E"], "hash_simple.cu",
+                               "for (uint32_t t = 0; t < cap; t++) {",
+                               "if (off < xv) { h = t + 1; found = true; break; }",
+                               "LDG", "draw (the paper's per-row loop)",
+                               os.path.join(ROOT, "profiles", "r2_sass_simple"), loop=True)
     spec = bitslice_regions()
     name, ins = disasm(os.path.join(BUILD, "hash_bitslice.cu.o"), a.kernel_match)
     fname, l0, l1 = spec["loop"]
-    addrs = [x[0] for x in ins if x[1] and x[1][0] == fname and l0 <= x[1][1] <= l1]
-    lo, hi = min(addrs), max(addrs)
+    # the round loop = the innermost natural loop (a backward branch and its
+    # target) that holds both test and combine instructions
+    test_pred = spec["regions"][2][1]
+    comb_pred = spec["regions"][3][1]
+    best = None
+    for addr, c, op in ins:
+        m = re.match(r"(?:@!?U?P\w+\s+)?BRA(?:\.\w+)*\s+0x([0-9a-f]+)", op)
+        if not m:
+            continue
+        tgt = int(m.group(1), 16)
+        if tgt >= addr:
+            continue
+        body = [x for x in ins if tgt <= x[0] <= addr]
+        if any(x[1] and test_pred(x[1]) for x in body) and any(x[1] and comb_pred(x[1]) for x in body):
+            if best is None or addr - tgt < best[1] - best[0]:
+                best = (tgt, addr)
+    if best is None:
+        raise SystemExit("round loop not found")
+    lo, hi = best
     rng = [x for x in ins if lo <= x[0] <= hi]
     counts = {r[0]: 0 for r in spec["regions"]}
     lines = []

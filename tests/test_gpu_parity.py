@@ -250,6 +250,31 @@ def test_bitslice_clamped_group_major(wmh, capfd, monkeypatch):
     assert "[wmh bitslice] P=4 clamp=1 G=4" in err, err[-300:]
 
 
+@pytest.mark.parametrize("name,n,k,algo,tile", [("c1", 300, 64, "simple", "auto"), ("c5", 150, 96, "simple", "auto"),
+                                                 ("c5", 150, 96, "tiled", "bitslice"), ("c3", 50, 64, "simple", "auto"),
+                                                 ("zero", 90, 48, "simple", "auto"), ("zero", 90, 48, "tiled", "bitslice")])
+def test_isgreen_binary_search(wmh, name, n, k, algo, tile):
+    """Sec. 3.3's alternative ISGREEN: the component by binary search over
+    CompToM instead of the IntToComp table, in SIMPLE (every draw) and the
+    bit-sliced tile's draw table -- bit-identical signatures, including layouts
+    with zero-width components (m_c = 0, reading R11) that the search must skip."""
+    if name == "zero":
+        rng = np.random.default_rng(21)
+        x = rng.integers(0, 12, size=(n, 256)).astype(np.uint8)
+        x[:, ::3] = 0                              # every third column absent: zero-width intervals
+        x[:, 255] = 0
+        cfg, data = datagen.Config("zero", n, 256, k, 65535, 2), datagen.Dense(x)
+    else:
+        cfg, data = datagen.make(name, n_rows=n)
+    rows = to_rows(data)
+    layout = wmh.prepare(rows)
+    L = oracle.Layout(oracle_bounds(data))
+    ref = oracle_hash(L, data, 3, k, 65535)
+    for isg in ("table", "bsearch"):
+        sig = wmh.hash(layout, rows, 3, k, 65535, 2, algo=algo, tile=tile, isgreen=isg)
+        _assert_sig_equal(sig, ref, f"{name}/{algo}/{tile}/{isg}")
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_hash_maximum_sizes(wmh, algo):
     """Limits: k = 65536 on CSR rows (the INDEX kernel keeps h[k] in shared
