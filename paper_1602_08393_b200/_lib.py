@@ -6,7 +6,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libwmh.so")
+SO_PATH = os.path.join(_HERE, "libwmh_debug.so" if os.environ.get("WMH_LIB") == "debug" else "libwmh.so")
 
 WMH_OK, WMH_EINVAL, WMH_EBOUND, WMH_EEMPTY, WMH_EOVERFLOW, WMH_ECUDA, WMH_ENOMEM = range(7)
 WMH_DENSE, WMH_CSR = 0, 1

@@ -10,7 +10,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-SO = os.path.join(PKG, "libwmh.so")
+# WMH_LIB=debug: a second library built with -DWMH_DEBUG, whose kernels check
+# their shared/global indices with device-side asserts (WMH_DASSERT) -- the
+# bounds checking used where compute-sanitizer is not available
+DEBUG = os.environ.get("WMH_LIB") == "debug"
+SO = os.path.join(PKG, "libwmh_debug.so" if DEBUG else "libwmh.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -53,11 +57,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 def _build(verbose: bool) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_debug" if DEBUG else "build")
     os.makedirs(objdir, exist_ok=True)
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *(["-DWMH_DEBUG"] if DEBUG else []), "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     # translation units compile in parallel (the two big template files dominate)

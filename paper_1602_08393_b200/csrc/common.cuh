@@ -27,6 +27,25 @@ struct wmh_layout {
 #define WMH_LAYOUT_UNIFORM 1u
 #define WMH_LAYOUT_WIDE 2u          // some bound > 255: no cell_pack, uint16 offsets
 
+// Device-side bounds checks of the debug library (WMH_LIB=debug, -DWMH_DEBUG):
+// an index outside its array prints and traps the kernel.  Compiled out of the
+// product library.
+#ifdef WMH_DEBUG
+#include <stdio.h>
+#define WMH_DASSERT(cond)                                                                 \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("WMH_DASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define WMH_DASSERT(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 namespace wmh {
 
 // ----------------------------------------------------------------- errors

@@ -236,6 +236,7 @@ __device__ __forceinline__ void bv_test(const BvParams &p, uint32_t planes_s, co
     constexpr int W = G * P;
     constexpr uint32_t TOP = (1u << P) - 1u;
     const uint32_t c = w >> 8, off = w & 0xFFu;
+    WMH_DASSERT(c < (uint32_t)p.D);
     const uint32_t gm = (uint32_t)gmax[c];
     const uint32_t blk = planes_s + c * (uint32_t)(W * 4);
     const uint32_t L = CLAMP ? (off < TOP ? TOP - off : 0u) : TOP - off;
@@ -280,7 +281,7 @@ __device__ __forceinline__ void bv_test(const BvParams &p, uint32_t planes_s, co
 }
 
 template <int P, int G, bool CLAMP, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvParams p) {
+__global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) {
     constexpr int R = 32 * G;
     constexpr int W = G * P;
     constexpr uint32_t TOP = (1u << P) - 1u;
@@ -333,9 +334,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
                 const int o = u & 3, g = (u >> 2) % G, cq = (u >> 2) / G;
                 const int rb = 32 * g + 8 * o;
                 const uint8_t *xr = p.x + (row0 + rb) * (int64_t)p.D + 4 * cq;
+                WMH_DASSERT(u >= n_units || (4 * cq + 3 < p.D && g < G));
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
                     const bool ok = u < n_units && rb + i < nr;
+                    WMH_DASSERT(!ok || row0 + rb + i < p.n_rows);
                     wb[bi][i] = ok ? __ldg(reinterpret_cast<const uint32_t *>(xr + (int64_t)i * p.D)) : 0u;
                 }
             }
@@ -373,6 +376,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
                     pw[b] = bv_prmt(x, __shfl_xor_sync(am, x, 2), s2);
                 }
                 const int c = 4 * cq + o;
+                WMH_DASSERT(c < p.D && g < G);
                 uint32_t *dst = planes + (size_t)c * W;
 #pragma unroll
                 for (int b = 0; b < P; b++) dst[BvLayout<P, G>::idx(g, b)] = pw[b];
@@ -450,27 +454,26 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
         uint32_t j = jb;
         // draw words: lane holds t = tb + lane (A) and tb + 32 + lane (B) of the
         // current round, the next round's pair, and the next hash's first pair
-        uint32_t na = 0, nb = 0, nc = 0, nd = 0;      // the next hash's rounds 0 and 1
+        // draw words: lane holds the pair t = tb + 2 lane, tb + 2 lane + 1 of the
+        // current round (one 8-byte load), the next round's pair, and the next
+        // hash's first two rounds
+        uint2 na = make_uint2(0u, 0u), nc = na;
         if (j < j1) {
-            const uint32_t *t0 = p.table + (int64_t)j * T0;
+            WMH_DASSERT(j < p.k);
+            const uint2 *t0 = reinterpret_cast<const uint2 *>(p.table + (int64_t)j * T0);
             na = __ldg(t0 + lane);
-            nb = __ldg(t0 + 32 + lane);
-            nc = __ldg(t0 + 64 + lane);
-            nd = __ldg(t0 + 96 + lane);
+            nc = __ldg(t0 + 32 + lane);
         }
         while (j < j1) {
             const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
             uint16_t *hres = hres_blk + (j - jb) * R;
-            const uint32_t *tj = p.table + (int64_t)j * T0;
+            const uint2 *tj = reinterpret_cast<const uint2 *>(p.table + (int64_t)j * T0);
             const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
-            uint32_t wA = na, wB = nb;
-            uint32_t xA = nc, xB = nd;                 // the next round's words
+            uint2 wc = na, wx = nc;                    // this round's pair, the next round's
             if (jn < j1) {                             // one hash ahead: its rounds 0 and 1
-                const uint32_t *tn = p.table + (int64_t)jn * T0;
+                const uint2 *tn = reinterpret_cast<const uint2 *>(p.table + (int64_t)jn * T0);
                 na = __ldg(tn + lane);
-                nb = __ldg(tn + 32 + lane);
-                nc = __ldg(tn + 64 + lane);
-                nd = __ldg(tn + 96 + lane);
+                nc = __ldg(tn + 32 + lane);
             }
             // all-zero rows: cap at once (lane = row)
 #pragma unroll
@@ -494,42 +497,41 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
                     }
                     break;
                 }
-                uint32_t w0 = wA, w1 = wB;
+                uint2 w = wc;
                 if (tb >= (uint32_t)T0) {              // beyond the table (rare): draw them here
-                    const uint32_t t0 = tb + lane;
-                    w0 = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t0), p.M), p.pack, p.uni_m, t0, p.cap);
-                    w1 = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)(t0 + 32)), p.M), p.pack, p.uni_m, t0 + 32, p.cap);
+                    const uint32_t t0 = tb + 2 * lane;
+                    w.x = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t0), p.M), p.pack, p.uni_m, t0, p.cap);
+                    w.y = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)(t0 + 1)), p.M), p.pack, p.uni_m, t0 + 1, p.cap);
                 }
                 // prefetch the round after next from the table (T0 draws per hash)
-                wA = xA;
-                wB = xB;
-                if (tb + 128 < (uint32_t)T0) {
-                    xA = __ldg(tj + tb + 128 + lane);
-                    xB = __ldg(tj + tb + 160 + lane);
-                }
+                wc = wx;
+                if (tb + 128 < (uint32_t)T0) wx = __ldg(tj + (tb + 128) / 2 + lane);
                 uint32_t mA[G], mB[G];
-                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w0, pend, mA);
-                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w1, pend, mB);
-                // ---- a8: the first green draw of each pending row.  Rows green among
-                //      the first 32 draws (RA) keep those; the others take the second
-                //      32; one transpose per group then gives lane = row its draws
-                uint32_t RA[G], Rall[G], u[G], anyR = 0u;
+                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w.x, pend, mA);
+                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w.y, pend, mB);
+                // ---- a8: the first green draw of each pending row.  Lane i tested
+                //      draws tb + 2i and tb + 2i + 1; one transpose of their union per
+                //      group gives lane = row the first lane i with a green, and that
+                //      lane's even-draw mask (a shuffle) says which of its two draws
+                uint32_t a[G], u[G], anyu = 0u;
 #pragma unroll
-                for (int g = 0; g < G; g++) {                 // all groups' reductions in flight together
-                    const uint32_t a = mA[g] & pend[g], bq = mB[g] & pend[g];
-                    RA[g] = __reduce_or_sync(0xFFFFFFFFu, a);
-                    Rall[g] = RA[g] | __reduce_or_sync(0xFFFFFFFFu, bq);
-                    u[g] = a | (bq & ~RA[g]);
-                    anyR |= Rall[g];
+                for (int g = 0; g < G; g++) {
+                    a[g] = mA[g] & pend[g];
+                    u[g] = a[g] | (mB[g] & pend[g]);
+                    anyu |= u[g];
                 }
-                if (anyR) {                                   // warp-uniform; the G transposes interleave
+                if (__any_sync(0xFFFFFFFFu, anyu != 0u)) {    // the G transposes interleave
                     uint32_t wt[G];
 #pragma unroll
-                    for (int g = 0; g < G; g++) wt[g] = tr(u[g]);   // bit i: draw (tb or tb+32) + i green for row lane
+                    for (int g = 0; g < G; g++) wt[g] = tr(u[g]);   // bit i: draw tb + 2i or + 2i + 1 green for row lane
 #pragma unroll
                     for (int g = 0; g < G; g++) {
-                        if (wt[g]) hres[32 * g + lane] = (uint16_t)(tb + (((RA[g] >> lane) & 1u) ? 0u : 32u) + (uint32_t)__ffs(wt[g]));
-                        pend[g] &= ~Rall[g];
+                        const int i = __ffs(wt[g]) - 1;                  // first lane (pair) with a green for this row
+                        const uint32_t ai = __shfl_sync(0xFFFFFFFFu, a[g], i & 31);
+                        const uint32_t odd = ((ai >> lane) & 1u) ^ 1u;    // 0: the pair's first draw was green
+                        WMH_DASSERT(j - jb < (uint32_t)BV_HB);
+                        if (wt[g]) hres[32 * g + lane] = (uint16_t)(tb + 2u * (uint32_t)i + odd + 1u);
+                        pend[g] &= ~__ballot_sync(0xFFFFFFFFu, wt[g] != 0u);
                     }
                 }
             }
@@ -541,6 +543,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) hash_bitslice_kernel(const BvPar
                 if (nh == BV_HB && p.vec_flush) {
                     for (int r = lane; r < nr; r += 32) {
                         const int64_t e = eoff + (int64_t)(r - lane) * p.k;
+                        WMH_DASSERT(e + BV_HB <= p.n_rows * (int64_t)p.k && r < R);
                         uint32_t hv[BV_HB];
 #pragma unroll
                         for (int u = 0; u < BV_HB; u++) hv[u] = hres_blk[u * R + r];
@@ -599,15 +602,10 @@ static void bv_launch(const BvParams &p, size_t smem, int grid, cudaStream_t s) 
 
 template <int P, bool CLAMP>
 static void bv_launch_g(int G, int NT, const BvParams &p, size_t smem, int grid, cudaStream_t s) {
-    if (NT == 256) {
-        if (G == 4) bv_launch<P, 4, CLAMP, 256>(p, smem, grid, s);
-        else if (G == 2) bv_launch<P, 2, CLAMP, 256>(p, smem, grid, s);
-        else bv_launch<P, 1, CLAMP, 256>(p, smem, grid, s);
-    } else {
-        if (G == 4) bv_launch<P, 4, CLAMP, 512>(p, smem, grid, s);
-        else if (G == 2) bv_launch<P, 2, CLAMP, 512>(p, smem, grid, s);
-        else bv_launch<P, 1, CLAMP, 512>(p, smem, grid, s);
-    }
+    (void)NT;                                    // 512 threads (measured: 768 at <= 85 registers spills, 13.3 vs 11.9 ms)
+    if (G == 4) bv_launch<P, 4, CLAMP, 512>(p, smem, grid, s);
+    else if (G == 2) bv_launch<P, 2, CLAMP, 512>(p, smem, grid, s);
+    else bv_launch<P, 1, CLAMP, 512>(p, smem, grid, s);
 }
 
 template <int P>
@@ -645,14 +643,14 @@ static BvShape bv_shape(const HashArgs &a) {
     const int NB = 32 - __builtin_clz(a.L->max_bound);
     int dev = 0;
     cudaGetDevice(&dev);
-    int smem_optin = 0, smem_sm = 0;
+    int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     static const int g_env = getenv("WMH_BV_GROUPS") ? atoi(getenv("WMH_BV_GROUPS")) : 0;
-    static const int c_env = getenv("WMH_BV_CTAS") ? atoi(getenv("WMH_BV_CTAS")) : 1;
     const int gmax_try = (g_env == 1 || g_env == 2 || g_env == 4) ? g_env : 4;
-    const int ctas = c_env == 2 ? 2 : 1, NT = 512 / ctas;
-    const size_t budget = std::min((size_t)smem_optin, (size_t)smem_sm / ctas - 1024) - 64;
+    // one 512-thread CTA per SM: the planes fill shared memory (measured: two
+    // 256-thread CTAs with one group each 15.5 vs 14.1 ms; 768 threads 13.3 vs 11.9)
+    const int ctas = 1, NT = 512;
+    const size_t budget = (size_t)smem_optin - 64;
     for (int G = gmax_try; G >= 1; G /= 2) {
         if (bv_smem(D, G, NB, NT) <= budget) return {NB, G, false, NT, ctas};
         // one plane fewer (clamped) when it buys this group count

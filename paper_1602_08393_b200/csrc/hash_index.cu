@@ -535,6 +535,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++)
                     if (len[q]) {
+                        WMH_DASSERT(slot < (uint32_t)CAPR);
                         ra[slot] = a[q] - f;
                         rp[slot] = f;
                         slot++;
@@ -577,7 +578,10 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                             v[u] = base + 32u * u + lane < lim ? __ldg(p.vals + addr[u]) : IX_NONE;
 #pragma unroll
                         for (int u = 0; u < IX_U; u++)
-                            if (v[u] != IX_NONE) atomicMin(h + (v[u] >> 16), v[u] & 0xFFFFu);
+                            if (v[u] != IX_NONE) {
+                                WMH_DASSERT((v[u] >> 16) < p.k);
+                                atomicMin(h + (v[u] >> 16), v[u] & 0xFFFFu);
+                            }
                         base += 32u * IX_U;
                     }
                 }

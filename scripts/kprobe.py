@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--tile", default="auto")
     ap.add_argument("--algo", default="auto")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--isgreen", default="table", choices=["table", "bsearch"])
     a = ap.parse_args()
     import datagen
     import paper_1602_08393_b200 as wmh
@@ -44,9 +45,10 @@ def main():
         out = torch.empty((rows.n_rows, k), dtype=torch.uint16, device="cuda")
         ms = []
         for i in range(a.reps + 1):
-            wmh.hash(layout, rows, cfg.seed, k, cfg.cap, 2, algo=a.algo, out=out, tile=a.tile, time_kernel=True)
+            wmh.hash(layout, rows, cfg.seed, k, cfg.cap, 2, algo=a.algo, out=out, tile=a.tile, time_kernel=True,
+                     isgreen=a.isgreen)
             ms.append(wmh.last_kernel_ms())
-        print(f"{a.config} rows={rows.n_rows} k={k} tile={a.tile} algo={wmh.last_algo}: "
+        print(f"{a.config} rows={rows.n_rows} k={k} tile={a.tile} algo={wmh.last_algo} isgreen={a.isgreen}: "
               f"{statistics.median(ms[1:]):.3f} ms (kernel)", flush=True)
 
 
