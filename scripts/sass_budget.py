@@ -119,7 +119,7 @@ def bitslice_regions():
             ("cap (cold)", lambda c: c[0] == fname and cap0 <= c[1] <= cap1),
             ("test (2 draws x G groups: decode, L masks, column-max skip, plane loads, carry chains)",
              lambda c: c[0] == fname and c[1] in test_lines),
-            ("combine (REDUX, 32x32 transpose, first green, record)",
+            ("combine (32x32 transpose, first green by a pair shuffle, record)",
              lambda c: (c[0] == fname and c[1] in comb_lines) or c[0].startswith("sm_")),
             ("loop control + prefetch", lambda c: True),
         ],
