@@ -135,7 +135,8 @@ def host_cores():
 def expected_draws(x_sum: np.ndarray, M: int, k: int, cap: int) -> float:
     """sum_n k * E_n with E_n = (1 - (1 - s_n)^cap) / s_n (Theorem 2 capped, reading R9)."""
     s = x_sum.astype(np.float64) / M
-    e = np.where(s > 0, -np.expm1(cap * np.log1p(-np.minimum(s, 1 - 1e-300))) / np.maximum(s, 1e-300), cap)
+    with np.errstate(divide="ignore"):                       # s = 1: log(0); that row needs one draw
+        e = np.where(s > 0, -np.expm1(cap * np.log1p(-np.minimum(s, 1 - 1e-300))) / np.maximum(s, 1e-300), cap)
     e = np.where(s >= 1, 1.0, e)
     return float(k * e.sum())
 
@@ -677,11 +678,26 @@ def roofline_index(x_sum, nnz, M, cfg, T, kern_s, in_bytes, out_bytes, peaks, dr
     hbm = peaks.get("hbm_gbs", 6650.0)
     gbs = algo_bytes / kern_s / 1e9
     issue = n_sm * 4 * 32 * sm_mhz * 1e6
-    return {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
-            "kernel": "index", "peak_source": "MEASURED_PEAKS hbm_gbs (copy)",
-            "algo_bytes": algo_bytes, "entries_visited": entries, "horizon": int(T),
-            "frac_vs_paper_loop": draws / kern_s / 1e9 / (issue / I_DRAW["simple"] / 1e9),
-            "t_kernel_ms": kern_s * 1e3}
+    # the issue floor of the entry walk: lane-instructions per visited entry from SASS
+    try:
+        per_entry = json.load(open(os.path.join(ROOT, "profiles", "r2_sass_index.json")))["lane_instr_per_unit"]
+    except (OSError, ValueError, KeyError):
+        per_entry = None
+    t_hbm = algo_bytes / (hbm * 1e9)
+    t_issue = entries * per_entry / issue if per_entry else 0.0
+    out = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
+           "kernel": "index", "peak_source": "MEASURED_PEAKS hbm_gbs (copy)",
+           "algo_bytes": algo_bytes, "entries_visited": entries, "horizon": int(T),
+           "t_hbm_floor_ms": t_hbm * 1e3, "t_issue_floor_ms": t_issue * 1e3,
+           "issue_floor_source": f"{per_entry} lane-instr per visited entry (profiles/r2_sass_index.json)",
+           "frac_vs_paper_loop": draws / kern_s / 1e9 / (issue / I_DRAW["simple"] / 1e9),
+           "t_kernel_ms": kern_s * 1e3}
+    if t_issue > t_hbm:              # the walk's instructions bind, not the bytes
+        out.update({"bound": "alu", "achieved": entries / kern_s / 1e9, "peak": issue / per_entry / 1e9,
+                    "unit": "Gentries/s", "frac": t_issue / kern_s,
+                    "peak_source": f"{n_sm} SMs x 128 lanes x {sm_mhz:.0f} MHz / {per_entry:.2f} lane-instr per "
+                                   "visited entry (SASS, profiles/r2_sass_index.json)"})
+    return out
 
 
 def measure_e2e(wmh, layout, data, cfg, n, args, dev, world, dist, xd=None):

@@ -7,6 +7,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libwmh_debug.so" if os.environ.get("WMH_LIB") == "debug" else "libwmh.so")
+if os.environ.get("WMH_LIB_AB"):          # A/B experiments: another build of the library (scripts only)
+    SO_PATH = os.path.join(_HERE, os.environ["WMH_LIB_AB"])
 
 WMH_OK, WMH_EINVAL, WMH_EBOUND, WMH_EEMPTY, WMH_EOVERFLOW, WMH_ECUDA, WMH_ENOMEM = range(7)
 WMH_DENSE, WMH_CSR = 0, 1

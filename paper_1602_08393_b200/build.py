@@ -77,8 +77,10 @@ def _build(verbose: bool) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = SO + f".tmp{os.getpid()}"
+    # the shared CUDA runtime (the process's libcudart.so.12 -- torch's when torch is
+    # loaded -- instead of a static copy inside libwmh.so); rpath for standalone use
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-           "-o", tmp, *objs]
+           "-cudart", "shared", "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

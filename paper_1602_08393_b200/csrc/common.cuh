@@ -21,6 +21,7 @@ struct wmh_layout {
     uint32_t *cell_pack = nullptr;    // [M]         (c << 8) | (t - CompToM[c]): Alg. 5 in one load (not wide)
     uint64_t rowsum_q = 0;            // 0.1% quantile (power of two) of prepare's nonzero row sums; 0 = unknown
     double mean_s = -1.0;             // mean effective sparsity |x|_1 / M of prepare's rows (Eq. 17); < 0 = unknown
+    uint64_t clamp_cells[8] = {0};    // sum_c max(0, m_c - (2^b - 1)), b = 0..7 (the plane tiles' clamp choice)
     int device = 0;
 };
 

@@ -537,12 +537,8 @@ wmh_status launch_hash_tiled_bs(const HashArgs &a, bool *handled) {
     int NBP = NB;                                // planes stored and tested
     bool clamp = false;
     if (G < 2 && NB >= 5 && bs_smem(D, 2, NB - 1) <= (size_t)smem_optin) {
-        std::vector<uint32_t> hb((size_t)D);
-        WMH_CUDA_TRY(cudaMemcpyAsync(hb.data(), a.L->bounds, sizeof(uint32_t) * D, cudaMemcpyDeviceToHost, a.stream), "bounds D2H");
-        WMH_CUDA_TRY(cudaStreamSynchronize(a.stream), "bounds D2H sync");
-        const uint32_t top = (1u << (NB - 1)) - 1u;
-        uint64_t flagged = 0;
-        for (uint32_t m : hb) flagged += m > top ? m - top : 0u;
+        // cells above the clamp, counted once by wmh_prepare (no device round trip here)
+        const uint64_t flagged = a.L->clamp_cells[NB - 1];
         static const double max_frac = getenv("WMH_BS_CLAMP_FRAC") ? atof(getenv("WMH_BS_CLAMP_FRAC")) : 1e-3;
         if ((double)flagged <= max_frac * (double)a.L->M) { NBP = NB - 1; NBS = -NBP; G = 2; clamp = true; }
     }

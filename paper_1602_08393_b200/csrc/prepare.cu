@@ -132,6 +132,24 @@ __global__ void check_csr(const int64_t *__restrict__ row_ptr, const int32_t *__
     }
 }
 
+// Cells above 2^b - 1 in every column, b = 0..7: sum_c max(0, m_c - (2^b - 1)) --
+// how many cells a tile whose planes clamp at b bits cannot test (the bit-plane
+// tiles' clamp decision, read on the host without a device round trip)
+__global__ void clamp_counts(const uint32_t *__restrict__ m, int64_t dim, unsigned long long *__restrict__ counts) {
+    unsigned long long loc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < dim; c += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = m[c];
+#pragma unroll
+        for (int b = 0; b < 8; b++) loc[b] += v > (1u << b) - 1u ? v - ((1u << b) - 1u) : 0u;
+    }
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        unsigned long long a = loc[b];
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        if ((threadIdx.x & 31) == 0 && a) atomicAdd(counts + b, a);
+    }
+}
+
 // ------------------------------------------------------- a3: prefix sums
 constexpr int SCAN_B = 1024;
 
@@ -355,16 +373,16 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
         return fail(cuda_fail(cudaGetLastError(), "copy bounds"));
 
     const int64_t nb = (dim + SCAN_B - 1) / SCAN_B;
-    // scratch: sums[nb], M, first_bad, mn, mx, colmax[dim] (dense validation)
+    // scratch: sums[nb], M, first_bad, mn, mx, pad, the 8 clamp counts, colmax[dim] (dense validation)
     unsigned long long *scr = nullptr;
-    size_t scr_bytes = sizeof(unsigned long long) * (nb + 4) + sizeof(uint32_t) * dim;
+    size_t scr_bytes = sizeof(unsigned long long) * (nb + 12) + sizeof(uint32_t) * dim;
     if (cudaMallocAsync((void **)&scr, scr_bytes, s) != cudaSuccess) {
         set_error("wmh_prepare: scratch alloc failed");
         return fail(WMH_ENOMEM);
     }
     unsigned long long *sums = scr, *Mdev = scr + nb, *bad = scr + nb + 1;
     unsigned int *mnmx = reinterpret_cast<unsigned int *>(scr + nb + 2);
-    unsigned long long init[4] = {0ull, ~0ull, 0x00000000FFFFFFFFull, 0ull};  // M, bad, {mn=~0,mx=0}, pad
+    unsigned long long init[12] = {0ull, ~0ull, 0x00000000FFFFFFFFull, 0ull};  // M, bad, {mn=~0,mx=0}, pad, counts
     cudaMemcpyAsync(Mdev, init, sizeof(init), cudaMemcpyHostToDevice, s);
 
     const int sms = num_sms();
@@ -372,7 +390,7 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
         if (rows->kind == WMH_DENSE) {
             // fast path: column maxima (one HBM pass) against the bounds; the
             // exact first offender is located only when a column fails
-            uint32_t *cm = reinterpret_cast<uint32_t *>(scr + nb + 4);
+            uint32_t *cm = reinterpret_cast<uint32_t *>(scr + nb + 12);
             wmh_status cst = wmh_colmax(rows, cm, stream);
             if (cst != WMH_OK) { cudaFreeAsync(scr, s); return fail(cst); }
             colmax_exceeds<<<(unsigned)((dim + 255) / 256), 256, 0, s>>>(cm, L->bounds, dim, bad);
@@ -403,10 +421,11 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     scan_block_sums<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, mnmx, mnmx + 1);
     scan_sums_single<<<1, SCAN_B, 0, s>>>(sums, nb, Mdev);
     scan_apply<<<(unsigned)nb, SCAN_B, 0, s>>>(L->bounds, dim, sums, Mdev, L->comp_to_m);
-    count_launch(3 + ((rows && rows->n_rows > 0) ? 1 : 0));
+    clamp_counts<<<(unsigned)std::min<int64_t>(sms * 4, (dim + 255) / 256), 256, 0, s>>>(L->bounds, dim, Mdev + 4);
+    count_launch(4 + ((rows && rows->n_rows > 0) ? 1 : 0));
     if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(scr, s); return fail(cuda_fail(cudaGetLastError(), "prepare scan launch")); }
 
-    unsigned long long host[4];
+    unsigned long long host[12];
     cudaError_t e1 = cudaMemcpyAsync(host, Mdev, sizeof(host), cudaMemcpyDeviceToHost, s);
     cudaError_t e2 = cudaStreamSynchronize(s);
     cudaFreeAsync(scr, s);
@@ -457,6 +476,7 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     L->M = M;
     if (mn == mx) { L->flags |= WMH_LAYOUT_UNIFORM; L->uniform_m = mx; }
     L->max_bound = (uint32_t)mx;
+    for (int b = 0; b < 8; b++) L->clamp_cells[b] = host[4 + b];
     if (mx > 255) L->flags |= WMH_LAYOUT_WIDE;       // 8-bit cell offsets no longer fit: no cell_pack
 
     if (cudaMalloc(&L->int_to_comp, sizeof(uint32_t) * M) != cudaSuccess ||

@@ -178,9 +178,9 @@ def main():
                                os.path.join(ROOT, "profiles", "r2_sass_cm"), extra_lines=["const uint4 q4 = e4[i4];"],
                                unit_prefix=False)
     if a.which == "index":         # the INDEX rows kernel's entry walk: one global load of a filed draw per entry
-        return per_unit_budget("hash_index.cu", ["hash_index_kernel", "ILi2ELb1ELi2E"], "hash_index.cu",
-                               "for (uint32_t w = w0; w < w1; w += IX_U) {",
-                               "if (v[u] != IX_NONE) atomicMin(h + (v[u] >> 16), v[u] & 0xFFFFu);",
+        return per_unit_budget("hash_index.cu", ["hash_index_kernel", "ILi2ELb1ELi2EhE"], "hash_index.cu",
+                               "v[u] = base + 32u * u + lane < lim ? __ldg(p.vals + addr[u]) : IX_NONE;",
+                               "atomicMin(h + (v[u] >> 16), v[u] & 0xFFFFu);",
                                "LDG", "visited entry (filed draw) per lane",
                                os.path.join(ROOT, "profiles", "r2_sass_index"), loop=True)
     if a.which == "simple":        # the paper's loop: one cell load per draw

@@ -34,7 +34,7 @@ def test_splitmix64_published_known_answer():
     """Reading R6: the mixer is the standard SplitMix64 output function."""
     for line in _read("splitmix64_known.txt"):
         v, want = line.split()
-        assert oracle.splitmix64(int(v)) == int(want, 16)
+        assert oracle.splitmix64(int(v, 0)) == int(want, 16)
 
 
 def test_draws_match_independent_survey_values():
