@@ -43,7 +43,7 @@
 namespace wmh {
 
 constexpr int BV_HB = 8;                  // hashes per claimed block (results flushed 8 per row)
-constexpr int BV_SB = 2;                  // staging units per thread whose loads are in flight together
+constexpr int BV_SB = 1;                  // staging units (quad pairs) per thread whose loads are in flight together
 
 struct BvParams {
     const uint8_t *x;
@@ -326,30 +326,36 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
         //      (quad, group) combine their column maxima with two shuffles.
         //      BV_SB units per batch: all their loads are issued before any is
         //      used (one memory round trip per batch, not per unit)
-        const int n_units = quads * G * 4;
-        auto stage_load = [&](int u0, uint32_t (&wb)[BV_SB][8]) {
+        // unit = (column-quad pair, group, octet): one 8-byte load per row covers
+        // both quads (full 32-byte sectors across the warp), processed as two quads
+        const int n_units = (quads / 2) * G * 4;
+        auto stage_load = [&](int u0, uint32_t (&wb)[BV_SB][2][8]) {
 #pragma unroll
             for (int bi = 0; bi < BV_SB; bi++) {
                 const int u = u0 + bi * NT;
-                const int o = u & 3, g = (u >> 2) % G, cq = (u >> 2) / G;
+                const int o = u & 3, g = (u >> 2) % G, cqp = (u >> 2) / G;
                 const int rb = 32 * g + 8 * o;
-                const uint8_t *xr = p.x + (row0 + rb) * (int64_t)p.D + 4 * cq;
-                WMH_DASSERT(u >= n_units || (4 * cq + 3 < p.D && g < G));
+                const uint8_t *xr = p.x + (row0 + rb) * (int64_t)p.D + 8 * cqp;
+                WMH_DASSERT(u >= n_units || (8 * cqp + 7 < p.D && g < G));
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
                     const bool ok = u < n_units && rb + i < nr;
                     WMH_DASSERT(!ok || row0 + rb + i < p.n_rows);
-                    wb[bi][i] = ok ? __ldg(reinterpret_cast<const uint32_t *>(xr + (int64_t)i * p.D)) : 0u;
+                    const uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(xr + (int64_t)i * p.D)) : make_uint2(0u, 0u);
+                    wb[bi][0][i] = v.x;
+                    wb[bi][1][i] = v.y;
                 }
             }
         };
-        auto stage_proc = [&](int u0, uint32_t (&wb)[BV_SB][8]) {
+        auto stage_proc = [&](int u0, uint32_t (&wb)[BV_SB][2][8]) {
 #pragma unroll
             for (int bi = 0; bi < BV_SB; bi++) {
+#pragma unroll
+            for (int qq = 0; qq < 2; qq++) {
                 const int u = u0 + bi * NT;
                 if (u >= n_units) break;                 // uniform over the 4 octet lanes of a unit
-                const int o = u & 3, g = (u >> 2) % G, cq = (u >> 2) / G;
-                uint32_t *w = wb[bi];
+                const int o = u & 3, g = (u >> 2) % G, cq = 2 * ((u >> 2) / G) + qq;
+                uint32_t *w = wb[bi][qq];
                 if (CLAMP) {
 #pragma unroll
                     for (int i = 0; i < 8; i++) w[i] = __vminu4(w[i], TOP * 0x01010101u);
@@ -400,11 +406,12 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                     if (lane == first && lv) atomicOr(&s_live[gg], lv);
                 }
             }
+            }
         };
         // two batches of BV_SB units in flight: the next batch's loads are issued
         // before the current one is transposed
         {
-            uint32_t bufA[BV_SB][8], bufB[BV_SB][8];
+            uint32_t bufA[BV_SB][2][8], bufB[BV_SB][2][8];
             int u0 = threadIdx.x;
             stage_load(u0, bufA);
             for (; u0 < n_units; u0 += 2 * BV_SB * NT) {
@@ -661,7 +668,7 @@ static BvShape bv_shape(const HashArgs &a) {
 
 bool bitslice_handles(const HashArgs &a) {
     const int D = (int)a.rows.dim;
-    if (a.rows.kind != WMH_DENSE || (D & 3) || ((uintptr_t)a.rows.dense & 3)) return false;
+    if (a.rows.kind != WMH_DENSE || (D & 7) || ((uintptr_t)a.rows.dense & 7)) return false;
     if ((a.L->flags & WMH_LAYOUT_WIDE) || weight_bytes(a.rows) != 1 || a.L->max_bound == 0 || a.L->max_bound > 255) return false;
     if ((uint64_t)D >= (1ull << 24)) return false;
     return bv_shape(a).G >= 1;
