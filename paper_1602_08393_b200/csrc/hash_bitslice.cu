@@ -658,6 +658,12 @@ static BvShape bv_shape(const HashArgs &a) {
     // 256-thread CTAs with one group each 15.5 vs 14.1 ms; 768 threads 13.3 vs 11.9)
     const int ctas = 1, NT = 512;
     const size_t budget = (size_t)smem_optin - 64;
+    // WMH_BV_PLANES=P (4 <= P < NB): clamp to P planes whenever they fit two groups
+    static const int p_env = getenv("WMH_BV_PLANES") ? atoi(getenv("WMH_BV_PLANES")) : 0;
+    if (p_env >= 4 && p_env < NB && p_env < 8) {
+        for (int G = gmax_try; G >= 1; G /= 2)
+            if (bv_smem(D, G, p_env, NT) <= budget) return {p_env, G, true, NT, ctas};
+    }
     for (int G = gmax_try; G >= 1; G /= 2) {
         if (bv_smem(D, G, NB, NT) <= budget) return {NB, G, false, NT, ctas};
         // one plane fewer (clamped) when it buys this group count
