@@ -69,6 +69,8 @@ def lib() -> ctypes.CDLL:
                 "oracle_total_M": (c_int, [u32p, i64, u64p]),
                 "oracle_build_layout": (c_int, [u32p, i64, u32p, u32p]),
                 "oracle_check_bounds_dense": (c_int, [u8p, i64, i64, u32p, i64p, i64p]),
+                "oracle_check_bounds_csr": (c_int, [i64p, i32p, u8p, i64, i64, i64, u32p, i64p,
+                                                    ctypes.POINTER(c_int)]),
                 "oracle_is_green_o1": (c_int, [u32p, u32p, u8p, u32]),
                 "oracle_is_green_binsearch": (c_int, [u32p, i32p, u8p, i64, u32]),
                 "oracle_is_green_direct": (c_int, [u32p, u8p, i64, u32]),
@@ -181,6 +183,18 @@ class Layout:
         rc = lib().oracle_check_bounds_dense(_p(x, ctypes.c_uint8), x.shape[0], x.shape[1],
                                              _p(self.m, ctypes.c_uint32), ctypes.byref(br), ctypes.byref(bc))
         return None if rc == OK else (br.value, bc.value)
+
+    def check_bounds_csr(self, row_ptr, col, val):
+        """None, or (index of the first offending nonzero -- of the row for a
+        malformed row_ptr --, reason 1 column range, 2 order, 3 bound, 4 row_ptr)."""
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        c = np.ascontiguousarray(col, np.int32)
+        v = _u8(val)
+        bi, why = ctypes.c_int64(-1), ctypes.c_int(0)
+        rc = lib().oracle_check_bounds_csr(_p(rp, ctypes.c_int64), _p(c, ctypes.c_int32), _p(v, ctypes.c_uint8),
+                                           len(rp) - 1, self.dim, len(c), _p(self.m, ctypes.c_uint32),
+                                           ctypes.byref(bi), ctypes.byref(why))
+        return None if rc == OK else (bi.value, why.value)
 
     # ISGREEN variants
     def is_green_o1(self, x_dense, r: int) -> bool:

@@ -135,6 +135,29 @@ int oracle_check_bounds_dense(const uint8_t *x, int64_t n_rows, int64_t dim, con
     return ORC_OK;
 }
 
+/* The same for CSR rows, with the structure the method relies on: row_ptr
+ * non-decreasing from 0 to nnz, columns in [0, dim) and strictly ascending
+ * within a row, every value within its bound.  Returns the first offending
+ * nonzero (its index; for a malformed row_ptr, the row) and why:
+ * 1 column out of range, 2 columns not ascending, 3 value above its bound,
+ * 4 row_ptr malformed. */
+int oracle_check_bounds_csr(const int64_t *row_ptr, const int32_t *col, const uint8_t *val, int64_t n_rows,
+                            int64_t dim, int64_t nnz, const uint32_t *m, int64_t *bad_index, int *why)
+{
+    for (int64_t n = 0; n < n_rows; n++) {
+        int64_t a = row_ptr[n], b = row_ptr[n + 1];
+        if (a > b || a < 0 || b > nnz || (n == 0 && a != 0) || (n == n_rows - 1 && b != nnz)) {
+            *bad_index = n; *why = 4; return ORC_EINVAL;
+        }
+        for (int64_t e = a; e < b; e++) {
+            if (col[e] < 0 || col[e] >= dim) { *bad_index = e; *why = 1; return ORC_EINVAL; }
+            if (e > a && col[e - 1] >= col[e]) { *bad_index = e; *why = 2; return ORC_EINVAL; }
+            if (val[e] > m[col[e]]) { *bad_index = e; *why = 3; return ORC_EBOUND; }
+        }
+    }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* ISGREEN: Alg. 5 and the Sec. 3.3 binary search       */
 /* ------------------------------------------------------------------------ */

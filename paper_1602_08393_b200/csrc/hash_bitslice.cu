@@ -455,6 +455,9 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
             pend0[g] = s_live[g] & valid;
             dead[g] = valid & ~s_live[g];
         }
+        bool any_dead = false;
+#pragma unroll
+        for (int g = 0; g < G; g++) any_dead |= dead[g] != 0u;
         uint32_t jb = grab();                          // current block [jb, je)
         uint32_t je = min(j1, jb + BV_HB);
         uint32_t jb_next = jb < j1 ? grab() : j1;
@@ -475,18 +478,19 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
             const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
             uint16_t *hres = hres_blk + (j - jb) * R;
             const uint2 *tj = reinterpret_cast<const uint2 *>(p.table + (int64_t)j * T0);
-            const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
             uint2 wc = na, wx = nc;                    // this round's pair, the next round's
             if (jn < j1) {                             // one hash ahead: its rounds 0 and 1
                 const uint2 *tn = reinterpret_cast<const uint2 *>(p.table + (int64_t)jn * T0);
                 na = __ldg(tn + lane);
                 nc = __ldg(tn + 32 + lane);
             }
-            // all-zero rows: cap at once (lane = row)
+            // all-zero rows: cap at once (lane = row); a tile without them skips this
+            if (any_dead) {
 #pragma unroll
-            for (int g = 0; g < G; g++) {
-                if ((dead[g] >> lane) & 1u) hres[32 * g + lane] = (uint16_t)p.cap;
-                sat += (lane == 0) ? __popc(dead[g]) : 0;
+                for (int g = 0; g < G; g++) {
+                    if ((dead[g] >> lane) & 1u) hres[32 * g + lane] = (uint16_t)p.cap;
+                    sat += (lane == 0) ? __popc(dead[g]) : 0;
+                }
             }
             uint32_t pend[G];
 #pragma unroll
@@ -506,6 +510,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 }
                 uint2 w = wc;
                 if (tb >= (uint32_t)T0) {              // beyond the table (rare): draw them here
+                    const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
                     const uint32_t t0 = tb + 2 * lane;
                     w.x = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t0), p.M), p.pack, p.uni_m, t0, p.cap);
                     w.y = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)(t0 + 1)), p.M), p.pack, p.uni_m, t0 + 1, p.cap);

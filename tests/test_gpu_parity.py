@@ -572,3 +572,38 @@ def test_sharding_invariance(wmh, name, n, k):
             layout = wmh.prepare(s, bounds=bounds.view(torch.int32))
             parts.append(wmh.hash(layout, s, cfg.seed, k, cfg.cap, cfg.sig_bytes).view(torch.int16).cpu())
         assert torch.equal(torch.cat(parts), ref), G
+
+
+def test_check_rows_and_validate_against_oracle(wmh):
+    """wmh_check_rows / hash(validate=True): rows a layout did not see
+    are checked against its bounds -- the same first offender as the oracle's
+    dense and CSR checks, and no error on conforming rows (x_c <= m_c)."""
+    rng = np.random.default_rng(9)
+    x = rng.integers(0, 6, size=(300, 64)).astype(np.uint8)
+    bounds = np.full(64, 5, np.uint32)
+    layout = wmh.prepare(bounds=torch.from_numpy(bounds).cuda())
+    L = oracle.Layout(bounds)
+    rows = to_rows(datagen.Dense(x))
+    wmh.check_rows(layout, rows)                          # conforming
+    wmh.hash(layout, rows, 1, 16, 100, validate=True)
+    x2 = x.copy()
+    x2[123, 7] = 6
+    x2[200, 1] = 9
+    assert L.check_bounds_dense(x2) == (123, 7)
+    with pytest.raises(wmh.WmhError, match=r"x\[123\]\[7\]"):
+        wmh.check_rows(layout, to_rows(datagen.Dense(x2)))
+    with pytest.raises(wmh.WmhError, match="exceeds its bound"):
+        wmh.hash(layout, to_rows(datagen.Dense(x2)), 1, 16, 100, validate=True)
+    # CSR
+    rp = np.zeros(301, np.int64)
+    cols, vals = [], []
+    for n in range(300):
+        c = np.flatnonzero(x2[n])
+        cols.append(c.astype(np.int32))
+        vals.append(x2[n, c])
+        rp[n + 1] = rp[n] + len(c)
+    csr = datagen.CSR(rp, np.concatenate(cols), np.concatenate(vals).astype(np.uint8), 64)
+    want = L.check_bounds_csr(csr.row_ptr, csr.col, csr.val)
+    assert want is not None and want[1] == 3
+    with pytest.raises(wmh.WmhError, match=f"nonzero {want[0]}: value exceeds its bound"):
+        wmh.check_rows(layout, to_rows(csr))

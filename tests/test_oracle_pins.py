@@ -407,3 +407,18 @@ def test_colmax_and_bounds():
     assert L.check_bounds_dense(x) == (0, 1)
     L = oracle.Layout([3, 5, 1])
     assert L.check_bounds_dense(x) is None
+
+
+def test_csr_bounds_and_structure():
+    """The CSR twin of the bounds check (hand examples): x = [[1, 5, 0], [3, 2, 0]]
+    as CSR against bounds [3, 4, 1] fails at nonzero 1 (value 5 in column 1)."""
+    rp = np.array([0, 2, 4], np.int64)
+    col = np.array([0, 1, 0, 1], np.int32)
+    val = np.array([1, 5, 3, 2], np.uint8)
+    assert oracle.Layout([3, 4, 1]).check_bounds_csr(rp, col, val) == (1, 3)
+    L = oracle.Layout([3, 5, 1])
+    assert L.check_bounds_csr(rp, col, val) is None
+    assert L.check_bounds_csr(rp, np.array([0, 1, 1, 0], np.int32), val) == (3, 2)        # not ascending
+    assert L.check_bounds_csr(rp, np.array([0, 3, 0, 1], np.int32), val) == (1, 1)        # column >= dim
+    assert L.check_bounds_csr(np.array([0, 5, 4], np.int64), col, val) == (0, 4)          # row_ptr past nnz
+    assert L.check_bounds_csr(np.array([0, 2, 4, 4], np.int64), col, val) is None          # an empty last row
