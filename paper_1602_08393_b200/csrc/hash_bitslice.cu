@@ -217,7 +217,7 @@ using bv_gmax_t = typename std::conditional<G == 1, uint8_t, typename std::condi
 
 // CLAMP: the draw (c, off >= 2^P - 1) against the rows of group g whose clamped
 // value is all ones (cand), read from the rows in global memory
-__device__ __noinline__ uint32_t bv_slow(const uint8_t *x, int64_t grow0, int D, uint32_t c, uint32_t off, uint32_t cand) {
+__device__ __forceinline__ uint32_t bv_slow(const uint8_t *x, int64_t grow0, int D, uint32_t c, uint32_t off, uint32_t cand) {
     uint32_t m = 0;
     while (cand) {
         const int i = __ffs(cand) - 1;
@@ -230,15 +230,16 @@ __device__ __noinline__ uint32_t bv_slow(const uint8_t *x, int64_t grow0, int D,
 // Green masks of the draw word w against the G groups (pending groups only):
 // the L_b masks are built once per draw; a group whose column maximum is at or
 // below the offset is red without touching its planes (R2).
+// Branch-free, so the chains of both draws and all groups interleave.  CLAMP:
+// a draw with off >= 2^P - 1 gets L = 0 (all red here) and returns true when a
+// group needs the exact test on the candidate rows (bv_test_slow).
 template <int P, int G, bool CLAMP>
-__device__ __forceinline__ void bv_test(const BvParams &p, uint32_t planes_s, const bv_gmax_t<G> *gmax, int64_t row0,
-                                        uint32_t w, const uint32_t (&pend)[G], uint32_t (&mask)[G]) {
-    constexpr int W = G * P;
+__device__ __forceinline__ bool bv_test(uint32_t planes_s, const bv_gmax_t<G> *gmax, uint32_t w, const uint32_t (&pend)[G],
+                                        uint32_t (&mask)[G]) {
     constexpr uint32_t TOP = (1u << P) - 1u;
     const uint32_t c = w >> 8, off = w & 0xFFu;
-    WMH_DASSERT(c < (uint32_t)p.D);
     const uint32_t gm = (uint32_t)gmax[c];
-    const uint32_t blk = planes_s + c * (uint32_t)(W * 4);
+    const uint32_t blk = planes_s + c * (uint32_t)(G * P * 4);
     const uint32_t L = CLAMP ? (off < TOP ? TOP - off : 0u) : TOP - off;
     const uint32_t Xh = L * 0x08040201u, Xl = L * 0x80402010u;
     uint32_t m[P];
@@ -257,27 +258,33 @@ __device__ __forceinline__ void bv_test(const BvParams &p, uint32_t planes_s, co
             uint32_t xg[P];
             bv_load_group<P, G>(blk, g, need[g], xg);
             mask[g] = need[g] ? bv_chain<P>(xg, m) : 0u;
-            if (CLAMP && need[g] && off >= TOP) {
-                uint32_t cand = xg[0];
-#pragma unroll
-                for (int b = 1; b < P; b++) cand &= xg[b];
-                mask[g] = bv_slow(p.x, row0 + 32 * g, p.D, c, off, cand);
-            }
         }
     } else {
         uint32_t xa[G][P];
         bv_load_all<P, G>(blk, need_any, xa);
 #pragma unroll
-        for (int g = 0; g < G; g++) {
-            mask[g] = need[g] ? bv_chain<P>(xa[g], m) : 0u;   // branch-free: the two draws' tests interleave
-            if (CLAMP && need[g] && off >= TOP) {
-                uint32_t cand = xa[g][0];
-#pragma unroll
-                for (int b = 1; b < P; b++) cand &= xa[g][b];
-                mask[g] = bv_slow(p.x, row0 + 32 * g, p.D, c, off, cand);
-            }
-        }
+        for (int g = 0; g < G; g++) mask[g] = need[g] ? bv_chain<P>(xa[g], m) : 0u;
     }
+    return CLAMP && need_any && off >= TOP;
+}
+
+// CLAMP, off >= 2^P - 1: the draw against group g's rows whose clamped value
+// is all ones, read from the rows in global memory (rare: the top cells of the
+// few columns whose bound exceeds 2^P - 1)
+template <int P, int G>
+__device__ __noinline__ uint32_t bv_test_slow(const BvParams &p, uint32_t planes_s, const bv_gmax_t<G> *gmax, int64_t row0,
+                                              uint32_t w, uint32_t pend, int g) {
+    const uint32_t c = w >> 8, off = w & 0xFFu;
+    WMH_DASSERT(c < (uint32_t)p.D);
+    if (pend == 0u || off >= (((uint32_t)gmax[c] >> (8 * g)) & 0xFFu)) return 0u;
+    const uint32_t blk = planes_s + c * (uint32_t)(G * P * 4);
+    uint32_t cand = 0xFFFFFFFFu;
+    for (int b = 0; b < P; b++) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(blk + 4u * (uint32_t)BvLayout<P, G>::idx(g, b)));
+        cand &= v;
+    }
+    return bv_slow(p.x, row0 + 32 * g, p.D, c, off, cand);
 }
 
 template <int P, int G, bool CLAMP, int NT>
@@ -519,8 +526,15 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 wc = wx;
                 if (tb + 128 < (uint32_t)T0) wx = __ldg(tj + (tb + 128) / 2 + lane);
                 uint32_t mA[G], mB[G];
-                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w.x, pend, mA);
-                bv_test<P, G, CLAMP>(p, planes_s, gmax, row0, w.y, pend, mB);
+                const bool slowA = bv_test<P, G, CLAMP>(planes_s, gmax, w.x, pend, mA);
+                const bool slowB = bv_test<P, G, CLAMP>(planes_s, gmax, w.y, pend, mB);
+                if (CLAMP && (slowA || slowB)) {           // rare, divergent
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        if (slowA) mA[g] = bv_test_slow<P, G>(p, planes_s, gmax, row0, w.x, pend[g], g);
+                        if (slowB) mB[g] = bv_test_slow<P, G>(p, planes_s, gmax, row0, w.y, pend[g], g);
+                    }
+                }
                 // ---- a8: the first green draw of each pending row.  Lane i tested
                 //      draws tb + 2i and tb + 2i + 1; one transpose of their union per
                 //      group gives lane = row the first lane i with a green, and that

@@ -93,7 +93,7 @@ def bitslice_regions():
     f = os.path.join(CSRC, "hash_bitslice.cu")
     loop0 = line_of(f, "for (uint32_t tb = 0;; tb += 64) {")
     loop1 = block_end(f, loop0)
-    t0 = line_of(f, "__device__ __forceinline__ void bv_test(")
+    t0 = line_of(f, "__device__ __forceinline__ bool bv_test(")
     t1 = block_end(f, t0)
     chain0 = line_of(f, "__device__ __forceinline__ uint32_t bv_chain(")
     ld0 = line_of(f, "__device__ __forceinline__ void bv_load_group(")
@@ -106,6 +106,8 @@ def bitslice_regions():
     late1 = block_end(f, late0)
     cap0 = line_of(f, "if (tb >= p.cap) {", loop0)
     cap1 = block_end(f, cap0)
+    slow0 = line_of(f, "if (CLAMP && (slowA || slowB)) {", loop0)
+    slow1 = block_end(f, slow0)
     fname = "hash_bitslice.cu"
     test_lines = set(range(t0, t1 + 1)) | set(range(chain0, block_end(f, chain0) + 1)) | \
         set(range(ld0, block_end(f, ld0) + 1)) | set(range(la0, block_end(f, la0) + 1)) | \
@@ -117,6 +119,7 @@ def bitslice_regions():
         "regions": [
             ("late_draws (t >= T0, cold)", lambda c: c[0] == "common.cuh" or (c[0] == fname and late0 <= c[1] <= late1)),
             ("cap (cold)", lambda c: c[0] == fname and cap0 <= c[1] <= cap1),
+            ("clamped top cells (cold)", lambda c: c[0] == fname and slow0 <= c[1] <= slow1),
             ("test (2 draws x G groups: decode, L masks, column-max skip, plane loads, carry chains)",
              lambda c: c[0] == fname and c[1] in test_lines),
             ("combine (32x32 transpose, first green by a pair shuffle, record)",
