@@ -44,6 +44,10 @@ namespace wmh {
 
 constexpr int BV_HB = 8;                  // hashes per claimed block (results flushed 8 per row)
 constexpr int BV_SB = 1;                  // staging units (quad pairs) per thread whose loads are in flight together
+constexpr int BV_DPL = 3;                 // draws screened per lane per round
+constexpr int BV_RD = 32 * BV_DPL;        // draws per round
+constexpr int BV_T0 = 4 * BV_RD;          // draws per hash kept in the per-launch table (whole rounds)
+constexpr int BV_NT = 512;               // threads per CTA
 
 struct BvParams {
     const uint8_t *x;
@@ -54,7 +58,7 @@ struct BvParams {
     uint32_t k, cap, M, uni_m;
     uint64_t S;
     int vec_flush, sigb;
-    const uint32_t *table;       // [k][T0] draw words (c << 8) | off; 0xFF (never green) at t >= cap
+    const uint32_t *table;       // [k][BV_T0] draw words (c << 8) | off; 0xFF (never green) at t >= cap
     const uint32_t *pack;
     void *sig;
     unsigned long long *n_sat;
@@ -67,14 +71,14 @@ __device__ __forceinline__ uint32_t bv_word(uint32_t r, const uint32_t *pack, ui
     return t < cap ? cell_of(r, pack, uni_m) : 0xFFu;
 }
 
-// the first T0 draw words of every hash; cells by the packed IntToComp table or
+// the first BV_T0 draw words of every hash; cells by the packed IntToComp table or
 // (c2m != null, WMH_OPT_ISGREEN_BINSEARCH) by binary search over CompToM
 __global__ void bv_table_kernel(uint32_t *__restrict__ table, uint32_t k, uint64_t S, uint32_t M,
                                 const uint32_t *__restrict__ pack, uint32_t uni_m, uint32_t cap,
                                 const uint32_t *__restrict__ c2m, uint32_t D) {
-    const int64_t total = (int64_t)k * T0;
+    const int64_t total = (int64_t)k * BV_T0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t j = (uint32_t)(i / T0), t = (uint32_t)(i % T0);
+        const uint32_t j = (uint32_t)(i / BV_T0), t = (uint32_t)(i % BV_T0);
         const uint32_t r = draw_r(S, j, t, M);
         if (c2m) {
             const uint2 cell = cell_bsearch(r, c2m, D);
@@ -268,6 +272,35 @@ __device__ __forceinline__ bool bv_test(uint32_t planes_s, const bv_gmax_t<G> *g
     return CLAMP && need_any && off >= TOP;
 }
 
+// Green masks of a listed (needed) draw word w against all G groups; lanes
+// without a draw (valid false) load nothing and get empty masks.  CLAMP: true
+// when off >= 2^P - 1 (the exact test on the candidate rows follows).
+template <int P, int G, bool CLAMP>
+__device__ __forceinline__ bool bv_test_c(uint32_t planes_s, uint32_t w, bool valid, uint32_t (&mask)[G]) {
+    constexpr uint32_t TOP = (1u << P) - 1u;
+    const uint32_t c = w >> 8, off = w & 0xFFu;
+    const uint32_t blk = planes_s + c * (uint32_t)(G * P * 4);
+    const uint32_t L = CLAMP ? (off < TOP ? TOP - off : 0u) : TOP - off;
+    const uint32_t Xh = L * 0x08040201u, Xl = L * 0x80402010u;
+    uint32_t m[P];
+#pragma unroll
+    for (int b = 0; b < P; b++) m[b] = bv_prmt(b < 4 ? Xl : Xh, 0, 0x8888u + 0x1111u * (uint32_t)(3 - (b & 3)));
+    if constexpr (BvLayout<P, G>::GROUP_MAJOR) {
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            uint32_t xg[P];
+            bv_load_group<P, G>(blk, g, valid, xg);
+            mask[g] = valid ? bv_chain<P>(xg, m) : 0u;
+        }
+    } else {
+        uint32_t xa[G][P];
+        bv_load_all<P, G>(blk, valid, xa);
+#pragma unroll
+        for (int g = 0; g < G; g++) mask[g] = valid ? bv_chain<P>(xa[g], m) : 0u;
+    }
+    return CLAMP && valid && off >= TOP;
+}
+
 // CLAMP, off >= 2^P - 1: the draw against group g's rows whose clamped value
 // is all ones, read from the rows in global memory (rare: the top cells of the
 // few columns whose bound exceeds 2^P - 1)
@@ -296,8 +329,8 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *planes = smem;                                                         // [D][W]
     gm_t *gmax = reinterpret_cast<gm_t *>(planes + (size_t)p.D * W);                 // [D] (G bytes each)
-    uint16_t *hres_all = reinterpret_cast<uint16_t *>(
-        reinterpret_cast<uint8_t *>(gmax) + (((size_t)p.D * sizeof(gm_t) + 15) & ~(size_t)15));   // [NW][HB][R]
+    uint32_t *cbuf_all = reinterpret_cast<uint32_t *>(
+        reinterpret_cast<uint8_t *>(gmax) + (((size_t)p.D * sizeof(gm_t) + 15) & ~(size_t)15));   // [NW][BV_RD]
     uint8_t *gbytes = reinterpret_cast<uint8_t *>(gmax);
     uint8_t *pbytes = reinterpret_cast<uint8_t *>(planes);
     __shared__ long long s_next;
@@ -305,7 +338,8 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
     __shared__ uint32_t s_live[G];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint16_t *hres_blk = hres_all + warp * BV_HB * R;
+    uint32_t *cbuf = cbuf_all + warp * BV_RD;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     unsigned long long sat = 0;
     const int quads = p.D >> 2;                        // D % 4 == 0 (launcher)
     const BvTranspose tr(lane);
@@ -336,6 +370,9 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
         // unit = (column-quad pair, group, octet): one 8-byte load per row covers
         // both quads (full 32-byte sectors across the warp), processed as two quads
         const int n_units = (quads / 2) * G * 4;
+        // a thread's units all belong to one group (NT / 4 is a multiple of G):
+        // its live rows are OR-ed in a register and merged once per warp
+        uint32_t live_acc = 0u;
         auto stage_load = [&](int u0, uint32_t (&wb)[BV_SB][2][8]) {
 #pragma unroll
             for (int bi = 0; bi < BV_SB; bi++) {
@@ -397,7 +434,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 uint32_t cand = 0u, mx = 0u;
 #pragma unroll
                 for (int b = 0; b < P; b++) cand |= pw[b];
-                const uint32_t live = cand;              // rows of the group nonzero in this column
+                live_acc |= cand;                        // rows of the group nonzero in this column
 #pragma unroll
                 for (int b = P - 1; b >= 0; b--) {
                     const uint32_t t = pw[b] & cand;
@@ -406,12 +443,6 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 // clamped planes saturate at TOP: then only "some row >= TOP" is known,
                 // so the flagged draws of this column keep testing (bv_slow is exact)
                 gbytes[(size_t)c * sizeof(gm_t) + g] = (uint8_t)((CLAMP && mx == TOP) ? 0xFFu : mx);
-                const int first = __ffs(am) - 1;
-#pragma unroll
-                for (int gg = 0; gg < G; gg++) {
-                    const uint32_t lv = __reduce_or_sync(am, g == gg ? live : 0u);
-                    if (lane == first && lv) atomicOr(&s_live[gg], lv);
-                }
             }
             }
         };
@@ -428,6 +459,15 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 if (u1 >= n_units) break;
                 if (u1 + BV_SB * NT < n_units) stage_load(u1 + BV_SB * NT, bufA);
                 stage_proc(u1, bufB);
+            }
+        }
+        {
+            static_assert((NT / 4) % G == 0, "a thread's staging units must share one group");
+            const int g_thr = (threadIdx.x >> 2) % G;
+#pragma unroll
+            for (int gg = 0; gg < G; gg++) {
+                const uint32_t lv = __reduce_or_sync(0xFFFFFFFFu, g_thr == gg ? live_acc : 0u);
+                if (lane == 0 && lv) atomicOr(&s_live[gg], lv);
             }
         }
         __syncthreads();
@@ -448,8 +488,9 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
         }
 
         // ---- hashes: a warp claims blocks of BV_HB consecutive hashes (the next
-        //      block one block ahead) and flushes a block's results with one
-        //      16-byte store per row
+        //      block one block ahead).  Lane = row: the block's results of rows
+        //      32g + lane are kept packed in registers (acc[g], 2 per word, shifted
+        //      in hash by hash) and flushed with one 16-byte store per row
         auto grab = [&]() {
             int bb = 0;
             if (lane == 0) bb = atomicAdd(&s_hash, 1);
@@ -462,139 +503,179 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
             pend0[g] = s_live[g] & valid;
             dead[g] = valid & ~s_live[g];
         }
-        bool any_dead = false;
+        uint32_t n_dead = 0;                           // all-zero rows: h = cap at once (R12)
 #pragma unroll
-        for (int g = 0; g < G; g++) any_dead |= dead[g] != 0u;
+        for (int g = 0; g < G; g++) n_dead += __popc(dead[g]);
+        uint32_t acc[G][BV_HB / 2];
+#pragma unroll
+        for (int g = 0; g < G; g++)
+#pragma unroll
+            for (int i = 0; i < BV_HB / 2; i++) acc[g][i] = 0u;
         uint32_t jb = grab();                          // current block [jb, je)
         uint32_t je = min(j1, jb + BV_HB);
         uint32_t jb_next = jb < j1 ? grab() : j1;
         uint32_t j = jb;
-        // draw words: lane holds t = tb + lane (A) and tb + 32 + lane (B) of the
-        // current round, the next round's pair, and the next hash's first pair
-        // draw words: lane holds the pair t = tb + 2 lane, tb + 2 lane + 1 of the
-        // current round (one 8-byte load), the next round's pair, and the next
-        // hash's first two rounds
-        uint2 na = make_uint2(0u, 0u), nc = na;
+        // draw words: lane holds t = tb + 32 s + lane (s < BV_DPL) of the current
+        // round, of the next round, and of the next hash's first round
+        uint32_t nw[BV_DPL];
+#pragma unroll
+        for (int s = 0; s < BV_DPL; s++) nw[s] = 0u;
         if (j < j1) {
             WMH_DASSERT(j < p.k);
-            const uint2 *t0 = reinterpret_cast<const uint2 *>(p.table + (int64_t)j * T0);
-            na = __ldg(t0 + lane);
-            nc = __ldg(t0 + 32 + lane);
+            const uint32_t *t0 = p.table + (int64_t)j * BV_T0;
+#pragma unroll
+            for (int s = 0; s < BV_DPL; s++) nw[s] = __ldg(t0 + 32 * s + lane);
         }
         while (j < j1) {
             const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
-            uint16_t *hres = hres_blk + (j - jb) * R;
-            const uint2 *tj = reinterpret_cast<const uint2 *>(p.table + (int64_t)j * T0);
-            uint2 wc = na, wx = nc;                    // this round's pair, the next round's
-            if (jn < j1) {                             // one hash ahead: its rounds 0 and 1
-                const uint2 *tn = reinterpret_cast<const uint2 *>(p.table + (int64_t)jn * T0);
-                na = __ldg(tn + lane);
-                nc = __ldg(tn + 32 + lane);
-            }
-            // all-zero rows: cap at once (lane = row); a tile without them skips this
-            if (any_dead) {
+            const uint32_t *tj = p.table + (int64_t)j * BV_T0;
+            uint32_t cw[BV_DPL];                       // this round's draw words
 #pragma unroll
-                for (int g = 0; g < G; g++) {
-                    if ((dead[g] >> lane) & 1u) hres[32 * g + lane] = (uint16_t)p.cap;
-                    sat += (lane == 0) ? __popc(dead[g]) : 0;
-                }
+            for (int s = 0; s < BV_DPL; s++) cw[s] = nw[s];
+            if (jn < j1) {                             // one hash ahead: its first round
+                const uint32_t *tn = p.table + (int64_t)jn * BV_T0;
+#pragma unroll
+                for (int s = 0; s < BV_DPL; s++) nw[s] = __ldg(tn + 32 * s + lane);
             }
+            // h of row 32g + lane; rows without a green draw before the cap (and
+            // all-zero rows) keep h = cap
+            uint32_t hcur[G];
             uint32_t pend[G];
 #pragma unroll
-            for (int g = 0; g < G; g++) pend[g] = pend0[g];
-            for (uint32_t tb = 0;; tb += 64) {
+            for (int g = 0; g < G; g++) {
+                hcur[g] = p.cap;
+                pend[g] = pend0[g];
+            }
+            sat += (lane == 0) ? n_dead : 0u;
+            for (uint32_t tb = 0;; tb += BV_RD) {
                 uint32_t anyp = 0;
 #pragma unroll
                 for (int g = 0; g < G; g++) anyp |= pend[g];
                 if (!anyp) break;
                 if (tb >= p.cap) {                     // a8: no green draw before the cap
 #pragma unroll
-                    for (int g = 0; g < G; g++) {
-                        if ((pend[g] >> lane) & 1u) hres[32 * g + lane] = (uint16_t)p.cap;
-                        sat += (lane == 0) ? __popc(pend[g]) : 0;
-                    }
+                    for (int g = 0; g < G; g++) sat += (lane == 0) ? __popc(pend[g]) : 0;
                     break;
                 }
-                uint2 w = wc;
-                if (tb >= (uint32_t)T0) {              // beyond the table (rare): draw them here
+                uint32_t w[BV_DPL];
+#pragma unroll
+                for (int s = 0; s < BV_DPL; s++) w[s] = cw[s];
+                if (tb >= (uint32_t)BV_T0) {           // beyond the table (rare): draw them here
                     const uint64_t keyj = p.S ^ ((uint64_t)j << 32);
-                    const uint32_t t0 = tb + 2 * lane;
-                    w.x = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t0), p.M), p.pack, p.uni_m, t0, p.cap);
-                    w.y = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)(t0 + 1)), p.M), p.pack, p.uni_m, t0 + 1, p.cap);
-                }
-                // prefetch the round after next from the table (T0 draws per hash)
-                wc = wx;
-                if (tb + 128 < (uint32_t)T0) wx = __ldg(tj + (tb + 128) / 2 + lane);
-                uint32_t mA[G], mB[G];
-                const bool slowA = bv_test<P, G, CLAMP>(planes_s, gmax, w.x, pend, mA);
-                const bool slowB = bv_test<P, G, CLAMP>(planes_s, gmax, w.y, pend, mB);
-                if (CLAMP && (slowA || slowB)) {           // rare, divergent
 #pragma unroll
-                    for (int g = 0; g < G; g++) {
-                        if (slowA) mA[g] = bv_test_slow<P, G>(p, planes_s, gmax, row0, w.x, pend[g], g);
-                        if (slowB) mB[g] = bv_test_slow<P, G>(p, planes_s, gmax, row0, w.y, pend[g], g);
+                    for (int s = 0; s < BV_DPL; s++) {
+                        const uint32_t t = tb + 32 * s + lane;
+                        w[s] = bv_word(mulhi_range(splitmix64(keyj ^ (uint64_t)t), p.M), p.pack, p.uni_m, t, p.cap);
                     }
                 }
-                // ---- a8: the first green draw of each pending row.  Lane i tested
-                //      draws tb + 2i and tb + 2i + 1; one transpose of their union per
-                //      group gives lane = row the first lane i with a green, and that
-                //      lane's even-draw mask (a shuffle) says which of its two draws
-                uint32_t a[G], u[G], anyu = 0u;
+                if (tb + BV_RD < (uint32_t)BV_T0) {    // prefetch the next round
 #pragma unroll
-                for (int g = 0; g < G; g++) {
-                    a[g] = mA[g] & pend[g];
-                    u[g] = a[g] | (mB[g] & pend[g]);
-                    anyu |= u[g];
+                    for (int s = 0; s < BV_DPL; s++) cw[s] = __ldg(tj + tb + BV_RD + 32 * s + lane);
                 }
-                if (__any_sync(0xFFFFFFFFu, anyu != 0u)) {    // the G transposes interleave
-                    uint32_t wt[G];
+                // ---- a5/a6 screen: a draw is needed when its offset is below the
+                //      column maximum of a pending group; the needed draws of the
+                //      round are compacted in draw order into the warp's list
+                //      (entry = word << 7 | t - tb)
+                uint32_t gms[BV_DPL];                  // all column maxima loaded before any list store
 #pragma unroll
-                    for (int g = 0; g < G; g++) wt[g] = tr(u[g]);   // bit i: draw tb + 2i or + 2i + 1 green for row lane
+                for (int s = 0; s < BV_DPL; s++) {
+                    WMH_DASSERT((w[s] >> 8) < (uint32_t)p.D);
+                    gms[s] = (uint32_t)gmax[w[s] >> 8];
+                }
+                uint32_t total = 0;
+#pragma unroll
+                for (int s = 0; s < BV_DPL; s++) {
+                    const uint32_t off = w[s] & 0xFFu, gm = gms[s];
+                    bool need = false;
+#pragma unroll
+                    for (int g = 0; g < G; g++) need |= pend[g] != 0u && off < ((gm >> (8 * g)) & 0xFFu);
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, need);
+                    if (need) cbuf[total + __popc(bal & lt_mask)] = (w[s] << 7) | (uint32_t)(32 * s + lane);
+                    total += __popc(bal);
+                }
+                __syncwarp();
+                // ---- test the needed draws, 32 at a time (lane = draw), in draw order
+                for (uint32_t base = 0; base < total; base += 32) {
+                    const bool valid = base + lane < total;
+                    const uint32_t e = valid ? cbuf[base + lane] : 0u;
+                    const uint32_t we = e >> 7, toff = e & 127u;
+                    uint32_t mk[G];
+                    const bool slow = bv_test_c<P, G, CLAMP>(planes_s, we, valid, mk);
+                    if (CLAMP && slow) {               // rare, divergent
+#pragma unroll
+                        for (int g = 0; g < G; g++) mk[g] = bv_test_slow<P, G>(p, planes_s, gmax, row0, we, pend[g], g);
+                    }
+                    // ---- a8: the first green draw of each pending row: one transpose
+                    //      per group gives lane = row the first list position i
+                    //      with a green; its draw is tb + toff_i
+                    uint32_t u[G], anyu = 0u;
 #pragma unroll
                     for (int g = 0; g < G; g++) {
-                        const int i = __ffs(wt[g]) - 1;                  // first lane (pair) with a green for this row
-                        const uint32_t ai = __shfl_sync(0xFFFFFFFFu, a[g], i & 31);
-                        const uint32_t odd = ((ai >> lane) & 1u) ^ 1u;    // 0: the pair's first draw was green
-                        WMH_DASSERT(j - jb < (uint32_t)BV_HB);
-                        if (wt[g]) hres[32 * g + lane] = (uint16_t)(tb + 2u * (uint32_t)i + odd + 1u);
-                        pend[g] &= ~__ballot_sync(0xFFFFFFFFu, wt[g] != 0u);
+                        u[g] = mk[g] & pend[g];
+                        anyu |= u[g];
+                    }
+                    if (__any_sync(0xFFFFFFFFu, anyu != 0u)) {
+                        uint32_t wt[G];
+#pragma unroll
+                        for (int g = 0; g < G; g++) wt[g] = tr(u[g]);   // bit i: list entry base + i green for row lane
+#pragma unroll
+                        for (int g = 0; g < G; g++) {
+                            const int i = __ffs(wt[g]) - 1;
+                            const uint32_t ti = __shfl_sync(0xFFFFFFFFu, toff, i & 31);
+                            if (wt[g]) hcur[g] = tb + ti + 1u;
+                            pend[g] &= ~__ballot_sync(0xFFFFFFFFu, wt[g] != 0u);
+                        }
                     }
                 }
+                __syncwarp();                          // the list is rewritten next round
             }
-            __syncwarp();
+            // shift the hash's results in: slot BV_HB - 1 is the newest
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+#pragma unroll
+                for (int i = 0; i < BV_HB / 2 - 1; i++) acc[g][i] = bv_prmt(acc[g][i], acc[g][i + 1], 0x5432u);
+                acc[g][BV_HB / 2 - 1] = bv_prmt(acc[g][BV_HB / 2 - 1], hcur[g], 0x5432u);
+            }
             if (j + 1 == je) {
                 // ---- a9: flush the block: row r's hashes jb..je-1 are contiguous in sig
-                const int64_t eoff = (row0 + lane) * (int64_t)p.k + jb;
                 const int nh = (int)(je - jb);
-                if (nh == BV_HB && p.vec_flush) {
-                    for (int r = lane; r < nr; r += 32) {
-                        const int64_t e = eoff + (int64_t)(r - lane) * p.k;
-                        WMH_DASSERT(e + BV_HB <= p.n_rows * (int64_t)p.k && r < R);
-                        uint32_t hv[BV_HB];
+                WMH_DASSERT(nh >= 1 && nh <= BV_HB);
+                for (int u = nh; u < BV_HB; u++) {     // a short block: align hash jb to slot 0
 #pragma unroll
-                        for (int u = 0; u < BV_HB; u++) hv[u] = hres_blk[u * R + r];
+                    for (int g = 0; g < G; g++) {
+#pragma unroll
+                        for (int i = 0; i < BV_HB / 2 - 1; i++) acc[g][i] = bv_prmt(acc[g][i], acc[g][i + 1], 0x5432u);
+                        acc[g][BV_HB / 2 - 1] = bv_prmt(acc[g][BV_HB / 2 - 1], 0u, 0x5432u);
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    const int r = 32 * g + lane;
+                    if (r >= nr) continue;
+                    const int64_t e = (row0 + r) * (int64_t)p.k + jb;
+                    WMH_DASSERT(e + nh <= p.n_rows * (int64_t)p.k);
+                    if (nh == BV_HB && p.vec_flush) {
+                        static_assert(BV_HB == 8, "the vector flush packs 8 hashes");
                         if (p.sigb == 2) {
                             uint16_t *ptr = reinterpret_cast<uint16_t *>(p.sig) + e;
-                            const uint4 v = make_uint4(hv[0] | (hv[1] << 16), hv[2] | (hv[3] << 16),
-                                                       hv[4] | (hv[5] << 16), hv[6] | (hv[7] << 16));
                             if (p.vec_flush == 2) {
-                                *reinterpret_cast<uint4 *>(ptr) = v;
+                                *reinterpret_cast<uint4 *>(ptr) = make_uint4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
                             } else {
-                                reinterpret_cast<uint2 *>(ptr)[0] = make_uint2(v.x, v.y);
-                                reinterpret_cast<uint2 *>(ptr)[1] = make_uint2(v.z, v.w);
+                                reinterpret_cast<uint2 *>(ptr)[0] = make_uint2(acc[g][0], acc[g][1]);
+                                reinterpret_cast<uint2 *>(ptr)[1] = make_uint2(acc[g][2], acc[g][3]);
                             }
                         } else {
                             uint8_t *ptr = reinterpret_cast<uint8_t *>(p.sig) + e;
-                            *reinterpret_cast<uint2 *>(ptr) = make_uint2(hv[0] | (hv[1] << 8) | (hv[2] << 16) | (hv[3] << 24),
-                                                                         hv[4] | (hv[5] << 8) | (hv[6] << 16) | (hv[7] << 24));
+                            *reinterpret_cast<uint2 *>(ptr) = make_uint2(bv_prmt(acc[g][0], acc[g][1], 0x6420u),
+                                                                         bv_prmt(acc[g][2], acc[g][3], 0x6420u));
                         }
-                    }
-                } else {
-                    for (int r = lane; r < nr; r += 32) {
-                        const int64_t e = eoff + (int64_t)(r - lane) * p.k;
-                        for (int u = 0; u < nh; u++) {
-                            if (p.sigb == 2) reinterpret_cast<uint16_t *>(p.sig)[e + u] = hres_blk[u * R + r];
-                            else reinterpret_cast<uint8_t *>(p.sig)[e + u] = (uint8_t)hres_blk[u * R + r];
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < BV_HB; u++) {
+                            if (u >= nh) break;
+                            const uint32_t v = (acc[g][u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+                            if (p.sigb == 2) reinterpret_cast<uint16_t *>(p.sig)[e + u] = (uint16_t)v;
+                            else reinterpret_cast<uint8_t *>(p.sig)[e + u] = (uint8_t)v;
                         }
                     }
                 }
@@ -614,7 +695,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
 
 static size_t bv_smem(int D, int G, int P, int NT) {
     const size_t gm_bytes = (size_t)D * (G == 1 ? 1 : G == 2 ? 2 : 4);
-    return (size_t)D * G * P * 4 + ((gm_bytes + 15) & ~(size_t)15) + (size_t)(NT / 32) * BV_HB * 32 * G * 2;
+    return (size_t)D * G * P * 4 + ((gm_bytes + 15) & ~(size_t)15) + (size_t)(NT / 32) * BV_RD * 4;
 }
 
 template <int P, int G, bool CLAMP, int NT>
@@ -629,9 +710,9 @@ static void bv_launch(const BvParams &p, size_t smem, int grid, cudaStream_t s) 
 template <int P, bool CLAMP>
 static void bv_launch_g(int G, int NT, const BvParams &p, size_t smem, int grid, cudaStream_t s) {
     (void)NT;                                    // 512 threads (measured: 768 at <= 85 registers spills, 13.3 vs 11.9 ms)
-    if (G == 4) bv_launch<P, 4, CLAMP, 512>(p, smem, grid, s);
-    else if (G == 2) bv_launch<P, 2, CLAMP, 512>(p, smem, grid, s);
-    else bv_launch<P, 1, CLAMP, 512>(p, smem, grid, s);
+    if (G == 4) bv_launch<P, 4, CLAMP, BV_NT>(p, smem, grid, s);
+    else if (G == 2) bv_launch<P, 2, CLAMP, BV_NT>(p, smem, grid, s);
+    else bv_launch<P, 1, CLAMP, BV_NT>(p, smem, grid, s);
 }
 
 template <int P>
@@ -675,7 +756,7 @@ static BvShape bv_shape(const HashArgs &a) {
     const int gmax_try = (g_env == 1 || g_env == 2 || g_env == 4) ? g_env : 4;
     // one 512-thread CTA per SM: the planes fill shared memory (measured: two
     // 256-thread CTAs with one group each 15.5 vs 14.1 ms; 768 threads 13.3 vs 11.9)
-    const int ctas = 1, NT = 512;
+    const int ctas = 1, NT = BV_NT;
     const size_t budget = (size_t)smem_optin - 64;
     // WMH_BV_PLANES=P (4 <= P < NB): clamp to P planes whenever they fit two groups
     static const int p_env = getenv("WMH_BV_PLANES") ? atoi(getenv("WMH_BV_PLANES")) : 0;
@@ -695,7 +776,7 @@ bool bitslice_handles(const HashArgs &a) {
     const int D = (int)a.rows.dim;
     if (a.rows.kind != WMH_DENSE || (D & 7) || ((uintptr_t)a.rows.dense & 7)) return false;
     if ((a.L->flags & WMH_LAYOUT_WIDE) || weight_bytes(a.rows) != 1 || a.L->max_bound == 0 || a.L->max_bound > 255) return false;
-    if ((uint64_t)D >= (1ull << 24)) return false;
+    if ((uint64_t)D >= (1ull << 16)) return false;     // list entries: (c << 8 | off) << 7 | t - tb in 31 bits
     return bv_shape(a).G >= 1;
 }
 
@@ -718,14 +799,14 @@ wmh_status launch_hash_bitslice(const HashArgs &a, bool *handled) {
     n_hchunks = (int)((a.k + hchunk - 1) / hchunk);
 
     uint8_t *scratch = nullptr;
-    const size_t tab_bytes = (size_t)a.k * T0 * sizeof(uint32_t);
+    const size_t tab_bytes = (size_t)a.k * BV_T0 * sizeof(uint32_t);
     WMH_CUDA_TRY(cudaMallocAsync((void **)&scratch, tab_bytes + 256, a.stream), "bitslice scratch alloc");
     uint32_t *table = reinterpret_cast<uint32_t *>(scratch);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(scratch + tab_bytes);
     WMH_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), a.stream), "bitslice counter memset");
     const uint32_t uni_m = (a.L->flags & WMH_LAYOUT_UNIFORM) ? a.L->uniform_m : 0u;
     {
-        const int64_t total = (int64_t)a.k * T0;
+        const int64_t total = (int64_t)a.k * BV_T0;
         const int blocks = (int)std::min((int64_t)sms * 8, (total + 255) / 256);
         bv_table_kernel<<<blocks, 256, 0, a.stream>>>(table, a.k, a.S, (uint32_t)a.L->M, a.L->cell_pack, uni_m, a.cap,
                                                       a.isgreen_bsearch ? a.L->comp_to_m : nullptr, (uint32_t)D);

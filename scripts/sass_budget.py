@@ -91,9 +91,9 @@ def disasm(obj, kernel_match):
 
 def bitslice_regions():
     f = os.path.join(CSRC, "hash_bitslice.cu")
-    loop0 = line_of(f, "for (uint32_t tb = 0;; tb += 64) {")
+    loop0 = line_of(f, "for (uint32_t tb = 0;; tb += BV_RD) {")
     loop1 = block_end(f, loop0)
-    t0 = line_of(f, "__device__ __forceinline__ bool bv_test(")
+    t0 = line_of(f, "__device__ __forceinline__ bool bv_test_c(")
     t1 = block_end(f, t0)
     chain0 = line_of(f, "__device__ __forceinline__ uint32_t bv_chain(")
     ld0 = line_of(f, "__device__ __forceinline__ void bv_load_group(")
@@ -102,11 +102,15 @@ def bitslice_regions():
     prmt0 = line_of(f, "__device__ __forceinline__ uint32_t bv_prmt(")
     rotl0 = line_of(f, "__device__ __forceinline__ uint32_t bv_rotl(")
     comb0 = line_of(f, "// ---- a8: the first green draw of each pending row", loop0)
-    late0 = line_of(f, "if (tb >= (uint32_t)T0) {", loop0)
+    late0 = line_of(f, "if (tb >= (uint32_t)BV_T0) {", loop0)
     late1 = block_end(f, late0)
     cap0 = line_of(f, "if (tb >= p.cap) {", loop0)
     cap1 = block_end(f, cap0)
-    slow0 = line_of(f, "if (CLAMP && (slowA || slowB)) {", loop0)
+    slow0 = line_of(f, "if (CLAMP && slow) {", loop0)
+    scr0 = line_of(f, "// ---- a5/a6 screen:", loop0)
+    scr1 = line_of(f, "// ---- test the needed draws", scr0)
+    pass0 = line_of(f, "for (uint32_t base = 0; base < total; base += 32) {", loop0)
+    pass1 = block_end(f, pass0)
     slow1 = block_end(f, slow0)
     fname = "hash_bitslice.cu"
     test_lines = set(range(t0, t1 + 1)) | set(range(chain0, block_end(f, chain0) + 1)) | \
@@ -116,10 +120,13 @@ def bitslice_regions():
         set(range(rotl0, block_end(f, rotl0) + 1))
     return {
         "loop": (fname, loop0, loop1),
+        "pass": (pass0, pass1),
         "regions": [
             ("late_draws (t >= T0, cold)", lambda c: c[0] == "common.cuh" or (c[0] == fname and late0 <= c[1] <= late1)),
             ("cap (cold)", lambda c: c[0] == fname and cap0 <= c[1] <= cap1),
             ("clamped top cells (cold)", lambda c: c[0] == fname and slow0 <= c[1] <= slow1),
+            ("screen (decode 3 draws, column-max test, ballot compaction into the list)",
+             lambda c: c[0] == fname and scr0 <= c[1] < scr1),
             ("test (2 draws x G groups: decode, L masks, column-max skip, plane loads, carry chains)",
              lambda c: c[0] == fname and c[1] in test_lines),
             ("combine (32x32 transpose, first green by a pair shuffle, record)",
@@ -197,8 +204,10 @@ def main():
     fname, l0, l1 = spec["loop"]
     # the round loop = the innermost natural loop (a backward branch and its
     # target) that holds both test and combine instructions
-    test_pred = spec["regions"][2][1]
-    comb_pred = spec["regions"][3][1]
+    rp = dict(spec["regions"])
+    test_pred = rp[[k for k in rp if k.startswith("test")][0]]
+    comb_pred = rp[[k for k in rp if k.startswith("combine")][0]]
+    scr_pred = rp[[k for k in rp if k.startswith("screen")][0]]
     best = None
     for addr, c, op in ins:
         m = re.match(r"(?:@!?U?P\w+\s+)?BRA(?:\.\w+)*\s+0x([0-9a-f]+)", op)
@@ -208,7 +217,8 @@ def main():
         if tgt >= addr:
             continue
         body = [x for x in ins if tgt <= x[0] <= addr]
-        if any(x[1] and test_pred(x[1]) for x in body) and any(x[1] and comb_pred(x[1]) for x in body):
+        if any(x[1] and test_pred(x[1]) for x in body) and any(x[1] and comb_pred(x[1]) for x in body) and \
+                any(x[1] and scr_pred(x[1]) for x in body):
             if best is None or addr - tgt < best[1] - best[0]:
                 best = (tgt, addr)
     if best is None:
