@@ -144,13 +144,21 @@ __device__ __forceinline__ void bv_t8(uint32_t &lo, uint32_t &hi) {
     t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
 }
 
+// bit select: (m & x) | (~m & y), one LOP3 when m is in a register
+__device__ __forceinline__ uint32_t bv_sel(uint32_t m, uint32_t x, uint32_t y) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "r"(m), "r"(x), "r"(y));
+    return d;
+}
+
 // Delta swap of bit blocks between two row words (one stage of an 8x8 bit
-// transpose per byte): bits j of a with j & S != 0 <-> bits j - S of b.
+// transpose per byte): bits j of a with j & S != 0 <-> bits j - S of b.  The
+// masks m and mh = m << S come in registers (two shifts and two selects).
 template <int S>
-__device__ __forceinline__ void bv_swap(uint32_t &a, uint32_t &b, uint32_t m) {
+__device__ __forceinline__ void bv_swap(uint32_t &a, uint32_t &b, uint32_t m, uint32_t mh) {
     const uint32_t x = a >> S, y = b << S;
-    b = (b & ~m) | (x & m);
-    a = (a & ~(m << S)) | (y & (m << S));
+    b = bv_sel(m, x, b);
+    a = bv_sel(mh, y, a);
 }
 
 // Column block of the planes: W = G*P words.  P % 4 == 0: group-major [g][b]
@@ -332,7 +340,6 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
     uint32_t *cbuf_all = reinterpret_cast<uint32_t *>(
         reinterpret_cast<uint8_t *>(gmax) + (((size_t)p.D * sizeof(gm_t) + 15) & ~(size_t)15));   // [NW][BV_RD]
     uint8_t *gbytes = reinterpret_cast<uint8_t *>(gmax);
-    uint8_t *pbytes = reinterpret_cast<uint8_t *>(planes);
     __shared__ long long s_next;
     __shared__ int s_hash;
     __shared__ uint32_t s_live[G];
@@ -373,21 +380,35 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
         // a thread's units all belong to one group (NT / 4 is a multiple of G):
         // its live rows are OR-ed in a register and merged once per warp
         uint32_t live_acc = 0u;
+        // the delta-swap masks, kept in registers (LOP3 takes one immediate)
+        uint32_t m1 = 0x55555555u, m1h = 0xAAAAAAAAu, m2 = 0x33333333u, m2h = 0xCCCCCCCCu, m4 = 0x0F0F0F0Fu, m4h = 0xF0F0F0F0u;
+        asm volatile("" : "+r"(m1), "+r"(m1h), "+r"(m2), "+r"(m2h), "+r"(m4), "+r"(m4h));
+        const uint8_t *xt = p.x + row0 * (int64_t)p.D;   // the tile's first row
         auto stage_load = [&](int u0, uint32_t (&wb)[BV_SB][2][8]) {
 #pragma unroll
             for (int bi = 0; bi < BV_SB; bi++) {
                 const int u = u0 + bi * NT;
                 const int o = u & 3, g = (u >> 2) % G, cqp = (u >> 2) / G;
                 const int rb = 32 * g + 8 * o;
-                const uint8_t *xr = p.x + (row0 + rb) * (int64_t)p.D + 8 * cqp;
                 WMH_DASSERT(u >= n_units || (8 * cqp + 7 < p.D && g < G));
+                // a tile holds < 2^32 bytes: 32-bit offsets from its first row
+                const uint8_t *xr = xt + (uint32_t)(rb * p.D + 8 * cqp);
+                if (u < n_units && rb + 8 <= nr) {     // the common case: the octet's rows all exist
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    const bool ok = u < n_units && rb + i < nr;
-                    WMH_DASSERT(!ok || row0 + rb + i < p.n_rows);
-                    const uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(xr + (int64_t)i * p.D)) : make_uint2(0u, 0u);
-                    wb[bi][0][i] = v.x;
-                    wb[bi][1][i] = v.y;
+                    for (int i = 0; i < 8; i++) {
+                        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(xr + (uint32_t)(i * p.D)));
+                        wb[bi][0][i] = v.x;
+                        wb[bi][1][i] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        const bool ok = u < n_units && rb + i < nr;
+                        WMH_DASSERT(!ok || row0 + rb + i < p.n_rows);
+                        const uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(xr + (uint32_t)(i * p.D))) : make_uint2(0u, 0u);
+                        wb[bi][0][i] = v.x;
+                        wb[bi][1][i] = v.y;
+                    }
                 }
             }
         };
@@ -407,13 +428,13 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 // 8x8 bit transposes of the 4 byte columns at once: delta swaps
                 // across the 8 row words; afterwards w[b] = plane b (byte u4 =
                 // column u4, bit i = row 8o + i)
-                bv_swap<1>(w[0], w[1], 0x55555555u); bv_swap<1>(w[2], w[3], 0x55555555u);
-                bv_swap<1>(w[4], w[5], 0x55555555u); bv_swap<1>(w[6], w[7], 0x55555555u);
-                bv_swap<2>(w[0], w[2], 0x33333333u); bv_swap<2>(w[1], w[3], 0x33333333u);
-                bv_swap<2>(w[4], w[6], 0x33333333u); bv_swap<2>(w[5], w[7], 0x33333333u);
+                bv_swap<1>(w[0], w[1], m1, m1h); bv_swap<1>(w[2], w[3], m1, m1h);
+                bv_swap<1>(w[4], w[5], m1, m1h); bv_swap<1>(w[6], w[7], m1, m1h);
+                bv_swap<2>(w[0], w[2], m2, m2h); bv_swap<2>(w[1], w[3], m2, m2h);
+                bv_swap<2>(w[4], w[6], m2, m2h); bv_swap<2>(w[5], w[7], m2, m2h);
 #pragma unroll
                 for (int i = 0; i < 4; i++)
-                    if (i < P) bv_swap<4>(w[i], w[i + 4], 0x0F0F0F0Fu);
+                    if (i < P) bv_swap<4>(w[i], w[i + 4], m4, m4h);
                 // 4x4 byte transpose across the 4 octet lanes: lane o then holds the
                 // full 32-row plane words of column 4cq + o
                 const unsigned am = __activemask();
