@@ -421,10 +421,6 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 if (u >= n_units) break;                 // uniform over the 4 octet lanes of a unit
                 const int o = u & 3, g = (u >> 2) % G, cq = 2 * ((u >> 2) / G) + qq;
                 uint32_t *w = wb[bi][qq];
-                if (CLAMP) {
-#pragma unroll
-                    for (int i = 0; i < 8; i++) w[i] = __vminu4(w[i], TOP * 0x01010101u);
-                }
                 // 8x8 bit transposes of the 4 byte columns at once: delta swaps
                 // across the 8 row words; afterwards w[b] = plane b (byte u4 =
                 // column u4, bit i = row 8o + i)
@@ -435,6 +431,13 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
 #pragma unroll
                 for (int i = 0; i < 4; i++)
                     if (i < P) bv_swap<4>(w[i], w[i + 4], m4, m4h);
+                if (CLAMP) {                             // min(x, 2^P - 1): a set plane >= P sets planes 0..P-1
+                    uint32_t hi = 0u;
+#pragma unroll
+                    for (int b = P; b < 8; b++) hi |= w[b];
+#pragma unroll
+                    for (int b = 0; b < P; b++) w[b] |= hi;
+                }
                 // 4x4 byte transpose across the 4 octet lanes: lane o then holds the
                 // full 32-row plane words of column 4cq + o
                 const unsigned am = __activemask();
