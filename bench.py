@@ -465,7 +465,7 @@ def main():
     roof = roofline(algo_used, draws, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(), peaks)
     if algo_used == "tiled" and wmh.last_tile == "bitslice":
         roof = roofline_bitslice(x_sum, M, cfg, kern_s, n_sm, sm_mhz, in_bytes, sig.numel() * sig.element_size(),
-                                 peaks, draws)
+                                 peaks, draws, lambda R: tile_need_rate(xd, data, n, R, M))
     if algo_used == "index":
         if xd is not None:
             nnz = sum(int((xd[a0:a0 + 65536].to(torch.int32) != 0).sum().item()) for a0 in range(0, n, 65536))
@@ -572,17 +572,18 @@ def roofline(algo, draws, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks):
             "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3, "t_kernel_ms": kern_s * 1e3}
 
 
-def group_expected_max(x_sum: np.ndarray, M: int, cap: int, sample: int = 4096, seed: int = 3) -> tuple[float, int]:
-    """E[max over the live rows r of a 32-row group of min(G_r, cap)], G_r ~ Geom(s_r)
-    (Theorem 2), summed over the groups of consecutive 32 rows the
+def group_expected_max(x_sum: np.ndarray, M: int, cap: int, sample: int = 4096, seed: int = 3,
+                       rows: int = 32) -> tuple[float, int]:
+    """E[max over the live rows r of a `rows`-row group of min(G_r, cap)], G_r ~ Geom(s_r)
+    (Theorem 2), summed over the groups of consecutive rows the
     bit-sliced tile tests together: sum_t P(max > t) = sum_t 1 - prod_r (1 - (1 - s_r)^t).
     Exact per group; computed on a seeded sample of groups and scaled when there
     are more than `sample` groups.  Returns (sum over groups, groups sampled)."""
     s = x_sum.astype(np.float64) / M
-    n_groups = (len(s) + 31) // 32
-    pad = np.zeros(n_groups * 32)
+    n_groups = (len(s) + rows - 1) // rows
+    pad = np.zeros(n_groups * rows)
     pad[:len(s)] = s
-    g = pad.reshape(n_groups, 32)
+    g = pad.reshape(n_groups, rows)
     idx = np.arange(n_groups)
     if n_groups > sample:
         idx = np.sort(np.random.default_rng(seed).choice(n_groups, size=sample, replace=False))
@@ -596,7 +597,7 @@ def group_expected_max(x_sum: np.ndarray, M: int, cap: int, sample: int = 4096, 
     while t < cap and not done.all():
         ts = np.arange(t, min(cap, t + step), dtype=np.float64)
         # P(max > t) = 1 - prod_r (1 - q_r^t) over live rows (dead rows contribute 1)
-        qt = np.exp(lq[:, :, None] * ts[None, None, :])                   # [G, 32, T]
+        qt = np.exp(lq[:, :, None] * ts[None, None, :])                   # [G, rows, T]
         with np.errstate(divide="ignore"):                                # t = 0: log(1 - 1) = -inf, P = 1
             logp = np.where(live[:, :, None], np.log1p(-qt), 0.0).sum(axis=1)
         tail = -np.expm1(logp)                                            # P(max > t)
@@ -607,40 +608,64 @@ def group_expected_max(x_sum: np.ndarray, M: int, cap: int, sample: int = 4096, 
     return float(total.sum() * n_groups / len(g)), len(g)
 
 
-def roofline_bitslice(x_sum, M, cfg, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks, draws):
-    """The bit-sliced tile (hash_bitslice.cu): integer-issue bound.  Algorithmic
-    work = the group-draws bit-slicing must test -- for every 32-row group and
-    hash, the draws up to its last row's first green, E[max_r min(G_r, cap)]
-    (Theorem 2 per row) -- times the lane-instructions one group-draw costs in
-    the kernel's own round loop (test + first-green combine), counted statically
-    from SASS (profiles/r2_sass_bitslice.json, scripts/sass_budget.py).  Waste
-    the bound does not pay for: rounds of 64 draws past the max, staging the
-    tile, flushing signatures, issue stalls."""
+def tile_need_rate(xd, data, n: int, R: int, M: int, sample: int = 512, seed: int = 5) -> float:
+    """The fraction of draws the bit-sliced tile must test: a draw (c, off) is
+    needed when off < the column maximum over the tile's R rows, so per tile
+    q = sum_c colmax_tile(c) / M (Alg. 5's green test can only pass there).  Mean
+    over a seeded sample of tiles."""
+    n_tiles = (n + R - 1) // R
+    tiles = np.sort(np.random.default_rng(seed).choice(n_tiles, size=min(sample, n_tiles), replace=False))
+    qs = []
+    for t in tiles:
+        r0, r1 = int(t) * R, min(n, int(t) * R + R)
+        if xd is not None:
+            cm = xd[r0:r1].amax(dim=0).to(torch.int64).sum().item()
+        elif hasattr(data, "x"):
+            cm = int(np.asarray(data.x[r0:r1]).max(axis=0).astype(np.int64).sum())
+        elif hasattr(data, "rows"):
+            cm = int(data.rows(np.arange(r0, r1)).max(axis=0).astype(np.int64).sum())
+        else:
+            return float("nan")
+        qs.append(cm / M)
+    return float(np.mean(qs))
+
+
+def roofline_bitslice(x_sum, M, cfg, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, peaks, draws, need_rate):
+    """The bit-sliced tile (hash_bitslice.cu): integer-issue bound.  Its work per
+    R-row tile and hash: screen every draw up to the tile's last row's first
+    green -- E[max_r min(G_r, cap)] over the tile's rows (Theorem 2 per row) --
+    against the tile's column maxima, and test the needed fraction q of them
+    (need_rate(R), tile_need_rate) on the bit planes.  Floor = (screened draws x lane-instr per
+    screened draw + tested draws x lane-instr per tested draw) / the SMs' lane
+    issue rate, both per-unit costs counted statically from the kernel's own SASS
+    (profiles/r2_sass_bitslice.json, scripts/sass_budget.py).  Waste the floor
+    does not pay for: rounds of 96 draws past the max, passes with fewer than 32
+    listed draws, staging the tile, flushing signatures, issue stalls."""
     try:
         sass = json.load(open(os.path.join(ROOT, "profiles", "r2_sass_bitslice.json")))
-    except (OSError, ValueError) as e:           # the committed SASS budget is missing: say so, no fraction
-        return {"bound": "alu", "achieved": None, "peak": None, "unit": "Ggroup-draws/s", "frac": None,
+        a_scr, b_test = sass["lane_instr_per_screened_draw"], sass["lane_instr_per_tested_entry"]
+    except (OSError, ValueError, KeyError) as e:  # the committed SASS budget is missing: say so, no fraction
+        return {"bound": "alu", "achieved": None, "peak": None, "unit": "Gdraws/s", "frac": None,
                 "traffic": None, "kernel": "tiled/bitslice", "error": f"profiles/r2_sass_bitslice.json: {e}",
                 "t_kernel_ms": kern_s * 1e3}
-    reg = sass["by_region"]
-    n_test = next(v for k_, v in reg.items() if k_.startswith("test"))
-    n_comb = next(v for k_, v in reg.items() if k_.startswith("combine"))
-    G = sass.get("groups", 2)
-    lane_per_gd = 32.0 * (n_test + n_comb) / (64.0 * G)            # lane-instructions per group-draw
-    emax, sampled = group_expected_max(x_sum, M, cfg.cap)
-    group_draws = cfg.k * emax
+    R = 32 * sass.get("groups", 2)                                  # rows per tile of the profiled variant
+    q = need_rate(R)
+    emax, sampled = group_expected_max(x_sum, M, cfg.cap, rows=R)
+    screened = cfg.k * emax                                         # tile-draws screened
+    tested = q * screened                                           # tile-draws tested on the planes
+    per_draw = a_scr + q * b_test                                   # lane-instructions per screened draw
     issue = n_sm * 4 * 32 * sm_mhz * 1e6                            # lane-instructions / s
-    t_floor = group_draws * lane_per_gd / issue
+    t_floor = screened * per_draw / issue
     hbm = peaks.get("hbm_gbs", 6650.0)
-    return {"bound": "alu", "achieved": group_draws / kern_s / 1e9, "peak": issue / lane_per_gd / 1e9,
-            "unit": "Ggroup-draws/s", "frac": t_floor / kern_s, "traffic": None, "kernel": "tiled/bitslice",
+    return {"bound": "alu", "achieved": screened / kern_s / 1e9, "peak": issue / per_draw / 1e9,
+            "unit": "Gdraws/s", "frac": t_floor / kern_s, "traffic": None, "kernel": "tiled/bitslice",
             "peak_source": f"{n_sm} SMs x 128 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) / "
-                           f"{lane_per_gd:.1f} lane-instr per group-draw (32 x ({n_test} test + {n_comb} combine) "
-                           f"SASS instructions per 64-draw round of {G} groups, profiles/r2_sass_bitslice.json)",
-            "group_draws_required": group_draws, "groups_sampled": sampled,
+                           f"({a_scr:.1f} lane-instr per screened draw + q = {q:.3f} x {b_test:.1f} per tested draw; "
+                           f"SASS of the round and pass loops, profiles/r2_sass_bitslice.json)",
+            "tile_rows": R, "draws_screened_required": screened, "draws_tested_required": tested,
+            "need_rate_q": q, "tiles_sampled": sampled,
             "t_floor_ms": t_floor * 1e3, "t_kernel_ms": kern_s * 1e3,
             "t_hbm_ms": (in_bytes + out_bytes) / (hbm * 1e9) * 1e3,
-            "frac_vs_theorem2_rowtests": draws * (32.0 * n_test / (64.0 * G)) / 32.0 / issue / kern_s,
             "frac_vs_paper_loop": draws / kern_s / 1e9 / (issue / I_DRAW["simple"] / 1e9)}
 
 

@@ -12,20 +12,24 @@
 //
 // one LOP3 per plane for 32 rows (reading R2: strict, integer cells).
 //
-// Work of a warp per round: its 32 lanes take 64 consecutive draws t = tb + lane
-// and tb + 32 + lane of one hash (Alg. 3's loop, unrolled over
-// lanes).  Each lane decodes a draw once (column, offset, the L_b masks) and
-// tests it against all G groups.
-// Before loading any plane it compares the offset with the group's column
-// maximum gmax[c][g] (kept next to the planes): off >= gmax means no row of the
-// group is green, so most draws touch 2 bytes of shared memory instead of 4*P.
-// Rows green among the first 32 draws keep those masks (one REDUX.OR finds
-// them), the rest take the second 32; the merged masks (lane = draw, bit = row)
-// are transposed with five shuffle stages so that lane = row holds its draws as
-// bits, and the first green draw of every pending row is one __ffs: h = t + 1
-// (reading R1).
+// Work of a warp per hash, in rounds of BV_RD = 96 draws (Alg. 3's loop,
+// P:166-176, unrolled over lanes):
+//   screen: lane l decodes draws t = tb + 32 s + l (s < 3; column c, offset off)
+//     from the per-launch draw table and compares off with the tile's column
+//     maxima gmax[c][g] (kept next to the planes).  A draw can turn a row of group
+//     g green only when off < gmax[c][g]; for c5 that is ~25% of the draws.  The
+//     needed draws are compacted, in draw order, into a per-warp list (ballot +
+//     popcount positions).
+//   test: 32 listed draws at a time, lane = draw: build the L_b masks, load the
+//     column's plane block, one carry chain per group -> a green mask per group
+//     (lane = draw, bit = row).
+//   combine: a 32x32 bit transpose per group gives lane = row the list positions
+//     with a green; the first one (__ffs) is the row's first green draw, h = t + 1
+//     (reading R1).  Rows found leave the pending masks.
 // A row stays pending until it is green or the cap is reached (h = cap, R9);
-// all-zero rows never turn green and take the cap at once (R12).
+// all-zero rows never turn green and take the cap at once (R12).  A block of 8
+// hashes' results is kept in registers (lane = row, two 16-bit h per word) and
+// flushed with one 16-byte store per row.
 //
 // Clamped planes (CLAMP): when the bit count NB of the largest bound would not
 // let two groups fit, P = NB - 1 planes hold min(x, 2^P - 1) and gmax the true
@@ -237,47 +241,6 @@ __device__ __forceinline__ uint32_t bv_slow(const uint8_t *x, int64_t grow0, int
         m |= (uint32_t)(__ldg(x + (grow0 + i) * (int64_t)D + c) > off) << i;
     }
     return m;
-}
-
-// Green masks of the draw word w against the G groups (pending groups only):
-// the L_b masks are built once per draw; a group whose column maximum is at or
-// below the offset is red without touching its planes (R2).
-// Branch-free, so the chains of both draws and all groups interleave.  CLAMP:
-// a draw with off >= 2^P - 1 gets L = 0 (all red here) and returns true when a
-// group needs the exact test on the candidate rows (bv_test_slow).
-template <int P, int G, bool CLAMP>
-__device__ __forceinline__ bool bv_test(uint32_t planes_s, const bv_gmax_t<G> *gmax, uint32_t w, const uint32_t (&pend)[G],
-                                        uint32_t (&mask)[G]) {
-    constexpr uint32_t TOP = (1u << P) - 1u;
-    const uint32_t c = w >> 8, off = w & 0xFFu;
-    const uint32_t gm = (uint32_t)gmax[c];
-    const uint32_t blk = planes_s + c * (uint32_t)(G * P * 4);
-    const uint32_t L = CLAMP ? (off < TOP ? TOP - off : 0u) : TOP - off;
-    const uint32_t Xh = L * 0x08040201u, Xl = L * 0x80402010u;
-    uint32_t m[P];
-#pragma unroll
-    for (int b = 0; b < P; b++) m[b] = bv_prmt(b < 4 ? Xl : Xh, 0, 0x8888u + 0x1111u * (uint32_t)(3 - (b & 3)));
-    bool need[G];
-    bool need_any = false;
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        need[g] = pend[g] != 0u && off < ((gm >> (8 * g)) & 0xFFu);
-        need_any |= need[g];
-    }
-    if constexpr (BvLayout<P, G>::GROUP_MAJOR) {
-#pragma unroll
-        for (int g = 0; g < G; g++) {
-            uint32_t xg[P];
-            bv_load_group<P, G>(blk, g, need[g], xg);
-            mask[g] = need[g] ? bv_chain<P>(xg, m) : 0u;
-        }
-    } else {
-        uint32_t xa[G][P];
-        bv_load_all<P, G>(blk, need_any, xa);
-#pragma unroll
-        for (int g = 0; g < G; g++) mask[g] = need[g] ? bv_chain<P>(xa[g], m) : 0u;
-    }
-    return CLAMP && need_any && off >= TOP;
 }
 
 // Green masks of a listed (needed) draw word w against all G groups; lanes

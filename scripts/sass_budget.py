@@ -127,9 +127,9 @@ def bitslice_regions():
             ("clamped top cells (cold)", lambda c: c[0] == fname and slow0 <= c[1] <= slow1),
             ("screen (decode 3 draws, column-max test, ballot compaction into the list)",
              lambda c: c[0] == fname and scr0 <= c[1] < scr1),
-            ("test (2 draws x G groups: decode, L masks, column-max skip, plane loads, carry chains)",
+            ("test (a listed draw x G groups: decode, L masks, plane loads, carry chains)",
              lambda c: c[0] == fname and c[1] in test_lines),
-            ("combine (32x32 transpose, first green by a pair shuffle, record)",
+            ("combine (a 32x32 transpose per group, first list position, record)",
              lambda c: (c[0] == fname and c[1] in comb_lines) or c[0].startswith("sm_")),
             ("loop control + prefetch", lambda c: True),
         ],
@@ -208,39 +208,60 @@ def main():
     test_pred = rp[[k for k in rp if k.startswith("test")][0]]
     comb_pred = rp[[k for k in rp if k.startswith("combine")][0]]
     scr_pred = rp[[k for k in rp if k.startswith("screen")][0]]
-    best = None
+    loops = []                       # natural loops: (target, back-edge address)
     for addr, c, op in ins:
         m = re.match(r"(?:@!?U?P\w+\s+)?BRA(?:\.\w+)*\s+0x([0-9a-f]+)", op)
-        if not m:
-            continue
-        tgt = int(m.group(1), 16)
-        if tgt >= addr:
-            continue
-        body = [x for x in ins if tgt <= x[0] <= addr]
-        if any(x[1] and test_pred(x[1]) for x in body) and any(x[1] and comb_pred(x[1]) for x in body) and \
-                any(x[1] and scr_pred(x[1]) for x in body):
-            if best is None or addr - tgt < best[1] - best[0]:
-                best = (tgt, addr)
-    if best is None:
-        raise SystemExit("round loop not found")
-    lo, hi = best
-    rng = [x for x in ins if lo <= x[0] <= hi]
+        if m and int(m.group(1), 16) < addr:
+            loops.append((int(m.group(1), 16), addr))
+
+    def innermost(*preds):
+        best = None
+        for tgt, addr in loops:
+            body = [x for x in ins if tgt <= x[0] <= addr]
+            if all(any(x[1] and pr(x[1]) for x in body) for pr in preds):
+                if best is None or addr - tgt < best[1] - best[0]:
+                    best = (tgt, addr)
+        return best
+
+    # the round loop holds the screen and the tests; the pass loop (inside it)
+    # the tests and the first-green combine only
+    rnd = innermost(test_pred, comb_pred, scr_pred)
+    pas = innermost(test_pred, comb_pred)
+    if rnd is None or pas is None or not (rnd[0] <= pas[0] and pas[1] <= rnd[1]):
+        raise SystemExit(f"round/pass loops not found: {rnd} {pas}")
+    cold = [rp[k] for k in rp if "cold" in k]
     counts = {r[0]: 0 for r in spec["regions"]}
     lines = []
-    for addr, c, op in rng:
+    n_pass = n_round = 0
+    for addr, c, op in [x for x in ins if rnd[0] <= x[0] <= rnd[1]]:
         c = c or ("?", 0)
         for rname, pred in spec["regions"]:
             if pred(c):
                 counts[rname] += 1
                 break
-        lines.append(f"/*{addr:05x}*/ {op:60s} // {c[0]}:{c[1]}  [{rname.split(' ')[0]}]")
+        hot = not any(pr(c) for pr in cold)
+        in_pass = pas[0] <= addr <= pas[1]
+        if hot:
+            if in_pass:
+                n_pass += 1
+            else:
+                n_round += 1
+        lines.append(f"/*{addr:05x}*/ {op:60s} // {c[0]}:{c[1]}  [{rname.split(' ')[0]}{'' if hot else ' cold'}"
+                     f"{' pass' if in_pass else ''}]")
     mt = re.search(r"ILi(\d+)ELi(\d+)ELb(\d)ELi(\d+)E", name)
+    src = open(os.path.join(CSRC, "hash_bitslice.cu")).read()
+    dpl = int(re.search(r"constexpr int BV_DPL = (\d+);", src).group(1))
     res = {"kernel": name.split(",")[0], "planes": int(mt.group(1)), "groups": int(mt.group(2)),
            "clamp": int(mt.group(3)), "threads": int(mt.group(4)),
-           "loop_source": f"{fname}:{l0}-{l1}", "address_range": [hex(lo), hex(hi)],
-           "instructions_in_range": len(rng), "by_region": counts,
-           "note": "static count of the round loop (64 draws per warp round: 2 per lane); cold regions run "
-                   "only past T0 draws / at the cap"}
+           "loop_source": f"{fname}:{l0}-{l1}", "round_loop": [hex(rnd[0]), hex(rnd[1])],
+           "pass_loop": [hex(pas[0]), hex(pas[1])], "by_region": counts,
+           "draws_per_round": 32 * dpl, "entries_per_pass": 32,
+           "round_instructions": n_round, "pass_instructions": n_pass,
+           "lane_instr_per_screened_draw": 32.0 * n_round / (32 * dpl),
+           "lane_instr_per_tested_entry": 32.0 * n_pass / 32,
+           "note": "static SASS counts of the hot paths (cold regions excluded: late draws past the table, the cap, "
+                   "the clamped top cells): per round (screen 32*BV_DPL draws, outside the pass loop) and per pass "
+                   "(test up to 32 listed draws + first-green combine)"}
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out + ".json", "w"), indent=1)
     open(a.out + ".txt", "w").write("\n".join(lines) + "\n")

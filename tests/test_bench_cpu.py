@@ -66,3 +66,31 @@ def test_reference_data_is_lazy_for_c5():
     x = data.rows(np.array([0, 15_999_999]))
     assert x.shape == (2, 4096)
     assert np.array_equal(x, datagen.gen_counter_c5_rows(cfg.data_seed, np.array([0, 15_999_999]), 4096))
+
+
+def test_group_expected_max_64_row_tiles_against_simulation():
+    """The same expectation over the 64-row tiles of the bit-sliced kernel (G = 2)."""
+    rng = np.random.default_rng(4)
+    M, cap = 10_000, 65535
+    x_sum = rng.integers(200, 600, size=128).astype(np.int64)
+    got, sampled = bench.group_expected_max(x_sum, M, cap, rows=64)
+    assert sampled == 2
+    s = x_sum / M
+    T = 100_000
+    tot = 0.0
+    for g in range(2):
+        draws = rng.geometric(s[64 * g:64 * g + 64][None, :], size=(T, 64))
+        tot += np.minimum(draws, cap).max(axis=1).mean()
+    assert got == pytest.approx(tot, rel=5e-3)
+
+
+def test_tile_need_rate_is_the_mean_tile_column_max_over_M():
+    """q per tile = sum_c max over the tile's rows of x[r][c] / M (a draw can only
+    be green where its offset is below that maximum); ragged last tile included."""
+    import datagen
+    rng = np.random.default_rng(6)
+    x = rng.integers(0, 9, size=(130, 8)).astype(np.uint8)
+    M = int(x.max(axis=0).astype(np.int64).sum())
+    want = np.mean([x[a:a + 64].max(axis=0).astype(np.int64).sum() / M for a in (0, 64, 128)])
+    got = bench.tile_need_rate(None, datagen.Dense(x), 130, 64, M)
+    assert got == pytest.approx(want, rel=1e-12)
