@@ -614,6 +614,8 @@ def tile_need_rate(xd, data, n: int, R: int, M: int, sample: int = 512, seed: in
     q = sum_c colmax_tile(c) / M (Alg. 5's green test can only pass there).  Mean
     over a seeded sample of tiles."""
     n_tiles = (n + R - 1) // R
+    if xd is not None:
+        import torch  # noqa: F401  (xd is a device tensor)
     tiles = np.sort(np.random.default_rng(seed).choice(n_tiles, size=min(sample, n_tiles), replace=False))
     qs = []
     for t in tiles:
