@@ -337,12 +337,16 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
         //      (quad, group) combine their column maxima with two shuffles.
         //      BV_SB units per batch: all their loads are issued before any is
         //      used (one memory round trip per batch, not per unit)
-        // unit = (column-quad pair, group, octet): one 8-byte load per row covers
-        // both quads (full 32-byte sectors across the warp), processed as two quads
+        // unit = (column-quad pair, group, octet), octet fastest then columns: one
+        // 8-byte load per row covers both quads, and a warp's load of a row index
+        // touches 4 rows x 64 contiguous bytes; processed as two quads
         const int n_units = (quads / 2) * G * 4;
-        // a thread's units all belong to one group (NT / 4 is a multiple of G):
-        // its live rows are OR-ed in a register and merged once per warp
-        uint32_t live_acc = 0u;
+        // each thread ORs its live rows (nonzero in some column) per group in
+        // registers; merged once per warp after staging
+        uint32_t live_acc[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) live_acc[g] = 0u;
+        const int ncqp = quads / 2;                    // column-quad pairs per row
         // the delta-swap masks, kept in registers (LOP3 takes one immediate)
         uint32_t m1 = 0x55555555u, m1h = 0xAAAAAAAAu, m2 = 0x33333333u, m2h = 0xCCCCCCCCu, m4 = 0x0F0F0F0Fu, m4h = 0xF0F0F0F0u;
         asm volatile("" : "+r"(m1), "+r"(m1h), "+r"(m2), "+r"(m2h), "+r"(m4), "+r"(m4h));
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
 #pragma unroll
             for (int bi = 0; bi < BV_SB; bi++) {
                 const int u = u0 + bi * NT;
-                const int o = u & 3, g = (u >> 2) % G, cqp = (u >> 2) / G;
+                const int o = u & 3, cqp = (u >> 2) % ncqp, g = (u >> 2) / ncqp;
                 const int rb = 32 * g + 8 * o;
                 WMH_DASSERT(u >= n_units || (8 * cqp + 7 < p.D && g < G));
                 // a tile holds < 2^32 bytes: 32-bit offsets from its first row
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
             for (int qq = 0; qq < 2; qq++) {
                 const int u = u0 + bi * NT;
                 if (u >= n_units) break;                 // uniform over the 4 octet lanes of a unit
-                const int o = u & 3, g = (u >> 2) % G, cq = 2 * ((u >> 2) / G) + qq;
+                const int o = u & 3, g = (u >> 2) / ncqp, cq = 2 * ((u >> 2) % ncqp) + qq;
                 uint32_t *w = wb[bi][qq];
                 // 8x8 bit transposes of the 4 byte columns at once: delta swaps
                 // across the 8 row words; afterwards w[b] = plane b (byte u4 =
@@ -421,7 +425,8 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 uint32_t cand = 0u, mx = 0u;
 #pragma unroll
                 for (int b = 0; b < P; b++) cand |= pw[b];
-                live_acc |= cand;                        // rows of the group nonzero in this column
+#pragma unroll
+                for (int gg = 0; gg < G; gg++) live_acc[gg] |= g == gg ? cand : 0u;   // rows of the group nonzero in this column
 #pragma unroll
                 for (int b = P - 1; b >= 0; b--) {
                     const uint32_t t = pw[b] & cand;
@@ -449,11 +454,9 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
             }
         }
         {
-            static_assert((NT / 4) % G == 0, "a thread's staging units must share one group");
-            const int g_thr = (threadIdx.x >> 2) % G;
 #pragma unroll
             for (int gg = 0; gg < G; gg++) {
-                const uint32_t lv = __reduce_or_sync(0xFFFFFFFFu, g_thr == gg ? live_acc : 0u);
+                const uint32_t lv = __reduce_or_sync(0xFFFFFFFFu, live_acc[gg]);
                 if (lane == 0 && lv) atomicOr(&s_live[gg], lv);
             }
         }
