@@ -51,7 +51,7 @@ constexpr int BV_SB = 1;                  // staging units (quad pairs) per thre
 constexpr int BV_DPL = 3;                 // draws screened per lane per round
 constexpr int BV_RD = 32 * BV_DPL;        // draws per round
 constexpr int BV_T0 = 4 * BV_RD;          // draws per hash kept in the per-launch table (whole rounds)
-constexpr int BV_NT = 512;               // threads per CTA
+constexpr int BV_NT = 640;               // threads per CTA: 20 warps at <= 96 registers (measured on c5: 512 10.59 ms, 640 10.14, 768 14.07 (spills))
 
 struct BvParams {
     const uint8_t *x;
@@ -276,7 +276,7 @@ __device__ __forceinline__ bool bv_test_c(uint32_t planes_s, uint32_t w, bool va
 // is all ones, read from the rows in global memory (rare: the top cells of the
 // few columns whose bound exceeds 2^P - 1)
 template <int P, int G>
-__device__ __noinline__ uint32_t bv_test_slow(const BvParams &p, uint32_t planes_s, const bv_gmax_t<G> *gmax, int64_t row0,
+__device__ __forceinline__ uint32_t bv_test_slow(const BvParams &p, uint32_t planes_s, const bv_gmax_t<G> *gmax, int64_t row0,
                                               uint32_t w, uint32_t pend, int g) {
     const uint32_t c = w >> 8, off = w & 0xFFu;
     WMH_DASSERT(c < (uint32_t)p.D);
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *cbuf = cbuf_all + warp * BV_RD;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    unsigned long long sat = 0;
+    uint32_t sat = 0;                                  // lane 0: rows capped in this item, flushed per item
     const int quads = p.D >> 2;                        // D % 4 == 0 (launcher)
     const BvTranspose tr(lane);
     const uint32_t planes_s = (uint32_t)__cvta_generic_to_shared(planes);
@@ -319,6 +319,10 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
     for (;;) {
         // items are claimed one ahead, during the previous item's hashes (warp 0),
         // so no thread waits here on a global atomic
+        if (p.n_sat && lane == 0 && sat) {             // the previous item's capped rows
+            atomicAdd(p.n_sat, (unsigned long long)sat);
+            sat = 0;
+        }
         __syncthreads();                               // previous hashes done: planes free, s_next visible
         const long long item = s_next;
         if (threadIdx.x == 0) s_hash = 0;
@@ -518,14 +522,14 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
         }
         while (j < j1) {
             const uint32_t jn = j + 1 < je ? j + 1 : jb_next;
-            const uint32_t *tj = p.table + (int64_t)j * BV_T0;
+            const uint32_t tj = j * (uint32_t)BV_T0;       // this hash's table row (k * BV_T0 < 2^32)
             uint32_t cw[BV_DPL];                       // this round's draw words
 #pragma unroll
             for (int s = 0; s < BV_DPL; s++) cw[s] = nw[s];
             if (jn < j1) {                             // one hash ahead: its first round
-                const uint32_t *tn = p.table + (int64_t)jn * BV_T0;
+                const uint32_t tn = jn * (uint32_t)BV_T0;
 #pragma unroll
-                for (int s = 0; s < BV_DPL; s++) nw[s] = __ldg(tn + 32 * s + lane);
+                for (int s = 0; s < BV_DPL; s++) nw[s] = __ldg(p.table + (tn + 32 * s + lane));
             }
             // h of row 32g + lane; rows without a green draw before the cap (and
             // all-zero rows) keep h = cap
@@ -560,7 +564,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 }
                 if (tb + BV_RD < (uint32_t)BV_T0) {    // prefetch the next round
 #pragma unroll
-                    for (int s = 0; s < BV_DPL; s++) cw[s] = __ldg(tj + tb + BV_RD + 32 * s + lane);
+                    for (int s = 0; s < BV_DPL; s++) cw[s] = __ldg(p.table + (tj + tb + BV_RD + 32 * s + lane));
                 }
                 // ---- a5/a6 screen: a draw is needed when its offset is below the
                 //      column maximum of a pending group; the needed draws of the
@@ -677,10 +681,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
             j = jn;
         }
     }
-    if (p.n_sat) {
-        for (int o = 16; o; o >>= 1) sat += __shfl_xor_sync(0xFFFFFFFFu, sat, o);
-        if (lane == 0 && sat) atomicAdd(p.n_sat, sat);
-    }
+    if (p.n_sat && lane == 0 && sat) atomicAdd(p.n_sat, (unsigned long long)sat);
 }
 
 static size_t bv_smem(int D, int G, int P, int NT) {
@@ -699,7 +700,7 @@ static void bv_launch(const BvParams &p, size_t smem, int grid, cudaStream_t s) 
 
 template <int P, bool CLAMP>
 static void bv_launch_g(int G, int NT, const BvParams &p, size_t smem, int grid, cudaStream_t s) {
-    (void)NT;                                    // 512 threads (measured: 768 at <= 85 registers spills, 13.3 vs 11.9 ms)
+    (void)NT;                                    // BV_NT threads
     if (G == 4) bv_launch<P, 4, CLAMP, BV_NT>(p, smem, grid, s);
     else if (G == 2) bv_launch<P, 2, CLAMP, BV_NT>(p, smem, grid, s);
     else bv_launch<P, 1, CLAMP, BV_NT>(p, smem, grid, s);
@@ -744,8 +745,8 @@ static BvShape bv_shape(const HashArgs &a) {
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     static const int g_env = getenv("WMH_BV_GROUPS") ? atoi(getenv("WMH_BV_GROUPS")) : 0;
     const int gmax_try = (g_env == 1 || g_env == 2 || g_env == 4) ? g_env : 4;
-    // one 512-thread CTA per SM: the planes fill shared memory (measured: two
-    // 256-thread CTAs with one group each 15.5 vs 14.1 ms; 768 threads 13.3 vs 11.9)
+    // one BV_NT-thread CTA per SM: the planes fill shared memory (measured: two
+    // 256-thread CTAs with one group each 15.5 vs 14.1 ms)
     const int ctas = 1, NT = BV_NT;
     const size_t budget = (size_t)smem_optin - 64;
     // WMH_BV_PLANES=P (4 <= P < NB): clamp to P planes whenever they fit two groups
