@@ -546,11 +546,6 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
 #pragma unroll
                 for (int g = 0; g < G; g++) anyp |= pend[g];
                 if (!anyp) break;
-                if (tb >= p.cap) {                     // a8: no green draw before the cap
-#pragma unroll
-                    for (int g = 0; g < G; g++) sat += (lane == 0) ? __popc(pend[g]) : 0;
-                    break;
-                }
                 uint32_t w[BV_DPL];
 #pragma unroll
                 for (int s = 0; s < BV_DPL; s++) w[s] = cw[s];
@@ -586,6 +581,14 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, need);
                     if (need) cbuf[total + __popc(bal & lt_mask)] = (w[s] << 7) | (uint32_t)(32 * s + lane);
                     total += __popc(bal);
+                }
+                if (total == 0u) {                     // draws at t >= cap are never needed (word 0xFF)
+                    if (tb + BV_RD >= p.cap) {         // a8: no green draw before the cap
+#pragma unroll
+                        for (int g = 0; g < G; g++) sat += (lane == 0) ? __popc(pend[g]) : 0;
+                        break;
+                    }
+                    continue;
                 }
                 __syncwarp();
                 // ---- test the needed draws, 32 at a time (lane = draw), in draw order

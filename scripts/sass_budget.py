@@ -104,7 +104,7 @@ def bitslice_regions():
     comb0 = line_of(f, "// ---- a8: the first green draw of each pending row", loop0)
     late0 = line_of(f, "if (tb >= (uint32_t)BV_T0) {", loop0)
     late1 = block_end(f, late0)
-    cap0 = line_of(f, "if (tb >= p.cap) {", loop0)
+    cap0 = line_of(f, "if (total == 0u) {", loop0)
     cap1 = block_end(f, cap0)
     slow0 = line_of(f, "if (CLAMP && slow) {", loop0)
     scr0 = line_of(f, "// ---- a5/a6 screen:", loop0)
