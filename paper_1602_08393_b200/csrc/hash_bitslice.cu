@@ -485,11 +485,18 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
         //      block one block ahead).  Lane = row: the block's results of rows
         //      32g + lane are kept packed in registers (acc[g], 2 per word, shifted
         //      in hash by hash) and flushed with one 16-byte store per row
+        //      The item's last ~4 hashes per warp are claimed in blocks of 4 (the
+        //      barrier tail behind the slowest warp is one block long).
+        const uint32_t span = j1 - j0, n_tail = 4u * (NT / 32);
+        const uint32_t tail0 = j0 + (span > n_tail ? (span - n_tail) & ~(uint32_t)(BV_HB - 1) : 0u);
+        const uint32_t nb_full = (tail0 - j0) / BV_HB;
         auto grab = [&]() {
             int bb = 0;
             if (lane == 0) bb = atomicAdd(&s_hash, 1);
-            return min(j1, j0 + (uint32_t)BV_HB * (uint32_t)__shfl_sync(0xFFFFFFFFu, bb, 0));
+            const uint32_t b = (uint32_t)__shfl_sync(0xFFFFFFFFu, bb, 0);
+            return min(j1, b < nb_full ? j0 + (uint32_t)BV_HB * b : tail0 + 4u * (b - nb_full));
         };
+        auto block_end = [&](uint32_t jb_) { return min(j1, jb_ + (jb_ < tail0 ? (uint32_t)BV_HB : 4u)); };
         uint32_t pend0[G], dead[G];
 #pragma unroll
         for (int g = 0; g < G; g++) {
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
 #pragma unroll
             for (int i = 0; i < BV_HB / 2; i++) acc[g][i] = 0u;
         uint32_t jb = grab();                          // current block [jb, je)
-        uint32_t je = min(j1, jb + BV_HB);
+        uint32_t je = block_end(jb);
         uint32_t jb_next = jb < j1 ? grab() : j1;
         uint32_t j = jb;
         // draw words: lane holds t = tb + 32 s + lane (s < BV_DPL) of the current
@@ -666,6 +673,9 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                             *reinterpret_cast<uint2 *>(ptr) = make_uint2(bv_prmt(acc[g][0], acc[g][1], 0x6420u),
                                                                          bv_prmt(acc[g][2], acc[g][3], 0x6420u));
                         }
+                    } else if (nh == 4 && p.vec_flush) {   // a tail block (jb - j0 = 0 mod 4)
+                        if (p.sigb == 2) *reinterpret_cast<uint2 *>(reinterpret_cast<uint16_t *>(p.sig) + e) = make_uint2(acc[g][0], acc[g][1]);
+                        else *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(p.sig) + e) = bv_prmt(acc[g][0], acc[g][1], 0x6420u);
                     } else {
 #pragma unroll
                         for (int u = 0; u < BV_HB; u++) {
@@ -678,7 +688,7 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 }
                 __syncwarp();
                 jb = jb_next;
-                je = min(j1, jb + BV_HB);
+                je = block_end(jb);
                 jb_next = jb < j1 ? grab() : j1;
             }
             j = jn;
