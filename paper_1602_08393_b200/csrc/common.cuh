@@ -22,6 +22,8 @@ struct wmh_layout {
     uint64_t rowsum_q = 0;            // 0.1% quantile (power of two) of prepare's nonzero row sums; 0 = unknown
     double mean_s = -1.0;             // mean effective sparsity |x|_1 / M of prepare's rows (Eq. 17); < 0 = unknown
     uint64_t clamp_cells[8] = {0};    // sum_c max(0, m_c - (2^b - 1)), b = 0..7 (the plane tiles' clamp choice)
+    uint64_t value_ge[8] = {0};       // sampled dense uint8 weights >= 2^b - 1 (b = 3..7; every 16th row given to prepare)
+    uint64_t value_cells = 0;         // cells in that sample (0: no sample -> the bit-sliced tile clamps only to fit)
     int device = 0;
 };
 

@@ -280,13 +280,24 @@ __global__ void __launch_bounds__(256) rowsum_hist(const W *__restrict__ dense, 
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long total = 0;                 // hist[65]: sum of all row sums
+    uint32_t ge[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // hist[66 + b]: sampled weights >= 2^b - 1 (b = 3..7), hist[74]: cells sampled
+    uint32_t cells = 0;
     for (int64_t r = w0; r < n_rows; r += nw) {
         unsigned long long s = 0;
         if (dense) {
             const W *x = dense + r * dim;
             if (sizeof(W) == 1 && (dim & 3) == 0 && ((uintptr_t)dense & 3) == 0) {
                 const uint32_t *x4 = reinterpret_cast<const uint32_t *>(x);
-                for (int64_t i = lane; i < dim / 4; i += 32) s += __dp4a(__ldg(x4 + i), 0x01010101u, 0u);
+                const bool sample = (r & 15) == 0;   // every 16th row: the value tail the bit-sliced tile clamps
+                for (int64_t i = lane; i < dim / 4; i += 32) {
+                    const uint32_t v = __ldg(x4 + i);
+                    s += __dp4a(v, 0x01010101u, 0u);
+                    if (sample) {
+#pragma unroll
+                        for (int b = 3; b < 8; b++) ge[b] += __popc(__vcmpgeu4(v, ((1u << b) - 1u) * 0x01010101u)) >> 3;
+                        cells += 4;
+                    }
+                }
             } else {
                 for (int64_t i = lane; i < dim; i += 32) s += __ldg(x + i);
             }
@@ -299,6 +310,14 @@ __global__ void __launch_bounds__(256) rowsum_hist(const W *__restrict__ dense, 
         total += s;
     }
     if (lane == 0 && total) atomicAdd(hist + 65, total);
+#pragma unroll
+    for (int b = 3; b < 8; b++) {
+        uint32_t a = ge[b];
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        if (lane == 0 && a) atomicAdd(hist + 66 + b, (unsigned long long)a);
+    }
+    for (int o = 16; o; o >>= 1) cells += __shfl_xor_sync(0xFFFFFFFFu, cells, o);
+    if (lane == 0 && cells) atomicAdd(hist + 74, (unsigned long long)cells);
 }
 
 extern "C" wmh_status wmh_colmax(const wmh_rows *rows, uint32_t *colmax, void *stream) {
@@ -404,7 +423,7 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
                                                   L->bounds, bad);
         }
     }
-    unsigned long long *hist = nullptr, hhist[66] = {0};
+    unsigned long long *hist = nullptr, hhist[75] = {0};
     const bool stats = rows && rows->n_rows > 0;
     if (stats) {
         if (cudaMallocAsync((void **)&hist, sizeof hhist, s) != cudaSuccess) { cudaFreeAsync(scr, s); set_error("wmh_prepare: scratch alloc failed"); return fail(WMH_ENOMEM); }
@@ -431,6 +450,10 @@ extern "C" wmh_status wmh_prepare(const uint32_t *bounds, int64_t dim, const wmh
     cudaFreeAsync(scr, s);
     if (hist) cudaFreeAsync(hist, s);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(cuda_fail(e1 != cudaSuccess ? e1 : e2, "prepare readback"));
+    if (stats) {
+        for (int b = 0; b < 8; b++) L->value_ge[b] = hhist[66 + b];
+        L->value_cells = hhist[74];
+    }
     if (stats) {             // 0.1% quantile of the nonzero row sums, as the bin's lower end 2^b; mean s
         L->mean_s = host[0] ? (double)hhist[65] / ((double)rows->n_rows * (double)host[0]) : -1.0;
         unsigned long long nz = 0, run = 0;

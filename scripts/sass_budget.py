@@ -177,7 +177,7 @@ def per_unit_budget(obj, kernel_match, src, first_marker, last_marker, unit_op, 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("which", choices=["bitslice", "cm", "index", "simple"])
-    ap.add_argument("--kernel-match", nargs="+", default=["bitslice_kernel", "ILi6ELi2ELb0ELi640"])
+    ap.add_argument("--kernel-match", nargs="+", default=["bitslice_kernel", "ILi5ELi2ELb0ELi640"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_sass_bitslice"))
     a = ap.parse_args()
     if a.which == "cm":            # the byte tile's SWAR round: one LDS of a 4-row word per draw
@@ -262,7 +262,7 @@ def main():
            "note": "static SASS counts of the hot paths (cold regions excluded: late draws past the table, the cap, "
                    "the clamped top cells): per round (screen 32*BV_DPL draws, outside the pass loop) and per pass "
                    "(test up to 32 listed draws + first-green combine).  Counted on the unclamped variant: the "
-                   "clamped one (c5's P = 6 of NB = 7) runs the same hot path plus the rare inline test of the "
+                   "clamped one (c5's P = 5 of NB = 7) runs the same hot path plus the rare inline test of the "
                    "top cells, whose block layout the loop finder cannot separate"}
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out + ".json", "w"), indent=1)

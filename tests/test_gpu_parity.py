@@ -226,6 +226,29 @@ def test_tiled_bitplanes_clamped(wmh, tile, capfd, monkeypatch):
         assert "[wmh bitslice] P=6 clamp=1 G=2" in err, err[-300:]
 
 
+def test_bitslice_thin_tail_clamps_to_fewer_planes(wmh, capfd, monkeypatch):
+    """Weights with a thin tail (geometric, a few cells at 70 and 100 so NB = 7):
+    prepare's sampled fraction of weights >= 15 is ~1e-5, so the tile keeps 4
+    planes and tests the draws in the top cells of the wide columns on the rows'
+    bytes -- still bit-exact with the oracle, including the rows that are green
+    only there."""
+    monkeypatch.setenv("WMH_TILED_STATS", "1")
+    rng = np.random.default_rng(79)
+    n, D = 200, 4096
+    x = np.minimum(rng.geometric(0.5, size=(n, D)) - 1, 12).astype(np.uint8)
+    x[5, 10] = 100
+    x[6, 11] = 70
+    x[7] = 0
+    x[7, 10] = 90                                # green only in column 10's cells 15..89
+    data = datagen.Dense(x)
+    cfg = datagen.Config("thin", n, D, 1, 255, 1)
+    for k, cap in [(64, 65535), (16, 300)]:
+        sig, L, _ = _run(wmh, data, cfg, k, cap, 2, "tiled", seed=13, tile="bitslice")
+        _assert_sig_equal(sig, oracle_hash(L, data, 13, k, cap), f"thin tail k={k}")
+    err = capfd.readouterr().err
+    assert "[wmh bitslice] P=4 clamp=1 G=2" in err, err[-300:]
+
+
 def test_bitslice_clamped_group_major(wmh, capfd, monkeypatch):
     """The bit-sliced tile with 4 clamped planes in group-major blocks (D = 2912,
     bounds up to 31: five planes would leave two groups, four give four): the
