@@ -68,6 +68,7 @@ struct BvParams {
     void *sig;
     unsigned long long *n_sat;
     unsigned long long *item_ctr;
+    int bulk_pf;                 // rows 16-byte aligned: the next tile's L2 prefetch by TMA bulk prefetches
 };
 
 // the draw word of cell r: (c << 8) | (r - CompToM[c]); t >= cap -> 0xFF, which
@@ -477,8 +478,18 @@ __global__ void __launch_bounds__(NT, 1) hash_bitslice_kernel(const BvParams p) 
                 const int64_t nrow0 = (nx / p.n_hchunks) * R;
                 const int64_t nbytes = min((int64_t)R, p.n_rows - nrow0) * (int64_t)p.D;
                 const char *base = reinterpret_cast<const char *>(p.x + nrow0 * (int64_t)p.D);
-                for (int64_t off = (int64_t)lane * 128; off < nbytes; off += 32 * 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+                if (p.bulk_pf) {
+                    // the tile's rows are contiguous: one TMA bulk prefetch per lane
+                    // (cp.async.bulk.prefetch.L2, 16-byte granules of its share)
+                    const int64_t per = ((nbytes + 31) / 32 + 15) & ~(int64_t)15;
+                    const int64_t off = (int64_t)lane * per;
+                    const int64_t sz = min(per, nbytes - off) & ~(int64_t)15;
+                    if (sz > 0)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"((uint32_t)sz) : "memory");
+                } else {
+                    for (int64_t off = (int64_t)lane * 128; off < nbytes; off += 32 * 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+                }
             }
         }
 
@@ -857,6 +868,8 @@ wmh_status launch_hash_bitslice(const HashArgs &a, bool *handled) {
     p.sig = a.sig;
     p.n_sat = a.n_sat;
     p.item_ctr = ctr;
+    // WMH_BV_NO_BULKPF: the per-line prefetch loop instead (A/B)
+    p.bulk_pf = ((uintptr_t)a.rows.dense & 15) == 0 && (D & 15) == 0 && !getenv("WMH_BV_NO_BULKPF");
     const int grid = (int)std::min((int64_t)sms * sh.ctas, p.n_items);
 #define WMH_BV_GO(V) bv_launch_p<V>(G, sh.clamp, sh.NT, p, smem, grid, a.stream)
     WMH_BV_P_SWITCH(P, WMH_BV_GO)

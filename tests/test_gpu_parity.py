@@ -630,3 +630,4 @@ def test_check_rows_and_validate_against_oracle(wmh):
     assert want is not None and want[1] == 3
     with pytest.raises(wmh.WmhError, match=f"nonzero {want[0]}: value exceeds its bound"):
         wmh.check_rows(layout, to_rows(csr))
+
