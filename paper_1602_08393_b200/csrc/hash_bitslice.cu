@@ -49,10 +49,16 @@ namespace wmh {
 
 constexpr int BV_HB = 8;                  // hashes per claimed block (results flushed 8 per row)
 constexpr int BV_SB = 1;                  // staging units (quad pairs) per thread whose loads are in flight together
-constexpr int BV_DPL = 3;                 // draws screened per lane per round
+#ifndef WMH_BV_DPL
+#define WMH_BV_DPL 3
+#endif
+#ifndef WMH_BV_NT
+#define WMH_BV_NT 640
+#endif
+constexpr int BV_DPL = WMH_BV_DPL;        // draws screened per lane per round
 constexpr int BV_RD = 32 * BV_DPL;        // draws per round
 constexpr int BV_T0 = 4 * BV_RD;          // draws per hash kept in the per-launch table (whole rounds)
-constexpr int BV_NT = 640;               // threads per CTA: 20 warps at <= 96 registers (measured on c5: 512 10.59 ms, 640 10.14, 768 14.07 (spills))
+constexpr int BV_NT = WMH_BV_NT;               // threads per CTA: 20 warps at <= 96 registers (measured on c5: 512 10.59 ms, 640 10.14, 768 14.07 (spills))
 
 struct BvParams {
     const uint8_t *x;
