@@ -631,3 +631,25 @@ def test_check_rows_and_validate_against_oracle(wmh):
     with pytest.raises(wmh.WmhError, match=f"nonzero {want[0]}: value exceeds its bound"):
         wmh.check_rows(layout, to_rows(csr))
 
+
+
+@pytest.mark.parametrize("D,offset", [(1032, 0), (4096, 8)])
+def test_bitslice_rows_without_bulk_prefetch(wmh, D, offset):
+    """The bit-sliced tile warms L2 with the next tile's rows by TMA bulk prefetches
+    only when the rows are 16-byte aligned (D % 16 == 0 and an aligned base);
+    D = 1032 and a view 8 bytes into its allocation take the per-line prefetch
+    loop.  Prefetching changes no result: bit-exact with the oracle either way."""
+    rng = np.random.default_rng(7000 + D + offset)
+    n = 200
+    x = np.minimum(rng.geometric(0.3, size=(n, D)), 40).astype(np.uint8)
+    x[rng.random((n, D)) < 0.5] = 0
+    flat = np.zeros(n * D + offset, np.uint8)
+    flat[offset:] = x.reshape(-1)
+    xt = torch.from_numpy(flat).cuda()[offset:].view(n, D)
+    assert xt.data_ptr() % 16 == offset % 16
+    rows = wmh.Rows.from_dense(xt)
+    layout = wmh.prepare(rows)
+    L = oracle.Layout(oracle.colmax_dense(x))
+    assert layout.M == L.M
+    sig = wmh.hash(layout, rows, 29, 96, 65535, 2, algo="tiled", tile="bitslice")
+    _assert_sig_equal(sig, L.hash_dense(x, 29, 96, 65535), f"bitslice D={D} offset={offset}")
