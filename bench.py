@@ -682,6 +682,18 @@ def index_epochs(T: int):
     return B + [T]
 
 
+def index_cf(k: int, dense: bool) -> float:
+    """The plan's fallback-draw cost the kernel uses (hash_index.cu index_rows):
+    2 for dense rows; CSR rows 24 with 8 warps per row, else 64 (warps per row:
+    2, doubled while 64/nw rows' h[k] would exceed 128 KiB)."""
+    if dense:
+        return 2.0
+    nw = 2
+    while nw < 8 and (64 // nw) * k * 4 > (128 << 10):
+        nw *= 2
+    return 24.0 if nw == 8 else 64.0
+
+
 def index_plan(s: np.ndarray, k: int, cap: int, B, cf: float) -> np.ndarray:
     """Per row the horizon T_x the index kernel picks (hash_index.cu ix_plan): the
     epoch minimising k*T*s + k*(1-s)^T * max(32, min(1/s, cap-T)) * cf."""
@@ -699,7 +711,7 @@ def roofline_index(x_sum, nnz, M, cfg, T, kern_s, in_bytes, out_bytes, peaks, dr
     row, T_x the kernel's own per-row horizon) + two 4 B range bounds per nonzero."""
     s = x_sum.astype(np.float64) / M
     live = s > 0
-    Tx = index_plan(s[live], cfg.k, cfg.cap, index_epochs(int(T)), 2.0 if dense else 16.0)
+    Tx = index_plan(s[live], cfg.k, cfg.cap, index_epochs(int(T)), index_cf(cfg.k, dense))
     entries = float(cfg.k * (Tx * s[live]).sum())
     algo_bytes = in_bytes + out_bytes + 4.0 * entries + 8.0 * nnz
     hbm = peaks.get("hbm_gbs", 6650.0)

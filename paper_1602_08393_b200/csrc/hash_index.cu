@@ -1037,10 +1037,20 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     p.k = a.k;
     p.cap = a.cap;
     p.capn = 0;
+    // warps per row: >= 2; keep <= ~128 KiB of h[] per SM at 64 resident warps
+    static const int nw_env = getenv("WMH_INDEX_NW") ? atoi(getenv("WMH_INDEX_NW")) : 0;
+    int nw = 2;
+    while (nw < 8 && (uint64_t)(64 / nw) * a.k * 4 > (128u << 10)) nw *= 2;
+    if (nw_env == 1 || nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
+    // the plan's cost of one fallback draw in units of one index entry: an
+    // unstaged CSR row's x_c lookup is a binary search over the row's columns in
+    // global memory (~11 dependent loads) with 1-4 warps, a shared-memory search of
+    // a column sample plus one or two loads with 8 (measured sweeps: c3 at 2 warps
+    // 10.07 ms at 16, 9.61 at 64-100; c4 at 8 warps 18.27 at 16, 18.19 at 24-32)
     static const float cfs = getenv("WMH_INDEX_CF") ? (float)atof(getenv("WMH_INDEX_CF")) : 0.f;
     p.cf_dense = cfs > 0 ? cfs : 2.f;
     p.cf_smem = cfs > 0 ? cfs : 3.f;
-    p.cf_global = cfs > 0 ? cfs : 16.f;
+    p.cf_global = cfs > 0 ? cfs : (nw == 8 ? 24.f : 64.f);
     p.sig = a.sig;
     p.n_sat = a.n_sat;
     p.row_ctr = ctr;
@@ -1086,11 +1096,6 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
         if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(oscr, a.stream); cudaFreeAsync(ctr, a.stream); return cuda_fail(cudaGetLastError(), "index order"); }
         p.perm = perm;
     }
-    // warps per row: >= 2; keep <= ~128 KiB of h[] per SM at 64 resident warps
-    static const int nw_env = getenv("WMH_INDEX_NW") ? atoi(getenv("WMH_INDEX_NW")) : 0;
-    int nw = 2;
-    while (nw < 8 && (uint64_t)(64 / nw) * a.k * 4 > (128u << 10)) nw *= 2;
-    if (nw_env == 1 || nw_env == 2 || nw_env == 4 || nw_env == 8) nw = nw_env;
     const int wb = weight_bytes(a.rows);
     if (a.sig_bytes == 1) st = csr ? ix_launch_w<1, true>(p, nw, wb, a.stream) : ix_launch_w<1, false>(p, nw, wb, a.stream);
     else st = csr ? ix_launch_w<2, true>(p, nw, wb, a.stream) : ix_launch_w<2, false>(p, nw, wb, a.stream);

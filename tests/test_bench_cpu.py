@@ -94,3 +94,15 @@ def test_tile_need_rate_is_the_mean_tile_column_max_over_M():
     want = np.mean([x[a:a + 64].max(axis=0).astype(np.int64).sum() / M for a in (0, 64, 128)])
     got = bench.tile_need_rate(None, datagen.Dense(x), 130, 64, M)
     assert got == pytest.approx(want, rel=1e-12)
+
+
+def test_index_cf_mirrors_kernel_warp_choice():
+    """bench.py's INDEX floor recomputes the kernel's own per-row plan, so it must
+    use the kernel's fallback cost: 2 for dense rows, 64 for CSR rows hashed with
+    2-4 warps (c3: k = 1000), 24 with 8 warps (c4: k = 4000)."""
+    import bench
+    assert bench.index_cf(1000, False) == 64.0
+    assert bench.index_cf(4000, False) == 24.0
+    assert bench.index_cf(4000, True) == 2.0
+    assert bench.index_cf(1024, False) == 64.0 and bench.index_cf(1025, False) == 64.0   # 4 warps
+    assert bench.index_cf(2049, False) == 24.0
