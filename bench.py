@@ -674,24 +674,31 @@ def roofline_bitslice(x_sum, M, cfg, kern_s, n_sm, sm_mhz, in_bytes, out_bytes, 
 def index_epochs(T: int):
     """The index kernel's nested epoch boundaries for horizon T (hash_index.cu index_epochs)."""
     B, b = [], 32
-    while b < T and len(B) < 9:
+    x2max = int(os.environ.get("WMH_INDEX_X2MAX", "512"))
+    while b < T and len(B) < 13:
         B.append(b)
-        b *= 2 if b < 512 else 4
+        b *= 2 if b < x2max else 4
     if B and 2 * T < 3 * B[-1]:
         B.pop()
     return B + [T]
 
 
-def index_cf(k: int, dense: bool) -> float:
+def index_cf(k: int, dense: bool, dim: int = 1 << 30) -> float:
     """The plan's fallback-draw cost the kernel uses (hash_index.cu index_rows):
-    2 for dense rows; CSR rows 24 with 8 warps per row, else 64 (warps per row:
-    2, doubled while 64/nw rows' h[k] would exceed 128 KiB)."""
+    2 for dense rows; CSR rows with 8 warps per row 6 when the row's column bitmap
+    fits the range buffers (ceil(dim/32) + its uint16 first-column index + the
+    uint16 hash list within 2*2048 + 33 words: dim <= ~66,000), else 24; with
+    fewer warps 64 (warps per row: 2, doubled while 64/nw rows' h[k] would exceed
+    128 KiB)."""
     if dense:
         return 2.0
     nw = 2
     while nw < 8 and (64 // nw) * k * 4 > (128 << 10):
         nw *= 2
-    return 24.0 if nw == 8 else 64.0
+    if nw < 8:
+        return 64.0
+    bmw = (dim + 31) // 32
+    return 6.0 if bmw + (bmw + 1) // 2 + 1024 <= 2 * 2048 + 33 else 24.0
 
 
 def index_plan(s: np.ndarray, k: int, cap: int, B, cf: float) -> np.ndarray:
@@ -711,7 +718,7 @@ def roofline_index(x_sum, nnz, M, cfg, T, kern_s, in_bytes, out_bytes, peaks, dr
     row, T_x the kernel's own per-row horizon) + two 4 B range bounds per nonzero."""
     s = x_sum.astype(np.float64) / M
     live = s > 0
-    Tx = index_plan(s[live], cfg.k, cfg.cap, index_epochs(int(T)), index_cf(cfg.k, dense))
+    Tx = index_plan(s[live], cfg.k, cfg.cap, index_epochs(int(T)), index_cf(cfg.k, dense, cfg.dim))
     entries = float(cfg.k * (Tx * s[live]).sum())
     algo_bytes = in_bytes + out_bytes + 4.0 * entries + 8.0 * nnz
     hbm = peaks.get("hbm_gbs", 6650.0)

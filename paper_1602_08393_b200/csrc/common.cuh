@@ -181,7 +181,7 @@ uint32_t index_k_max();
 bool index_feasible(const wmh_layout *L, uint32_t k, uint32_t cap, uint32_t horizon);
 // The index of one call, reusable by several row batches of the same (layout,
 // seed, k, cap): built on a.stream, freed stream-ordered.
-constexpr int IX_MAXE = 10;
+constexpr int IX_MAXE = 14;
 struct IxEpochs {
     int E;
     uint32_t B[IX_MAXE + 1];                   // B[0] = 0, epoch e holds t < B[e + 1]

@@ -264,6 +264,8 @@ struct IxParams {
     uint32_t k, cap;
     int capn;                    // CSR rows with nnz <= capn stage their columns in shared memory
     float cf_dense, cf_smem, cf_global;   // cost of one fallback draw / one index entry
+    float cf_bitmap;             // ... with the row's column bitmap in shared memory (8 warps)
+    int bm_words;                // 8 warps, unstaged CSR rows: ceil(D / 32) when the bitmap fits, else 0
     void *sig;
     unsigned long long *n_sat;
     unsigned long long *row_ctr;
@@ -273,16 +275,25 @@ struct IxParams {
 
 // x_c of the current row: dense byte, or a lower_bound over the CSR slice
 // (its columns staged in shared memory when the row is short enough).
-// x_c of the row: dense -> direct; CSR -> binary search of c among the row's
-// columns, in shared memory when staged (scol), else first over the staged
-// sample samp[i] = col[i * sd] (ns entries) and then among the <= sd - 1
-// columns of one block in global memory (one or two cache lines)
+// x_c of the row: dense -> direct; CSR -> with the row's column bitmap bm[]
+// (bit c set iff c is a column of the row) and pre[w] = the index of the first
+// column in bitmap word w, one shared load plus, for a column of the row, its
+// rank; else binary search of c among the row's columns, in shared memory when
+// staged (scol), else first over the staged sample samp[i] = col[i * sd] (ns
+// entries) and then among the <= sd - 1 columns of one block in global memory
+// (one or two cache lines)
 template <bool CSR, typename W>
 __device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const W *xrow, const uint32_t *scol,
                                              int64_t e0, int n, uint32_t c, const uint32_t *samp = nullptr,
-                                             int ns = 0, int sd = 1) {
+                                             int ns = 0, int sd = 1, const uint32_t *bm = nullptr,
+                                             const uint16_t *pre = nullptr) {
     const W *val = reinterpret_cast<const W *>(p.val);
     if (!CSR) return scol ? (uint32_t)reinterpret_cast<const W *>(scol)[c] : (uint32_t)__ldg(xrow + c);
+    if (bm) {                                    // the row's column bitmap: one shared load decides
+        const uint32_t w = bm[c >> 5], b = c & 31u;    // x_c = 0 (most draws); else the rank of c
+        if (!((w >> b) & 1u)) return 0u;               // among the row's columns gives its weight
+        return (uint32_t)__ldg(val + e0 + pre[c >> 5] + __popc(w & ((1u << b) - 1u)));
+    }
     int lo = 0, hi = n;
     if (!scol && samp) {
         int a = 0, b = ns;                       // first i with samp[i] >= c
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(256) ix_order_count(const IxParams p, uint8_t 
             for (int64_t i = lane; i < p.D; i += 32) xs += __ldg(x + i);
         }
         for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xFFFFFFFFu, xs, o);
-        const int e = xs ? ix_plan(p, (float)((double)xs / (double)p.M), CSR ? p.cf_global : p.cf_dense) : 0;
+        const int e = xs ? ix_plan(p, (float)((double)xs / (double)p.M), CSR ? (p.bm_words ? p.cf_bitmap : p.cf_global) : p.cf_dense) : 0;
         if (lane == 0) {
             row_epoch[r] = (uint8_t)e;
             atomicAdd(cnt + e, 1u);
@@ -485,7 +496,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
             plan |= 128u;
         } else {
             const float s = (float)((double)xs / (double)p.M);
-            const int e = ix_plan(p, s, CSR ? (staged ? p.cf_smem : p.cf_global) : p.cf_dense);
+            const int e = ix_plan(p, s, CSR ? (staged ? p.cf_smem : (p.bm_words && n < 65536) ? p.cf_bitmap : p.cf_global) : p.cf_dense);
             plan |= (uint32_t)e;
             const uint32_t T = p.ep.B[e + 1];
             const uint32_t *pe = p.pos + (uint64_t)e * p.M;
@@ -593,16 +604,37 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                 //      now); each warp keeps IX_FB of them in flight, lane = draw
                 //      (IX_FB independent lookups per lane), refilling from the list
                 const uint32_t *scol = staged ? scol_buf : nullptr;
-                uint32_t *list = ra;
+                using list_t = typename std::conditional<NW == 8, uint16_t, uint32_t>::type;   // k < 2^16
+                list_t *list = reinterpret_cast<list_t *>(ra);
                 // 8 warps (large k: many fallback hashes per row) on an unstaged CSR
-                // row: a sample of its columns in rp[] (free after phase 2) turns the
-                // ~11 dependent global loads of each lookup into shared-memory steps
-                // and one or two global ones (c4: 19.9 -> 18.9 ms; with fewer warps
-                // the extra code cost more than it saved, c3 10.0 -> 11.0 ms)
-                const uint32_t *samp = nullptr;
+                // row: the row's column bitmap (bit c of bm[] set iff x_c > 0) and the
+                // index of the first column of each bitmap word in ra[] (free after
+                // phase 2), so most lookups are one shared load (x_c = 0) and the rest
+                // a rank plus one global load of the weight; when the bitmap does not
+                // fit, a sample of the columns in rp[] turns the ~11 dependent global
+                // loads of each lookup into shared-memory steps and one or two global
+                // ones (c4: 19.9 -> 18.9 ms; with fewer warps the extra code cost more
+                // than it saved, c3 10.0 -> 11.0 ms)
+                const uint32_t *samp = nullptr, *bm = nullptr;
+                const uint16_t *pre = nullptr;
                 int ns = 0, sd = 1;
                 if constexpr (CSR && NW == 8) {
-                    if (!staged) {
+                    if (!staged && p.bm_words && n < 65536) {
+                        const int bmw = p.bm_words;
+                        uint32_t *bmw_s = ra;
+                        uint16_t *pre_s = reinterpret_cast<uint16_t *>(ra + bmw);
+                        for (int i = threadIdx.x; i < bmw; i += NT) bmw_s[i] = 0u;
+                        __syncthreads();
+                        for (int i = threadIdx.x; i < n; i += NT) {
+                            const uint32_t c = (uint32_t)__ldg(p.col + e0 + i);
+                            atomicOr(bmw_s + (c >> 5), 1u << (c & 31u));
+                            // columns strictly ascending: the first of its word sets pre[]
+                            if (i == 0 || ((uint32_t)__ldg(p.col + e0 + i - 1) >> 5) != (c >> 5)) pre_s[c >> 5] = (uint16_t)i;
+                        }
+                        bm = bmw_s;
+                        pre = pre_s;
+                        list = reinterpret_cast<list_t *>(ra + bmw + ((bmw + 1) >> 1));
+                    } else if (!staged) {
                         sd = (n + CAPR - 1) / CAPR;
                         ns = (n + sd - 1) / sd;
                         for (int i = threadIdx.x; i < ns; i += NT) rp[i] = (uint32_t)__ldg(p.col + e0 + (int64_t)i * sd);
@@ -620,7 +652,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                         if (lane == 0 && m) base = atomicAdd(&s_nu, (uint32_t)__popc(m));
                         base = __shfl_sync(FULL, base, 0);
                         const uint32_t slot = base + __popc(m & (lanemask_le >> 1));
-                        if (need && slot < (uint32_t)CAPR) list[slot] = jl;
+                        if (need && slot < (uint32_t)CAPR) list[slot] = (list_t)jl;
                     }
                     __syncthreads();
                     const uint32_t U = min(s_nu, (uint32_t)CAPR);
@@ -668,7 +700,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
 #pragma unroll
                         for (int q = 0; q < IX_FB; q++) {
                             if (!((live >> q) & 1u)) continue;
-                            const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q], samp, ns, sd);
+                            const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q], samp, ns, sd, bm, pre);
                             const unsigned gm = __ballot_sync(FULL, g);
                             bool done = false;
                             if (gm) {
@@ -728,7 +760,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                             }
 #pragma unroll
                             for (int q = 0; q < IX_FB; q++) {
-                                const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q], samp, ns, sd);
+                                const bool g = off[q] != 0xFFFFFFFFu && off[q] < ix_row_x<CSR, W>(p, xrow, scol, e0, n, c[q], samp, ns, sd, bm, pre);
                                 const unsigned gm = __ballot_sync(FULL, g);
                                 if (gm) {
                                     if (lane == 0) h[jq[q]] = t0 + __ffs(gm) - 1;
@@ -841,7 +873,8 @@ static IxEpochs index_epochs(uint32_t T) {
     ep.B[0] = 0;
     int E = 0;
     // x2 steps up to 512 draws (dense rows at s ~ 0.05 stop there), x4 beyond
-    for (uint64_t b = 32; b < T && E < IX_MAXE - 1; b *= (b < 512 ? 2 : 4)) ep.B[++E] = (uint32_t)b;
+    static const uint64_t x2max = getenv("WMH_INDEX_X2MAX") ? (uint64_t)atoll(getenv("WMH_INDEX_X2MAX")) : 512;
+    for (uint64_t b = 32; b < T && E < IX_MAXE - 1; b *= (b < x2max ? 2 : 4)) ep.B[++E] = (uint32_t)b;
     // a last step shorter than half the previous boundary is merged into it
     if (E > 0 && (uint64_t)T * 2 < (uint64_t)ep.B[E] * 3) E--;
     ep.B[++E] = T;
@@ -1051,6 +1084,17 @@ wmh_status index_rows(const HashArgs &a, const IndexBuilt &ix) {
     p.cf_dense = cfs > 0 ? cfs : 2.f;
     p.cf_smem = cfs > 0 ? cfs : 3.f;
     p.cf_global = cfs > 0 ? cfs : (nw == 8 ? 24.f : 64.f);
+    // 8 warps, CSR: the row's column bitmap (ceil(D/32) words) + the first-column
+    // index per word (uint16) + the uint16 hash list must fit the 2*CAPR + 33 words
+    // of the range buffers (D <= ~66,000); WMH_INDEX_BITMAP=0 turns it off
+    static const int bm_env = getenv("WMH_INDEX_BITMAP") ? atoi(getenv("WMH_INDEX_BITMAP")) : 1;
+    static const float cfb = getenv("WMH_INDEX_CF_BM") ? (float)atof(getenv("WMH_INDEX_CF_BM")) : 0.f;
+    {
+        constexpr int64_t capr8 = 8 * 32 * 8;
+        const int64_t bmw = (a.rows.dim + 31) / 32;
+        p.bm_words = (csr && nw == 8 && bm_env && bmw + (bmw + 1) / 2 + capr8 / 2 <= 2 * capr8 + 33) ? (int)bmw : 0;
+    }
+    p.cf_bitmap = cfs > 0 ? cfs : cfb > 0 ? cfb : 6.f;
     p.sig = a.sig;
     p.n_sat = a.n_sat;
     p.row_ctr = ctr;

@@ -99,10 +99,13 @@ def test_tile_need_rate_is_the_mean_tile_column_max_over_M():
 def test_index_cf_mirrors_kernel_warp_choice():
     """bench.py's INDEX floor recomputes the kernel's own per-row plan, so it must
     use the kernel's fallback cost: 2 for dense rows, 64 for CSR rows hashed with
-    2-4 warps (c3: k = 1000), 24 with 8 warps (c4: k = 4000)."""
+    2-4 warps (c3: k = 1000), with 8 warps (c4: k = 4000) 6 when the row's column
+    bitmap fits shared memory (dim <= ~66,000), else 24."""
     import bench
     assert bench.index_cf(1000, False) == 64.0
-    assert bench.index_cf(4000, False) == 24.0
+    assert bench.index_cf(4000, False) == 24.0                       # dim too wide for the bitmap
+    assert bench.index_cf(4000, False, 65536) == 6.0                 # c4: the bitmap
+    assert bench.index_cf(4000, False, 66240) == 6.0 and bench.index_cf(4000, False, 66241) == 24.0
     assert bench.index_cf(4000, True) == 2.0
     assert bench.index_cf(1024, False) == 64.0 and bench.index_cf(1025, False) == 64.0   # 4 warps
-    assert bench.index_cf(2049, False) == 24.0
+    assert bench.index_cf(2049, False) == 24.0 and bench.index_cf(2049, False, 1000) == 6.0
