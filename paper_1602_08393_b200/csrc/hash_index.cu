@@ -292,7 +292,9 @@ __device__ __forceinline__ uint32_t ix_row_x(const IxParams &p, const W *xrow, c
     if (bm) {                                    // the row's column bitmap: one shared load decides
         const uint32_t w = bm[c >> 5], b = c & 31u;    // x_c = 0 (most draws); else the rank of c
         if (!((w >> b) & 1u)) return 0u;               // among the row's columns gives its weight
-        return (uint32_t)__ldg(val + e0 + pre[c >> 5] + __popc(w & ((1u << b) - 1u)));
+        const uint32_t rk = pre[c >> 5] + __popc(w & ((1u << b) - 1u));
+        WMH_DASSERT(rk < (uint32_t)n && (uint32_t)__ldg(p.col + e0 + rk) == c);
+        return (uint32_t)__ldg(val + e0 + rk);
     }
     int lo = 0, hi = n;
     if (!scol && samp) {
@@ -627,6 +629,7 @@ __global__ void __maxnreg__((NW == 2 || NW == 4) ? 48 : 64) hash_index_kernel(co
                         __syncthreads();
                         for (int i = threadIdx.x; i < n; i += NT) {
                             const uint32_t c = (uint32_t)__ldg(p.col + e0 + i);
+                            WMH_DASSERT((c >> 5) < (uint32_t)bmw);
                             atomicOr(bmw_s + (c >> 5), 1u << (c & 31u));
                             // columns strictly ascending: the first of its word sets pre[]
                             if (i == 0 || ((uint32_t)__ldg(p.col + e0 + i - 1) >> 5) != (c >> 5)) pre_s[c >> 5] = (uint16_t)i;

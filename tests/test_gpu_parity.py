@@ -145,6 +145,20 @@ def test_index_horizons(wmh, name, n, k, horizon):
     _assert_sig_equal(sig, oracle_hash(L, data, cfg.seed, k, cfg.cap), f"{name}/index T={horizon}")
 
 
+@pytest.mark.parametrize("horizon", [1, 0])
+@pytest.mark.parametrize("dim", [4097, 66000, 200000])
+def test_index_8warp_fallback_lookups(wmh, dim, horizon):
+    """INDEX at 8 warps per row (k = 4000) on c4-recipe CSR rows: the fallback's x_c
+    lookup through the row's column bitmap in shared memory when it fits the range
+    buffers (D = 4097 with a ragged last word, D = 66,000 the widest that fits) and
+    through the sampled binary search when it does not (D = 200,000); T = 1 makes
+    every hash take the fallback."""
+    cfg, data = datagen.make("c4", n_rows=24, dim=dim)
+    sig, L, _ = _run(wmh, data, cfg, 4000, cfg.cap, cfg.sig_bytes, "index", fixed_bound=cfg.fixed_bound,
+                     horizon=horizon)
+    _assert_sig_equal(sig, oracle_hash(L, data, cfg.seed, 4000, cfg.cap), f"c4 D={dim} index T={horizon}")
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_hash_edge_cases_dense(wmh, algo):
     """Empty rows saturate (reading R12), full-green rows give 1, tiny caps
